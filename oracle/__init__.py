@@ -1,0 +1,200 @@
+"""oracle/ -- TEST INFRASTRUCTURE ONLY (see sv_oracle.c header).
+
+Python face of the plain complex128 CPU oracle.  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference` legs
+may import this package; the product package never does.
+
+  run(circuit)           level 1: gate-by-gate in-place update (PAPER.md
+                         L236-241), C + OpenMP, complex128
+  kron_unitary(n, gates) level 2: every gate padded to a dense 2^n x 2^n
+                         matrix and multiplied in order,
+                         numpy, n <= 8 -- the "enormously wasteful" baseline
+  gate_matrix(...)       the oracle's own gate table (sv_oracle.c)
+  compare(psi, ref)      max |delta|, fidelity, norms
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import time
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sv_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+KINDS = {"h": 0, "x": 1, "y": 2, "z": 3, "s": 4, "t": 5, "sx": 6, "sy": 7, "sw": 8,
+         "cz": 9, "cnot": 10, "swap": 11, "cphase": 12, "fsim": 13, "u1": 14, "u2": 15}
+
+
+class _Gate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("adjoint", ctypes.c_int32),
+                ("q0", ctypes.c_int32), ("q1", ctypes.c_int32),
+                ("theta", ctypes.c_double), ("phi", ctypes.c_double),
+                ("m", ctypes.POINTER(ctypes.c_double))]
+
+
+def build(force: bool = False) -> str:
+    """Compile sv_oracle.c (plain C, -O2, OpenMP) in-tree."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-fopenmp",
+               "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        L.oracle_gate_matrix.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]
+        L.oracle_run.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p,
+                                 ctypes.POINTER(_Gate), ctypes.c_int64, ctypes.c_int]
+        L.oracle_apply.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(_Gate),
+                                   ctypes.c_int64, ctypes.c_int]
+        L.oracle_norm.argtypes = [ctypes.c_int, ctypes.c_void_p]
+        L.oracle_norm.restype = ctypes.c_double
+        _lib = L
+    return _lib
+
+
+def _angle(a):
+    num, den = a
+    return float(num) * np.pi / float(den)
+
+
+def _split(name):
+    if name.endswith("_dg"):
+        return name[:-3], 1
+    return name, 0
+
+
+def _marshal(gates):
+    arr = (_Gate * max(1, len(gates)))()
+    keep = []
+    for i, (name, qs, p) in enumerate(gates):
+        base, adj = _split(name)
+        g = arr[i]
+        g.kind = KINDS[base]
+        g.adjoint = adj
+        g.q0 = qs[0]
+        g.q1 = qs[1] if len(qs) > 1 else -1
+        g.theta = g.phi = 0.0
+        if base == "cphase":
+            g.phi = _angle(p[0])
+        elif base == "fsim":
+            g.theta, g.phi = _angle(p[0]), _angle(p[1])
+        if base in ("u1", "u2"):
+            m = (ctypes.c_double * len(p))(*p)
+            keep.append(m)
+            g.m = m
+        else:
+            g.m = None
+    return arr, keep
+
+
+def gate_matrix(name: str, params: tuple = ()) -> np.ndarray:
+    """The oracle's matrix for one gate (first-listed qubit = MSB)."""
+    base, adj = _split(name)
+    theta = phi = 0.0
+    if base == "cphase":
+        phi = _angle(params[0])
+    elif base == "fsim":
+        theta, phi = _angle(params[0]), _angle(params[1])
+    m = (ctypes.c_double * 32)(*(params if base in ("u1", "u2") else ()))
+    out = (ctypes.c_double * 32)()
+    d = lib().oracle_gate_matrix(KINDS[base], adj, theta, phi, m, out)
+    if d < 0:
+        raise ValueError(name)
+    a = np.array(out[: 2 * d * d]).reshape(d, d, 2)
+    return a[..., 0] + 1j * a[..., 1]
+
+
+def apply(n: int, psi: np.ndarray, gates, nthreads: int = 0) -> np.ndarray:
+    """psi <- C psi in place (complex128, length 2^n)."""
+    assert psi.dtype == np.complex128 and psi.size == 1 << n and psi.flags.c_contiguous
+    arr, keep = _marshal(gates)
+    rc = lib().oracle_apply(n, psi.ctypes.data, arr, len(gates), nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle: bad gate {-rc - 1}")
+    return psi
+
+
+def run(circuit, nthreads: int = 0, gates=None, x0=None) -> np.ndarray:
+    """Level 1: psi = U_G ... U_1 e_{x0} (complex128)."""
+    n = circuit.n
+    x0 = circuit.x0 if x0 is None else x0
+    gates = circuit.gates if gates is None else gates
+    psi = np.empty(1 << n, dtype=np.complex128)
+    arr, keep = _marshal(gates)
+    rc = lib().oracle_run(n, x0, psi.ctypes.data, arr, len(gates), nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle: rc={rc}")
+    return psi
+
+
+def norm(psi: np.ndarray) -> float:
+    n = int(psi.size).bit_length() - 1
+    return lib().oracle_norm(n, np.ascontiguousarray(psi, dtype=np.complex128).ctypes.data)
+
+
+def padded(n: int, name: str, qs, params=()) -> np.ndarray:
+    """Level 2 building block: gate padded to 2^n x 2^n by its definition
+    M[i][j] = U[l(i)][l(j)] if i, j agree off the gate's bits, else 0
+    (PAPER.md L230-233)."""
+    U = gate_matrix(name, params)
+    q = len(qs)
+    N = 1 << n
+    idx = np.arange(N)
+    loc = np.zeros(N, dtype=np.int64)
+    for i, qq in enumerate(qs):
+        loc |= ((idx >> qq) & 1) << (q - 1 - i)
+    mask = 0
+    for qq in qs:
+        mask |= 1 << qq
+    off = idx & ~mask
+    same = off[:, None] == off[None, :]
+    return np.where(same, U[loc[:, None], loc[None, :]], 0)
+
+
+def kron_unitary(n: int, gates) -> np.ndarray:
+    """Level 2 (n <= 8): the whole circuit as one dense matrix."""
+    assert n <= 8
+    M = np.eye(1 << n, dtype=np.complex128)
+    for name, qs, p in gates:
+        M = padded(n, name, qs, p) @ M
+    return M
+
+
+def compare(psi: np.ndarray, ref: np.ndarray, chunk: int = 1 << 26) -> dict:
+    """max_abs, fidelity F = |<ref|psi>|^2/(|ref|^2|psi|^2),
+    both norms; streamed in fixed-order chunks, fp64."""
+    assert psi.size == ref.size
+    max_abs = 0.0
+    ov = 0j
+    n1 = n2 = 0.0
+    for s in range(0, psi.size, chunk):
+        a = np.asarray(psi[s:s + chunk], dtype=np.complex128)
+        b = np.asarray(ref[s:s + chunk], dtype=np.complex128)
+        max_abs = max(max_abs, float(np.max(np.abs(a - b))) if a.size else 0.0)
+        ov += np.vdot(b, a)
+        n1 += float(np.vdot(a, a).real)
+        n2 += float(np.vdot(b, b).real)
+    fid = abs(ov) ** 2 / (n1 * n2) if n1 > 0 and n2 > 0 else 0.0
+    n = int(psi.size).bit_length() - 1
+    return {"max_abs": max_abs, "fidelity": fid, "norm_gpu": n1, "norm_ref": n2,
+            "max_abs_rms": max_abs * 2 ** (n / 2)}
+
+
+def timed_run(circuit, nthreads: int = 0, gates=None):
+    t0 = time.perf_counter()
+    psi = run(circuit, nthreads, gates)
+    return psi, time.perf_counter() - t0

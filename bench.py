@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""bench.py -- fused-gate state-vector update throughput on B200.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0.  A "step" is one whole-circuit simulation through the
+C ABI: sv_set_basis(|0..0>) + sv_apply_circuit(all gates of the workload)
+(planning included), i.e. one pass of every SURVEY.md 8(a) row.
+
+Workload at N=1: BASELINE.json configs[1] = c2, the 30-qubit 5x6-grid random
+circuit (20 cycles, sqrt X/Y/W + fSim(pi/2, pi/6)), complex64 state (8 GiB,
+far larger than the 126 MB L2, so no flush is needed between steps).
+
+metric/value: BASELINE.json's metric "fused-gate state-vector update GB/s".
+value is GATE-EQUIVALENT GB/s = gates x 16 B x 2^n / (sec per circuit), the
+bandwidth a one-pass-per-gate complex64 simulator would need to match this
+time (BASELINE.md "Derived context" defines the same quantity for the
+paper's CPU numbers).  It is whole-job (all ranks) and inversely
+proportional to sec/circuit, also reported.  The per-pass HBM fraction of
+peak is the `roofline` object (dominant kernel: the fused tile pass).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused-gate state-vector update GB/s (% of HBM peak); sec/circuit at n=30–37"
+UNIT = "GB/s (gate-equivalent)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--kmax", type=int, default=0)
+    ap.add_argument("--budget", type=int, default=0)
+    ap.add_argument("--tile-bits", type=int, default=0)
+    ap.add_argument("--low-bits", type=int, default=0)
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-gates", type=int, default=24, help="cpu_baseline sample size (gates)")
+    ap.add_argument("--sweep", default="", help="comma list of budgets to sweep (extra output lines to stderr)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+def workload(cfg, world):
+    from inputs import circuits as C
+    if world == 1:
+        if cfg.startswith("c"):
+            return C.config(int(cfg[1:]))
+        return C.weak_ladder(int(cfg))
+    # weak scaling: 2^30 amplitudes per GPU, same circuit family as c2
+    g = world.bit_length() - 1
+    shapes = {30: (5, 6, 0), 31: (5, 7, 4), 32: (4, 8, 0), 33: (5, 7, 2)}
+    R, Cc, rm = shapes[30 + g]
+    return C.grid_circuit(f"weak{30 + g}", R, Cc, rm, 20, "fsim", 2)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.rows = []
+        self.stop = threading.Event()
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the tile pass from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "tile_pass_traffic.json")
+    try:
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def oracle_sample(circ, ngates, threads):
+    """Time the CPU oracle (as it stands) on the first `ngates` gates of circ."""
+    import numpy as np
+    import oracle
+    n = circ.n
+    psi = np.empty(1 << n, dtype=np.complex128)
+    lib = oracle.lib()
+    arr, keep = oracle._marshal(circ.gates[:ngates])
+    t0 = time.perf_counter()
+    lib.oracle_run(n, circ.x0, psi.ctypes.data, arr, ngates, threads)
+    t = time.perf_counter() - t0
+    del psi
+    return t
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, circ):
+    """`--impl reference`: the CPU oracle (the deliberately slow, plain
+    complex128 program of oracle/) on the host cores, on bounded samples."""
+    import numpy as np
+    import oracle
+    cores = cpu_cores()
+    n = circ.n
+    gpp = 4                                  # gates per step (bounded sample)
+    psi = np.empty(1 << n, dtype=np.complex128)
+    lib = oracle.lib()
+    psi[:] = 0
+    psi[circ.x0] = 1
+    G = len(circ.gates)
+    pos = 0
+
+    def step():
+        nonlocal pos
+        gs = [circ.gates[(pos + i) % G] for i in range(gpp)]
+        pos += gpp
+        arr, keep = oracle._marshal(gs)
+        lib.oracle_apply(n, psi.ctypes.data, arr, gpp, cores)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    t = time.perf_counter() - t0
+    per_gate = t / (args.steps * gpp)
+    sec_circ = per_gate * G
+    value = G * 16 * (1 << n) / sec_circ / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE.json configs[1] circuit)",
+            "config": {"workload": circ.name, "n": n, "gates": G, "state": "complex128 (oracle)",
+                       "step": f"{gpp} gates of the circuit, gate by gate", "l2": "state 16 GiB >> L2"},
+            "sec_per_circuit": sec_circ,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} steps x {gpp} gates of {circ.name} (n={n}), complex128, "
+                                       f"{cores} OpenMP threads; sec/circuit extrapolated x{G}/gate"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    circ = workload(args.config, world)
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, workload(args.config, 1))
+        return
+
+    import numpy as np
+    import torch
+    import paper_2008_00216_b200 as stv
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        uid = [stv.nccl_unique_id() if rank == 0 else None]
+        td.broadcast_object_list(uid, src=0)
+        dist = {"rank": rank, "world": world, "uid": uid[0]}
+    stv.lib()
+    n = circ.n
+    st = stv.State(n, args.dtype, dist=dist)
+    arr, keep = stv.marshal(circ.gates)
+    opts = stv.options(kmax=args.kmax, tile_bits=args.tile_bits, low_bits=args.low_bits, budget=args.budget,
+                       flags=args.flags, profile=True)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def one_step():
+        st.set_basis(0)
+        st.apply_marshalled(arr, len(circ.gates), opts)
+
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    barrier()
+    tile_ms = 0.0
+    tile_launches = 0
+    launches = 0
+    plan_ms = []
+    kinds = {}
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+            s = st.stats()
+            tile_ms += s["pass_ms"]["tile_low"] + s["pass_ms"]["tile_high"]
+            tile_launches += s["n_pass"]["tile_low"] + s["n_pass"]["tile_high"]
+            launches += s["n_kernels"] + 1           # + the init kernel of set_basis
+            plan_ms.append(s["plan_ms"])
+            kinds = s
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    sec = ms / 1e3
+    G = len(circ.gates)
+    value = G * 16 * (1 << n) / sec / 1e9        # gate-equivalent GB/s, whole job
+    esz = 8 if args.dtype == "c64" else 16
+    n_local = n - (world.bit_length() - 1)
+    tile_bytes = 2 * esz * (1 << n_local)        # algorithmic R+W bytes per tile-pass launch
+    hbm, peak_kind = peaks()
+    achieved = tile_bytes / (tile_ms / max(1, tile_launches) / 1e3) / 1e9 if tile_launches else None
+
+    # e2e: host gate list in, full state vector out (pinned host memory)
+    e2e = None
+    if args.e2e_steps > 0:
+        host = torch.empty((1 << n_local) * esz, dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        ee0 = torch.cuda.Event(enable_timing=True)
+        ee1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        ee0.record(stream)
+        for _ in range(args.e2e_steps):
+            st.set_basis(0)
+            st.apply(circ.gates, kmax=args.kmax, tile_bits=args.tile_bits, low_bits=args.low_bits,
+                     budget=args.budget, flags=args.flags)
+            if world == 1:
+                st.read_state(0, 1 << n, out=hv.ctypes.data)
+        ee1.record(stream)
+        barrier()
+        ems = ee0.elapsed_time(ee1) / args.e2e_steps
+        h2d = int(st.stats().get("h2d_bytes", 0)) or None
+        e2e = {"value": G * 16 * (1 << n) / (ems / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d if h2d is not None else 0,
+               "d2h_bytes_per_step": (esz << n) if world == 1 else 0,
+               "ms_per_step": ems,
+               "what": "host gate list -> sv_apply_circuit -> sv_read_state of all 2^n amplitudes into pinned host memory"}
+        del host
+
+    if rank != 0:
+        st.close()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        ng = args.oracle_gates
+        t = oracle_sample(circ, ng, cpu_cores())
+        cpu = {"value": ng * 16 * (1 << n) / t / 1e9, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"first {ng} of {G} gates of {circ.name} (n={n}), complex128 gate-by-gate, "
+                         f"{cpu_cores()} OpenMP threads, {t:.2f} s",
+               "sec_per_circuit_extrapolated": t / ng * G}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.dtype == "c64" else "f64",
+        "data": "synthetic (seeded BASELINE.json circuit; no dataset)",
+        "config": {"workload": circ.name, "n": n, "gates": G, "state": args.dtype,
+                   "state_bytes_per_gpu": esz << n_local, "l2": "state >> 126 MB L2 (no flush needed)",
+                   "kmax": args.kmax or 4, "budget": args.budget or 96, "tile_bits": args.tile_bits or None},
+        "sec_per_circuit": sec,
+        "passes": {k: v for k, v in kinds["n_pass"].items() if v},
+        "ops": kinds["n_ops"],
+        "plan_ms": statistics.median(plan_ms),
+        "hbm_effective_gbs": kinds["alg_bytes"] / sec / 1e9,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm if achieved else None, "traffic": ncu_traffic(),
+                     "kernel": "k_tile_pass (fused tile pass)", "peak_kind": peak_kind,
+                     "bytes_per_launch": tile_bytes, "launches": tile_launches,
+                     "avg_launch_ms": tile_ms / max(1, tile_launches)},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    st.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,647 @@
+// api.cpp -- the C ABI of include/sv.h: state object, executor (pass dispatch
+// on one CUDA stream), readout, norm, virtual shards and the NCCL partition.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "plan.h"
+
+namespace stv {
+struct GatherMap {
+    int32_t perm[64];
+    uint64_t xmask;
+    int32_t n;
+    int32_t n_local;
+    uint64_t rank_bits;
+};
+cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
+                             uint32_t mat_bytes, cudaStream_t st, int *kernels);
+cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
+                             cudaStream_t st, int *kernels);
+cudaError_t launch_cnot(bool c128, void *state, int c, int t, int n_local, cudaStream_t st, int *kernels);
+cudaError_t launch_bitswap(bool c128, void *state, int a, int b, int n_bits, cudaStream_t st, int *kernels);
+cudaError_t launch_norm(bool c128, const void *state, uint64_t N, double *part, int np, double *out, cudaStream_t st,
+                        int *kernels);
+cudaError_t launch_fill(bool c128, void *state, uint64_t N, double val, int64_t one_at, cudaStream_t st, int *kernels);
+cudaError_t launch_gather(bool c128, const void *state, const uint64_t *didx, uint64_t first, uint64_t count,
+                          const GatherMap &gm, bool out_native, void *dout, cudaStream_t st, int *kernels);
+}  // namespace stv
+
+using namespace stv;
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded at run time (the torch-bundled libnccl.so.2 is already in the
+// process when torch.distributed initialised NCCL); no link-time dependency.
+// ---------------------------------------------------------------------------
+namespace {
+typedef struct { char internal[128]; } ncclUniqueId_t;
+typedef void *ncclComm_t;
+enum { ncclInt8 = 0, ncclUint8 = 1, ncclFloat64 = 8 };
+enum { ncclSum = 0 };
+struct Nccl {
+    void *h = nullptr;
+    int (*commInitRank)(ncclComm_t *, int, ncclUniqueId_t, int) = nullptr;
+    int (*commDestroy)(ncclComm_t) = nullptr;
+    int (*send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    int (*recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    int (*groupStart)() = nullptr;
+    int (*groupEnd)() = nullptr;
+    int (*allReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*errStr)(int) = nullptr;
+    bool load() {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+        commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+        send = (decltype(send))dlsym(h, "ncclSend");
+        recv = (decltype(recv))dlsym(h, "ncclRecv");
+        groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
+        groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
+        allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+        errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+        return commInitRank && send && recv && groupStart && groupEnd && allReduce;
+    }
+};
+Nccl g_nccl;
+
+thread_local std::string g_err;
+
+sv_status fail(sv_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+}  // namespace
+
+struct sv_state {
+    int n = 0, n_global = 0, n_local = 0;
+    int rank = 0, world = 1;
+    bool virt = false;            // virtual shards (single GPU, n_global > 0)
+    sv_dtype dt = SV_C64;
+    void *buf = nullptr;
+    size_t bytes = 0;
+    bool owned = false;
+    cudaStream_t stream = nullptr;
+    bool poisoned = false;
+    int perm[64];                 // logical -> actual physical bit
+    uint64_t xmask = 0;           // over actual physical bits
+    sv_stats stats;
+    // device scratch
+    uint8_t *dblob = nullptr;
+    size_t dblob_cap = 0;
+    uint8_t *hblob = nullptr;     // pinned staging
+    size_t hblob_cap = 0;
+    double *dnorm = nullptr;      // partials + result
+    void *dstage = nullptr;       // readout staging
+    size_t dstage_cap = 0;
+    uint64_t *didx = nullptr;
+    size_t didx_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> pev;
+    // distributed
+    ncclComm_t comm = nullptr;
+    void *xbuf = nullptr;         // remap send/recv staging
+    size_t xbuf_bytes = 0;
+
+    bool c128() const { return dt == SV_C128; }
+    size_t esz() const { return dt == SV_C128 ? 16 : 8; }
+    uint64_t nloc_amps() const { return 1ull << n_local; }
+};
+
+namespace {
+const int kNormParts = 148 * 8;
+
+sv_status cuda_fail(sv_state *s, cudaError_t e, const char *where) {
+    if (s) s->poisoned = true;
+    return fail(SV_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(s, call)                                                   \
+    do {                                                              \
+        cudaError_t _e = (call);                                      \
+        if (_e != cudaSuccess) return cuda_fail((s), _e, #call);      \
+    } while (0)
+
+sv_status check_state(const sv_state *s) {
+    if (!s) return fail(SV_ERR_INVALID_ARG, "NULL state");
+    if (s->poisoned) return fail(SV_ERR_STATE, "state poisoned by an earlier CUDA/NCCL failure");
+    return SV_OK;
+}
+
+void reset_frame(sv_state *s) {
+    for (int i = 0; i < 64; ++i) s->perm[i] = i;
+    s->xmask = 0;
+}
+
+sv_status common_init(sv_state *s) {
+    CK(s, cudaMalloc((void **)&s->dnorm, sizeof(double) * (kNormParts + 1)));
+    CK(s, cudaEventCreate(&s->ev0));
+    CK(s, cudaEventCreate(&s->ev1));
+    reset_frame(s);
+    std::memset(&s->stats, 0, sizeof(s->stats));
+    return SV_OK;
+}
+
+uint64_t rank_value(const sv_state *s) { return s->virt ? 0 : (uint64_t)s->rank; }
+
+sv_status fill(sv_state *s, double val, int64_t one_at) {
+    int k = 0;
+    CK(s, launch_fill(s->c128(), s->buf, s->nloc_amps(), val, one_at, s->stream, &k));
+    CK(s, cudaStreamSynchronize(s->stream));
+    return SV_OK;
+}
+
+sv_status ensure(sv_state *s, void **p, size_t *cap, size_t need, bool pinned) {
+    if (*cap >= need) return SV_OK;
+    if (*p) {
+        if (pinned) cudaFreeHost(*p);
+        else cudaFree(*p);
+        *p = nullptr;
+        *cap = 0;
+    }
+    size_t c = std::max(need, (size_t)1 << 20);
+    cudaError_t e = pinned ? cudaMallocHost(p, c) : cudaMalloc(p, c);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return fail(SV_ERR_OUT_OF_MEMORY, std::string("scratch allocation: ") + cudaGetErrorString(e));
+    }
+    *cap = c;
+    return SV_OK;
+}
+
+// all-to-all exchange for one set of global<->local bit swaps
+sv_status dist_remap(sv_state *s, const std::vector<std::pair<int, int>> &swaps, int *kernels);
+}  // namespace
+
+extern "C" {
+
+const char *sv_last_error(void) { return g_err.c_str(); }
+const char *sv_version(void) { return "stv-b200 0.1 (sm_100a)"; }
+
+static sv_status make_state(int n, sv_dtype dt, int n_global, sv_state **out) {
+    if (!out) return fail(SV_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || n > 40) return fail(SV_ERR_INVALID_ARG, "n must be in [1, 40]");
+    if (dt != SV_C64 && dt != SV_C128) return fail(SV_ERR_INVALID_ARG, "unknown dtype");
+    if (n_global < 0 || n - n_global < (n_global ? 4 : 1)) return fail(SV_ERR_INVALID_ARG, "need at least 4 local qubits per shard");
+    sv_state *s = new sv_state();
+    s->n = n;
+    s->dt = dt;
+    s->n_global = n_global;
+    s->n_local = n - n_global;
+    *out = s;
+    return SV_OK;
+}
+
+sv_status sv_create(int n, sv_dtype dt, sv_state **out) {
+    sv_status st = make_state(n, dt, 0, out);
+    if (st) return st;
+    sv_state *s = *out;
+    s->bytes = s->esz() << n;
+    cudaError_t e = cudaMalloc(&s->buf, s->bytes);
+    if (e != cudaSuccess) {
+        delete s;
+        *out = nullptr;
+        return fail(SV_ERR_OUT_OF_MEMORY, std::string("state allocation: ") + cudaGetErrorString(e));
+    }
+    s->owned = true;
+    if ((st = common_init(s))) return st;
+    return fill(s, 0.0, 0);
+}
+
+sv_status sv_wrap(int n, sv_dtype dt, void *dev_buf, size_t bytes, void *stream, sv_state **out) {
+    sv_status st = make_state(n, dt, 0, out);
+    if (st) return st;
+    sv_state *s = *out;
+    if (!dev_buf || bytes < (s->esz() << n) || ((uintptr_t)dev_buf & 255)) {
+        delete s;
+        *out = nullptr;
+        return fail(SV_ERR_INVALID_ARG, "dev_buf NULL, too small or not 256-B aligned");
+    }
+    s->buf = dev_buf;
+    s->bytes = bytes;
+    s->stream = (cudaStream_t)stream;
+    if ((st = common_init(s))) return st;
+    return fill(s, 0.0, 0);
+}
+
+sv_status sv_create_virtual(int n, sv_dtype dt, int g, sv_state **out) {
+    if (g < 0 || g > 3) return fail(SV_ERR_INVALID_ARG, "virtual shards: g in [0, 3]");
+    sv_status st = sv_create(n, dt, out);
+    if (st) return st;
+    (*out)->n_global = g;
+    (*out)->n_local = n;     // one buffer holds all shards; the planner keeps the top g bits global
+    (*out)->virt = true;
+    return SV_OK;
+}
+
+sv_status sv_create_dist(int n, sv_dtype dt, const void *uid, int rank, int world, void *dev_buf, size_t bytes,
+                         void *stream, sv_state **out) {
+    if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world)
+        return fail(SV_ERR_INVALID_ARG, "world must be a power of two, 0 <= rank < world");
+    int g = 0;
+    while ((1 << g) < world) ++g;
+    sv_status st = make_state(n, dt, g, out);
+    if (st) return st;
+    sv_state *s = *out;
+    s->rank = rank;
+    s->world = world;
+    s->stream = (cudaStream_t)stream;
+    const size_t need = s->esz() << s->n_local;
+    if (dev_buf) {
+        if (bytes < need || ((uintptr_t)dev_buf & 255)) {
+            delete s;
+            *out = nullptr;
+            return fail(SV_ERR_INVALID_ARG, "dev_buf too small or not 256-B aligned");
+        }
+        s->buf = dev_buf;
+        s->bytes = bytes;
+    } else {
+        cudaError_t e = cudaMalloc(&s->buf, need);
+        if (e != cudaSuccess) {
+            delete s;
+            *out = nullptr;
+            return fail(SV_ERR_OUT_OF_MEMORY, "state allocation failed");
+        }
+        s->owned = true;
+        s->bytes = need;
+    }
+    if ((st = common_init(s))) return st;
+    if (world > 1) {
+        if (!g_nccl.load()) return fail(SV_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+        ncclUniqueId_t id;
+        std::memcpy(&id, uid, sizeof(id));
+        int r = g_nccl.commInitRank(&s->comm, world, id, rank);
+        if (r) return fail(SV_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+    }
+    return fill(s, 0.0, rank == 0 ? 0 : -1);
+}
+
+sv_status sv_set_basis(sv_state *s, uint64_t x) {
+    sv_status st = check_state(s);
+    if (st) return st;
+    if (s->n < 64 && x >> s->n) return fail(SV_ERR_INVALID_ARG, "basis index >= 2^n");
+    reset_frame(s);
+    const uint64_t owner = s->virt ? 0 : x >> s->n_local;
+    const int64_t at = (owner == rank_value(s)) ? (int64_t)(s->virt ? x : (x & (s->nloc_amps() - 1))) : -1;
+    return fill(s, 0.0, at);
+}
+
+sv_status sv_set_uniform(sv_state *s) {
+    sv_status st = check_state(s);
+    if (st) return st;
+    reset_frame(s);
+    return fill(s, std::ldexp(1.0, -s->n) > 0 ? std::pow(2.0, -0.5 * s->n) : 0.0, -1);
+}
+
+sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const sv_options *opt) {
+    sv_status st = check_state(s);
+    if (st) return st;
+    if (ng && !gates) return fail(SV_ERR_INVALID_ARG, "gates is NULL");
+    std::string err = validate(s->n, gates, ng);
+    if (!err.empty()) return fail(SV_ERR_INVALID_ARG, err);
+    auto t0 = std::chrono::steady_clock::now();
+    // plan in "virtual physical" bits = the state's current actual bits
+    Frame fr;
+    for (int q = 0; q < 64; ++q) fr.perm[q] = s->perm[q];
+    fr.xmask = s->xmask;
+    const uint32_t flags = opt ? opt->flags : 0;
+    std::vector<PGate> pg = to_physical(s->n, gates, ng, fr, flags);
+    PlanOptions po = resolve_options(opt, (int)s->esz(), s->virt ? s->n - s->n_global : s->n_local);
+    int sigma[64];
+    for (int v = 0; v < 64; ++v) sigma[v] = v;
+    Plan plan;
+    try {
+        plan = build_plan(s->n, s->n_global, (int)s->esz(), pg, po, sigma);
+    } catch (const std::exception &ex) {
+        return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
+    }
+    const int enc_local = s->n_local;   // virtual: the whole buffer is addressed directly
+    Encoded enc = encode(plan, enc_local, s->c128());
+    // rank bits into every pass header
+    for (uint32_t off : enc.pass_off) {
+        StvPass *hp = (StvPass *)&enc.blob[off];
+        hp->rank_bits = s->virt ? 0 : (uint64_t)s->rank << s->n_local;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    std::memset(&s->stats, 0, sizeof(s->stats));
+    s->stats.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    s->stats.alg_bytes = plan.alg_bytes;
+    s->stats.h2d_bytes = (double)enc.blob.size();
+    if ((st = ensure(s, (void **)&s->hblob, &s->hblob_cap, enc.blob.size(), true))) return st;
+    if ((st = ensure(s, (void **)&s->dblob, &s->dblob_cap, enc.blob.size(), false))) return st;
+    std::memcpy(s->hblob, enc.blob.data(), enc.blob.size());
+    CK(s, cudaEventRecord(s->ev0, s->stream));
+    CK(s, cudaMemcpyAsync(s->dblob, s->hblob, enc.blob.size(), cudaMemcpyHostToDevice, s->stream));
+    const bool prof = flags & SV_OPT_PROFILE;
+    if (prof && s->pev.size() < plan.passes.size() + 1) {
+        for (size_t i = s->pev.size(); i < plan.passes.size() + 1; ++i) {
+            cudaEvent_t e;
+            CK(s, cudaEventCreate(&e));
+            s->pev.push_back(e);
+        }
+    }
+    int kernels = 0;
+    std::vector<int> kind_of(plan.passes.size());
+    if (prof) CK(s, cudaEventRecord(s->pev[0], s->stream));
+    for (size_t i = 0; i < plan.passes.size(); ++i) {
+        const PPass &ps = plan.passes[i];
+        const StvPass *hp = (const StvPass *)&enc.blob[enc.pass_off[i]];
+        int kind = 7;
+        cudaError_t e = cudaSuccess;
+        if (ps.kind == PASS_TILE) {
+            kind = hp->h == 0 ? 1 : 2;
+            e = launch_tile_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->mat_bytes,
+                                 s->stream, &kernels);
+            for (auto &o : ps.ops) s->stats.n_ops[o.type == OP_DENSE ? 0 : o.type == OP_DIAG ? 1 : 2]++;
+        } else if (ps.kind == PASS_DIAG) {
+            kind = 3;
+            e = launch_diag_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, s->stream, &kernels);
+        } else if (ps.kind == PASS_CNOT) {
+            kind = 4;
+            int c = hp->cnot_c, t = hp->cnot_t;
+            bool run = true;
+            if (!s->virt && c >= s->n_local) {   // control on a global bit: per-rank predicate
+                run = (s->rank >> (c - s->n_local)) & 1;
+                c = -1;
+            }
+            if (run) e = launch_cnot(s->c128(), s->buf, c, t, enc_local, s->stream, &kernels);
+        } else if (ps.kind == PASS_REMAP) {
+            kind = 5;
+            if (s->virt) {
+                for (auto &sw : ps.swaps) {
+                    e = launch_bitswap(s->c128(), s->buf, sw.first, sw.second, s->n, s->stream, &kernels);
+                    if (e != cudaSuccess) break;
+                    s->stats.remap_bytes += (double)s->esz() * std::ldexp(1.0, s->n - 1) / (1 << s->n_global);
+                }
+            } else {
+                if ((st = dist_remap(s, ps.swaps, &kernels))) return st;
+            }
+        }
+        if (e != cudaSuccess) return cuda_fail(s, e, "pass launch");
+        kind_of[i] = kind;
+        s->stats.n_pass[kind]++;
+        if (prof) CK(s, cudaEventRecord(s->pev[i + 1], s->stream));
+    }
+    CK(s, cudaEventRecord(s->ev1, s->stream));
+    CK(s, cudaStreamSynchronize(s->stream));
+    float ms = 0;
+    CK(s, cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+    s->stats.run_ms = ms;
+    if (prof) {
+        for (size_t i = 0; i < plan.passes.size(); ++i) {
+            float pm = 0;
+            CK(s, cudaEventElapsedTime(&pm, s->pev[i], s->pev[i + 1]));
+            s->stats.pass_ms[kind_of[i]] += pm;
+        }
+    }
+    s->stats.n_kernels = kernels;
+    // new frame: logical -> actual
+    uint64_t xm = 0;
+    for (int v = 0; v < s->n; ++v)
+        if ((fr.xmask >> v) & 1) xm |= 1ull << sigma[v];
+    for (int q = 0; q < s->n; ++q) s->perm[q] = sigma[fr.perm[q]];
+    s->xmask = xm;
+    return SV_OK;
+}
+
+static GatherMap gather_map(const sv_state *s) {
+    GatherMap gm;
+    for (int q = 0; q < 64; ++q) gm.perm[q] = s->perm[q];
+    gm.xmask = s->xmask;
+    gm.n = s->n;
+    gm.n_local = s->virt ? s->n : s->n_local;
+    gm.rank_bits = s->virt ? 0 : (uint64_t)s->rank;
+    return gm;
+}
+
+static sv_status gather_impl(sv_state *s, const uint64_t *idx, uint64_t first, uint64_t count, bool native,
+                             void *out) {
+    sv_status st = check_state(s);
+    if (st) return st;
+    if (!count) return SV_OK;
+    if (!out) return fail(SV_ERR_INVALID_ARG, "out is NULL");
+    const uint64_t N = s->n >= 64 ? ~0ull : 1ull << s->n;
+    if (idx) {
+        for (uint64_t k = 0; k < count; ++k)
+            if (idx[k] >= N) return fail(SV_ERR_INVALID_ARG, "amplitude index " + std::to_string(idx[k]) + " >= 2^n");
+    } else if (first >= N || count > N - first) {
+        return fail(SV_ERR_INVALID_ARG, "amplitude range out of [0, 2^n)");
+    }
+    const size_t osz = native ? s->esz() : 16;
+    const uint64_t chunk = std::min<uint64_t>(count, (64ull << 20) / osz);
+    if ((st = ensure(s, &s->dstage, &s->dstage_cap, chunk * osz, false))) return st;
+    if (idx && (st = ensure(s, (void **)&s->didx, &s->didx_cap, chunk * 8, false))) return st;
+    GatherMap gm = gather_map(s);
+    int kernels = 0;
+    for (uint64_t b = 0; b < count; b += chunk) {
+        const uint64_t c = std::min(chunk, count - b);
+        if (s->world > 1) CK(s, cudaMemsetAsync(s->dstage, 0, c * osz, s->stream));
+        if (idx) CK(s, cudaMemcpyAsync(s->didx, idx + b, c * 8, cudaMemcpyHostToDevice, s->stream));
+        CK(s, launch_gather(s->c128(), s->buf, idx ? s->didx : nullptr, first + b, c, gm, native, s->dstage,
+                            s->stream, &kernels));
+        if (s->world > 1) {
+            // exactly one rank owns each amplitude; the others contribute zeros
+            const size_t nd = c * osz / 8;
+            int r = native && !s->c128()
+                        ? 1   // float sums of x + 0 are exact as well, but use doubles only
+                        : 0;
+            (void)r;
+            if (native && !s->c128()) {
+                int rr = g_nccl.allReduce(s->dstage, s->dstage, c * 2, 7 /*ncclFloat32*/, ncclSum, s->comm, s->stream);
+                if (rr) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (gather)"); }
+            } else {
+                int rr = g_nccl.allReduce(s->dstage, s->dstage, nd, ncclFloat64, ncclSum, s->comm, s->stream);
+                if (rr) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (gather)"); }
+            }
+        }
+        CK(s, cudaMemcpyAsync((uint8_t *)out + b * osz, s->dstage, c * osz, cudaMemcpyDeviceToHost, s->stream));
+    }
+    CK(s, cudaStreamSynchronize(s->stream));
+    return SV_OK;
+}
+
+sv_status sv_get_amplitudes(sv_state *s, const uint64_t *idx, uint64_t first, size_t count, double *out) {
+    return gather_impl(s, idx, first, count, false, out);
+}
+
+sv_status sv_read_state(sv_state *s, uint64_t first, uint64_t count, void *out) {
+    return gather_impl(s, nullptr, first, count, true, out);
+}
+
+sv_status sv_norm(sv_state *s, double *out) {
+    sv_status st = check_state(s);
+    if (st) return st;
+    if (!out) return fail(SV_ERR_INVALID_ARG, "out is NULL");
+    int k = 0;
+    CK(s, launch_norm(s->c128(), s->buf, s->nloc_amps(), s->dnorm, kNormParts, s->dnorm + kNormParts, s->stream, &k));
+    if (s->world > 1) {
+        int r = g_nccl.allReduce(s->dnorm + kNormParts, s->dnorm + kNormParts, 1, ncclFloat64, ncclSum, s->comm,
+                                 s->stream);
+        if (r) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (norm)"); }
+    }
+    CK(s, cudaMemcpyAsync(out, s->dnorm + kNormParts, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    CK(s, cudaStreamSynchronize(s->stream));
+    return SV_OK;
+}
+
+sv_status sv_last_run_stats(const sv_state *s, sv_stats *out) {
+    if (!s || !out) return fail(SV_ERR_INVALID_ARG, "NULL argument");
+    *out = s->stats;
+    return SV_OK;
+}
+
+sv_status sv_get_frame(const sv_state *s, int32_t *perm, uint64_t *xmask) {
+    if (!s) return fail(SV_ERR_INVALID_ARG, "NULL state");
+    if (perm) for (int q = 0; q < s->n; ++q) perm[q] = s->perm[q];
+    if (xmask) *xmask = s->xmask;
+    return SV_OK;
+}
+
+sv_status sv_plan_json(int n, int n_global, sv_dtype dt, const sv_gate *gates, size_t ng, const sv_options *opt,
+                       char *buf, size_t cap, size_t *needed) {
+    if (n < 1 || n > 40 || n_global < 0 || n - n_global < 4) return fail(SV_ERR_INVALID_ARG, "bad n / n_global");
+    std::string err = validate(n, gates, ng);
+    if (!err.empty()) return fail(SV_ERR_INVALID_ARG, err);
+    Frame fr;
+    fr.identity(n);
+    const int esz = dt == SV_C128 ? 16 : 8;
+    std::vector<PGate> pg = to_physical(n, gates, ng, fr, opt ? opt->flags : 0);
+    PlanOptions po = resolve_options(opt, esz, n - n_global);
+    int sigma[64];
+    for (int v = 0; v < 64; ++v) sigma[v] = v;
+    Plan plan;
+    try {
+        plan = build_plan(n, n_global, esz, pg, po, sigma);
+    } catch (const std::exception &ex) {
+        return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
+    }
+    // compose the final frame (logical -> actual)
+    plan.frame_out.xmask = 0;
+    for (int v = 0; v < n; ++v)
+        if ((fr.xmask >> v) & 1) plan.frame_out.xmask |= 1ull << sigma[v];
+    for (int q = 0; q < 64; ++q) plan.frame_out.perm[q] = q < n ? sigma[fr.perm[q]] : q;
+    std::string js = plan_to_json(plan);
+    if (needed) *needed = js.size() + 1;
+    if (!buf || cap < js.size() + 1) return fail(SV_ERR_INVALID_ARG, "buffer too small");
+    std::memcpy(buf, js.c_str(), js.size() + 1);
+    return SV_OK;
+}
+
+sv_status sv_remap_peers(int g, int rank, uint32_t gbits, int m, int32_t *peer) {
+    if (g < 0 || g > 10 || rank < 0 || rank >= (1 << g) || !peer || m != __builtin_popcount(gbits) ||
+        (gbits >> g))
+        return fail(SV_ERR_INVALID_ARG, "bad remap arguments");
+    // global bits gb_0 < gb_1 < ... (within the rank index) swap with local
+    // bits lb_0..lb_{m-1}: chunk c (value of the local bits) moves to the rank
+    // whose selected global bits equal c; its slot there is this rank's
+    // selected-global-bit value.
+    std::vector<int> gb;
+    for (int b = 0; b < g; ++b)
+        if ((gbits >> b) & 1) gb.push_back(b);
+    for (int c = 0; c < (1 << m); ++c) {
+        int r = rank;
+        for (int i = 0; i < m; ++i) {
+            r &= ~(1 << gb[i]);
+            r |= ((c >> i) & 1) << gb[i];
+        }
+        peer[c] = r;
+    }
+    return SV_OK;
+}
+
+sv_status sv_destroy(sv_state *s) {
+    if (!s) return SV_OK;
+    if (s->comm && g_nccl.commDestroy) g_nccl.commDestroy(s->comm);
+    if (s->owned && s->buf) cudaFree(s->buf);
+    if (s->dblob) cudaFree(s->dblob);
+    if (s->hblob) cudaFreeHost(s->hblob);
+    if (s->dnorm) cudaFree(s->dnorm);
+    if (s->dstage) cudaFree(s->dstage);
+    if (s->didx) cudaFree(s->didx);
+    if (s->xbuf) cudaFree(s->xbuf);
+    if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->ev1) cudaEventDestroy(s->ev1);
+    for (auto e : s->pev) cudaEventDestroy(e);
+    delete s;
+    return SV_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// distributed remap: pack -> grouped ncclSend/ncclRecv -> unpack, chunked
+// ---------------------------------------------------------------------------
+namespace stv {
+cudaError_t launch_pack(bool c128, const void *state, void *dst, const int *lbits, int m, uint32_t chunk,
+                        uint64_t first, uint64_t count, int n_local, bool unpack, cudaStream_t st, int *kernels);
+}
+
+namespace {
+sv_status dist_remap(sv_state *s, const std::vector<std::pair<int, int>> &swaps, int *kernels) {
+    if (s->world < 2) return SV_OK;
+    const int m = (int)swaps.size();
+    uint32_t gbits = 0;
+    int lbits[8];
+    // pairs sorted by global bit so chunk value bit i <-> global bit i-th
+    std::vector<std::pair<int, int>> sw = swaps;
+    std::sort(sw.begin(), sw.end());
+    for (int i = 0; i < m; ++i) {
+        gbits |= 1u << (sw[i].first - s->n_local);
+        lbits[i] = sw[i].second;
+    }
+    int32_t peer[256];
+    sv_status st = sv_remap_peers(s->n_global, s->rank, gbits, m, peer);
+    if (st) return st;
+    // my own chunk index: the value of my selected global bits
+    int mine = 0;
+    for (int i = 0; i < m; ++i) mine |= ((s->rank >> (sw[i].first - s->n_local)) & 1) << i;
+    const uint64_t chunk_amps = 1ull << (s->n_local - m);
+    const uint64_t piece = std::min<uint64_t>(chunk_amps, (256ull << 20) / s->esz());   // 256 MiB pieces
+    const int npeers = (1 << m) - 1;
+    const size_t need = 2ull * npeers * piece * s->esz();
+    if ((st = ensure(s, &s->xbuf, &s->xbuf_bytes, need, false))) return st;
+    uint8_t *sendb = (uint8_t *)s->xbuf, *recvb = sendb + (size_t)npeers * piece * s->esz();
+    for (uint64_t off = 0; off < chunk_amps; off += piece) {
+        const uint64_t cnt = std::min(piece, chunk_amps - off);
+        int slot = 0;
+        for (int c = 0; c < (1 << m); ++c) {
+            if (c == mine) continue;
+            cudaError_t e = launch_pack(s->c128(), s->buf, sendb + (size_t)slot * piece * s->esz(), lbits, m, c, off,
+                                        cnt, s->n_local, false, s->stream, kernels);
+            if (e != cudaSuccess) return cuda_fail(s, e, "remap pack");
+            ++slot;
+        }
+        g_nccl.groupStart();
+        slot = 0;
+        for (int c = 0; c < (1 << m); ++c) {
+            if (c == mine) continue;
+            const size_t b = cnt * s->esz();
+            int r1 = g_nccl.send(sendb + (size_t)slot * piece * s->esz(), b, ncclUint8, peer[c], s->comm, s->stream);
+            int r2 = g_nccl.recv(recvb + (size_t)slot * piece * s->esz(), b, ncclUint8, peer[c], s->comm, s->stream);
+            if (r1 || r2) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclSend/Recv (remap)"); }
+            ++slot;
+        }
+        if (g_nccl.groupEnd()) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclGroupEnd (remap)"); }
+        slot = 0;
+        for (int c = 0; c < (1 << m); ++c) {
+            if (c == mine) continue;
+            // data from peer[c] (its chunk `mine`) lands in my chunk slot c
+            cudaError_t e = launch_pack(s->c128(), s->buf, recvb + (size_t)slot * piece * s->esz(), lbits, m, c, off,
+                                        cnt, s->n_local, true, s->stream, kernels);
+            if (e != cudaSuccess) return cuda_fail(s, e, "remap unpack");
+            ++slot;
+        }
+        s->stats.remap_bytes += (double)npeers * cnt * s->esz();
+    }
+    return SV_OK;
+}
+}  // namespace

@@ -1,0 +1,750 @@
+// kernels.cu -- hand-written sm_100a kernels of the state-vector hot path.
+//
+//   k_tile_pass      SURVEY.md 8(a) a5/a6: one HBM pass applies a fused
+//                    sequence of dense k-qubit ops, diagonal-phase ops and
+//                    in-tile CNOTs to every tile.  Tiles (2^h runs of 2^L
+//                    contiguous amplitudes) are staged into shared memory by
+//                    TMA bulk copies (cp.async.bulk + mbarrier) in a 3-stage
+//                    ring on persistent CTAs, and written back by bulk stores.
+//                    Paper analog: "apply all applicable gates to a resident
+//                    cache line".
+//   k_diag_pass      a8: standalone diagonal cluster, one read pass, writes
+//                    only amplitudes whose phase != 1.
+//   k_cnot_pass      a9: CNOT as a pure permutation, touches only the half of
+//                    the state with control = 1.
+//   k_bitswap        remap of one global<->local bit pair for virtual shards.
+//   k_norm_*         a10: fp64 fixed-shape reduction.
+//   k_init_*, k_gather  a11.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pass_format.h"
+
+namespace stv {
+
+template <typename R> struct C2T;
+template <> struct C2T<float> { using T = float2; };
+template <> struct C2T<double> { using T = double2; };
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA bulk copies (sm_90+/sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    while (!mbar_try_wait(a, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst_smem)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void *dst, const void *src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t pdep64(uint64_t x, uint64_t mask) {
+    uint64_t r = 0;
+    for (uint64_t m = mask; m; m &= m - 1) {
+        if (x & 1) r |= m & (0 - m);
+        x >>= 1;
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// complex helpers and the phase application (multiply-free for quarter turns)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 cfma(float2 m, float2 x, float2 acc) {
+    acc.x = fmaf(m.x, x.x, acc.x);
+    acc.x = fmaf(-m.y, x.y, acc.x);
+    acc.y = fmaf(m.x, x.y, acc.y);
+    acc.y = fmaf(m.y, x.x, acc.y);
+    return acc;
+}
+__device__ __forceinline__ double2 cfma(double2 m, double2 x, double2 acc) {
+    acc.x = fma(m.x, x.x, acc.x);
+    acc.x = fma(-m.y, x.y, acc.x);
+    acc.y = fma(m.x, x.y, acc.y);
+    acc.y = fma(m.y, x.x, acc.y);
+    return acc;
+}
+
+__device__ __forceinline__ void phase_cs(uint64_t ph, float &c, float &s) {
+    const float x = (float)(int32_t)(uint32_t)(ph >> 32) * 4.656612873077392578125e-10f;  // 2^-31 (units of pi)
+    sincospif(x, &s, &c);
+}
+__device__ __forceinline__ void phase_cs(uint64_t ph, double &c, double &s) {
+    const double x = (double)(int64_t)ph * 1.0842021724855044340074528008699e-19;  // 2^-63
+    sincospi(x, &s, &c);
+}
+
+// amplitude *= exp(2 pi i ph / 2^64).  Quarter turns (+-1, +-i) use sign
+// flips and (re, im) swaps only -- no floating-point multiply (PAPER.md
+// L365-369, Sec. 4.1); other phases cost one complex multiply (reading A9).
+template <typename C>
+__device__ __forceinline__ C apply_phase(C a, uint64_t ph) {
+    if (ph == 0) return a;
+    if ((ph & ((1ull << 62) - 1)) == 0) {
+        const uint32_t q = (uint32_t)(ph >> 62);
+        C b;
+        if (q == 2) { b.x = -a.x; b.y = -a.y; }
+        else if (q == 1) { b.x = -a.y; b.y = a.x; }
+        else { b.x = a.y; b.y = -a.x; }
+        return b;
+    }
+    decltype(a.x) c, s;
+    phase_cs(ph, c, s);
+    C b;
+    b.x = a.x * c - a.y * s;
+    b.y = a.x * s + a.y * c;
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// diagonal-phase evaluation over a tile (shared by k_tile_pass and k_diag_pass)
+//
+// Tile-local index of the amplitudes a thread owns:
+//   i = (r << (V + 8)) | (tid << V) | e,   e < 2^V, V = 1 (c64) / 0 (c128)
+// so every thread touches 16 contiguous bytes per r.  The phase splits into
+//   per-tile constant ct + per-thread part (thread bits) + per-amplitude part
+// (e and r bits): the per-amplitude part is a precomputed quadratic table qf
+// over the <= 6 "free" bits plus a sum of <= 6 linear terms (the GPU form of
+// the paper's incremental Gray-code update).
+// ---------------------------------------------------------------------------
+struct DiagScratch {
+    uint64_t ct;
+    uint64_t pad;
+    uint64_t linp[STV_MAX_TILE_BITS + 2];
+    uint64_t qf[64];
+};
+
+// per-tile prep: linp[q] = lin[q] + sum of cross terms whose outside bit is set
+// in full_base; ct = cst + outside linear + outside quadratic terms;
+// qf[c] = in-tile pair terms among the free bits of combo c.
+template <int V>
+__device__ void diag_prep(const StvDiag *__restrict__ D, int S, uint64_t full_base, DiagScratch *sc) {
+    const int tid = threadIdx.x;
+    const uint8_t *rec = (const uint8_t *)D;
+    if (tid < S) {
+        uint64_t l = D->lin[tid];
+        const StvTerm *cr = (const StvTerm *)(rec + D->cross_off);
+        const int b = D->cross_start[tid], e = D->cross_start[tid + 1];
+        for (int k = b; k < e; ++k)
+            if ((full_base >> cr[k].b) & 1) l += cr[k].ang;
+        sc->linp[tid] = l;
+    }
+    if (tid >= 32 && tid < 64) {
+        const int lane = tid - 32;
+        uint64_t acc = 0;
+        const StvTerm *ol = (const StvTerm *)(rec + D->olin_off);
+        for (int k = lane; k < D->n_olin; k += 32)
+            if ((full_base >> ol[k].a) & 1) acc += ol[k].ang;
+        const StvTerm *oq = (const StvTerm *)(rec + D->oquad_off);
+        for (int k = lane; k < D->n_oquad; k += 32)
+            if (((full_base >> oq[k].a) & 1) && ((full_base >> oq[k].b) & 1)) acc += oq[k].ang;
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) sc->ct = D->cst + acc;
+    }
+    // free bits: F = [0, V) U [V+8, S)
+    const int nr = S > V + 8 ? S - V - 8 : 0;
+    const int nF = V + nr;
+    if (tid >= 64 && tid < 64 + (1 << nF)) {
+        const int c = tid - 64;
+        int fpos[6];
+        int m = 0;
+        for (int f = 0; f < V; ++f) fpos[m++] = f;
+        for (int f = 0; f < nr; ++f) fpos[m++] = V + 8 + f;
+        uint64_t acc = 0;
+        for (int a = 0; a < nF; ++a)
+            if ((c >> a) & 1)
+                for (int b = a + 1; b < nF; ++b)
+                    if ((c >> b) & 1) acc += D->A[fpos[a]][fpos[b]];
+        sc->qf[c] = acc;
+    }
+}
+
+// per-thread constant and the linear coefficients of the free bits
+template <int V>
+__device__ __forceinline__ void diag_thread(const StvDiag *__restrict__ D, int S, const DiagScratch *sc,
+                                            uint64_t &bt, uint64_t *lf, int &nF) {
+    const int tid = threadIdx.x;
+    const int tb_hi = min(S, V + 8);
+    const int nr = S > V + 8 ? S - V - 8 : 0;
+    nF = V + nr;
+    bt = sc->ct;
+    for (int q = V; q < tb_hi; ++q) {
+        if (!((tid >> (q - V)) & 1)) continue;
+        bt += sc->linp[q];
+        for (int p = V; p < q; ++p)
+            if ((tid >> (p - V)) & 1) bt += D->A[p][q];
+    }
+    for (int f = 0; f < nF; ++f) {
+        const int fp = f < V ? f : V + 8 + (f - V);
+        uint64_t l = sc->linp[fp];
+        for (int q = V; q < tb_hi; ++q)
+            if ((tid >> (q - V)) & 1) l += D->A[q][fp];
+        lf[f] = l;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// dense k-qubit op on a shared-memory tile (register-resident 2^k vector)
+// ---------------------------------------------------------------------------
+template <int K, typename C>
+__device__ void dense_op(C *__restrict__ tile, int S, const int *tp, const C *__restrict__ M) {
+    constexpr int D = 1 << K;
+    const uint32_t nvec = 1u << (S - K);
+    for (uint32_t v = threadIdx.x; v < nvec; v += blockDim.x) {
+        uint32_t base = v;
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+            const uint32_t lo = base & ((1u << tp[b]) - 1);
+            base = ((base >> tp[b]) << (tp[b] + 1)) | lo;
+        }
+        C x[D];
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int b = 0; b < K; ++b)
+                if ((l >> b) & 1) o |= 1u << tp[b];
+            x[l] = tile[base | o];
+        }
+        // rows: full unroll for K <= 2 (M fits in registers), else a rolled
+        // row loop so only x[] and one accumulator stay live
+#pragma unroll(K <= 2 ? D : 1)
+        for (int r = 0; r < D; ++r) {
+            C acc;
+            acc.x = 0;
+            acc.y = 0;
+            const C *Mr = M + r * D;
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc = cfma(Mr[c], x[c], acc);
+            uint32_t o = 0;
+#pragma unroll
+            for (int b = 0; b < K; ++b)
+                if ((r >> b) & 1) o |= 1u << tp[b];
+            tile[base | o] = acc;
+        }
+    }
+}
+
+template <typename C>
+__device__ void cnot_op(C *__restrict__ tile, int S, int t, int c_loc) {
+    const uint32_t npair = 1u << (S - 1);
+    for (uint32_t v = threadIdx.x; v < npair; v += blockDim.x) {
+        const uint32_t lo = v & ((1u << t) - 1);
+        const uint32_t i0 = ((v >> t) << (t + 1)) | lo;
+        if (c_loc >= 0 && !((i0 >> c_loc) & 1)) continue;
+        const uint32_t i1 = i0 | (1u << t);
+        C a = tile[i0];
+        tile[i0] = tile[i1];
+        tile[i1] = a;
+    }
+}
+
+template <int V, typename C>
+__device__ void diag_op_tile(C *__restrict__ tile, int S, const StvDiag *__restrict__ D, const DiagScratch *sc) {
+    uint64_t bt, lf[6];
+    int nF;
+    diag_thread<V>(D, S, sc, bt, lf, nF);
+    const uint32_t tsz = 1u << S;
+    const int ncombo = 1 << nF;
+    for (int c = 0; c < ncombo; ++c) {
+        const uint32_t e = c & ((1 << V) - 1), r = (uint32_t)c >> V;
+        const uint32_t i = (r << (V + 8)) | ((uint32_t)threadIdx.x << V) | e;
+        if (i >= tsz) continue;
+        uint64_t ph = bt + sc->qf[c];
+#pragma unroll
+        for (int f = 0; f < 6; ++f)
+            if (f < nF && ((c >> f) & 1)) ph += lf[f];
+        tile[i] = apply_phase(tile[i], ph);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the fused tile pass
+// ---------------------------------------------------------------------------
+constexpr int kStages = 3;
+constexpr int kHdrBytes = 1024;    // barriers, tile bases, DiagScratch
+
+template <typename R>
+__global__ void __launch_bounds__(STV_THREADS, 2)
+k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
+            uint64_t ntiles) {
+    using C = typename C2T<R>::T;
+    constexpr int V = sizeof(C) == 8 ? 1 : 0;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const StvPass *P = (const StvPass *)(blob + pass_off);
+    const int S = P->S, L = P->L, h = P->h;
+    const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
+    const int nops = P->nops;
+    const StvOp *ops = (const StvOp *)((const uint8_t *)P + P->ops_off);
+    uint64_t hmask = 0;
+    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
+
+    uint64_t *bars = (uint64_t *)smem;                 // [3]
+    uint64_t *tbase = (uint64_t *)(smem + 32);         // [3]
+    DiagScratch *sc = (DiagScratch *)(smem + 64);
+    uint8_t *mat = smem + kHdrBytes;
+    const uint32_t mat_bytes = P->mat_bytes;
+    const uint32_t mat_pad = (mat_bytes + 127u) & ~127u;
+    C *tiles = (C *)(smem + kHdrBytes + mat_pad);
+    const uint32_t tile_elems = 1u << S;
+    const uint32_t run_elems = 1u << L;
+    const uint32_t nruns = 1u << h;
+    const uint32_t run_bytes = run_elems * sizeof(C);
+    const uint32_t tile_bytes = tile_elems * sizeof(C);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // stage matrices (once per persistent CTA)
+    {
+        const uint4 *src = (const uint4 *)((const uint8_t *)P + P->mat_off);
+        uint4 *dst = (uint4 *)mat;
+        for (uint32_t k = tid; k < mat_bytes / 16; k += blockDim.x) dst[k] = src[k];
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+    }
+    __syncthreads();
+
+    const uint64_t first = blockIdx.x, stride = gridDim.x;
+    uint64_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+
+    auto issue_load = [&](uint64_t j) {   // warp 0 only
+        const uint64_t t = first + j * stride;
+        const int s = (int)(j % kStages);
+        const uint64_t base = pdep64(t, out_mask);
+        if (lane == 0) {
+            tbase[s] = base;
+            mbar_arrive_expect_tx(&bars[s], tile_bytes);
+        }
+        __syncwarp();
+        C *dst = tiles + (size_t)s * tile_elems;
+        for (uint32_t r = lane; r < nruns; r += 32) {
+            const uint64_t off = base | pdep64(r, hmask);
+            tma_load_1d(dst + (size_t)r * run_elems, state + off, run_bytes, &bars[s]);
+        }
+    };
+
+    if (warp == 0) {
+        for (uint64_t j = 0; j < (uint64_t)(kStages - 1) && j < my_tiles; ++j) issue_load(j);
+    }
+
+    for (uint64_t j = 0; j < my_tiles; ++j) {
+        const int s = (int)(j % kStages);
+        mbar_wait(&bars[s], (uint32_t)((j / kStages) & 1));
+        C *tile = tiles + (size_t)s * tile_elems;
+        const uint64_t base = tbase[s];
+        const uint64_t full_base = base | rank_bits;
+        for (int o = 0; o < nops; ++o) {
+            const StvOp &op = ops[o];
+            const int type = op.type;
+            if (type == OP_DENSE) {
+                int tp[STV_MAX_K];
+#pragma unroll
+                for (int b = 0; b < STV_MAX_K; ++b) tp[b] = op.tpos[b];
+                const C *M = (const C *)(mat + op.mat_off);
+                switch (op.k) {
+                case 1: dense_op<1, C>(tile, S, tp, M); break;
+                case 2: dense_op<2, C>(tile, S, tp, M); break;
+                case 3: dense_op<3, C>(tile, S, tp, M); break;
+                case 4: dense_op<4, C>(tile, S, tp, M); break;
+                }
+            } else if (type == OP_CNOT) {
+                const bool on = op.c_phys < 0 || ((full_base >> op.c_phys) & 1);
+                if (on) cnot_op<C>(tile, S, op.t_loc, op.c_loc);
+            } else {
+                const StvDiag *D = (const StvDiag *)((const uint8_t *)P + op.diag_off);
+                diag_prep<V>(D, S, full_base, sc);
+                __syncthreads();
+                diag_op_tile<V, C>(tile, S, D, sc);
+            }
+            __syncthreads();
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (warp == 0) {
+            for (uint32_t r = lane; r < nruns; r += 32) {
+                const uint64_t off = base | pdep64(r, hmask);
+                tma_store_1d(state + off, tile + (size_t)r * run_elems, run_bytes);
+            }
+            bulk_commit();
+            if (j + kStages - 1 < my_tiles) {
+                bulk_wait_read_1();      // buffer of tile j-1 drained by its store
+                __syncwarp();
+                issue_load(j + kStages - 1);
+            }
+        }
+    }
+    if (warp == 0) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------
+// standalone diagonal pass (streaming; skip-write)
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(STV_THREADS)
+k_diag_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
+            uint64_t nchunks) {
+    using C = typename C2T<R>::T;
+    constexpr int V = sizeof(C) == 8 ? 1 : 0;
+    __shared__ DiagScratch sc;
+    const StvPass *P = (const StvPass *)(blob + pass_off);
+    const StvDiag *D = (const StvDiag *)((const uint8_t *)P + P->diag_off);
+    const int S = P->S;
+    const uint64_t rank_bits = P->rank_bits;
+    for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const uint64_t base = ch << S;
+        __syncthreads();
+        diag_prep<V>(D, S, base | rank_bits, &sc);
+        __syncthreads();
+        uint64_t bt, lf[6];
+        int nF;
+        diag_thread<V>(D, S, &sc, bt, lf, nF);
+        const int nr = nF - V;
+        const uint32_t tsz = 1u << S;
+        for (int r = 0; r < (1 << nr); ++r) {
+            const uint32_t i0 = ((uint32_t)r << (V + 8)) | ((uint32_t)threadIdx.x << V);
+            if (i0 >= tsz) continue;
+            if (V == 1) {
+                float4 *p = (float4 *)(state + base + i0);
+                float4 v = *p;
+                uint64_t ph0 = bt + sc.qf[r << 1], ph1 = bt + sc.qf[(r << 1) | 1] + lf[0];
+#pragma unroll
+                for (int f = 1; f < 6; ++f)
+                    if (f < nF && (((r << 1) >> f) & 1)) { ph0 += lf[f]; ph1 += lf[f]; }
+                if (ph0 == 0 && ph1 == 0) continue;
+                float2 a = make_float2(v.x, v.y), b = make_float2(v.z, v.w);
+                a = apply_phase(a, ph0);
+                b = apply_phase(b, ph1);
+                *p = make_float4(a.x, a.y, b.x, b.y);
+            } else {
+                C *p = state + base + i0;
+                uint64_t ph = bt + sc.qf[r];
+#pragma unroll
+                for (int f = 0; f < 6; ++f)
+                    if (f < nF && ((r >> f) & 1)) ph += lf[f];
+                if (ph == 0) continue;
+                *p = apply_phase(*p, ph);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// standalone CNOT(c, t): swap alpha_i <-> alpha_{i ^ 2^t} where bit c = 1;
+// c < 0: unconditional X on t (control resolved per rank)
+// ---------------------------------------------------------------------------
+template <typename C>
+__global__ void __launch_bounds__(STV_THREADS)
+k_cnot_pass(C *__restrict__ state, int c, int t, uint64_t nitems) {
+    const int lo_b = c >= 0 ? min(c, t) : t, hi_b = c >= 0 ? max(c, t) : -1;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nitems;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t i = ((v >> lo_b) << (lo_b + 1)) | (v & ((1ull << lo_b) - 1));
+        if (hi_b >= 0) i = ((i >> hi_b) << (hi_b + 1)) | (i & ((1ull << hi_b) - 1));
+        if (c >= 0) i |= 1ull << c;
+        const uint64_t j = i | (1ull << t);
+        C a = state[i];
+        state[i] = state[j];
+        state[j] = a;
+    }
+}
+
+// swap physical index bits a and b (a != b): exchanges alpha_{..1_a..0_b..} <-> alpha_{..0_a..1_b..}
+template <typename C>
+__global__ void __launch_bounds__(STV_THREADS) k_bitswap(C *__restrict__ state, int a, int b, uint64_t nitems) {
+    const int lo_b = min(a, b), hi_b = max(a, b);
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nitems;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t i = ((v >> lo_b) << (lo_b + 1)) | (v & ((1ull << lo_b) - 1));
+        i = ((i >> hi_b) << (hi_b + 1)) | (i & ((1ull << hi_b) - 1));
+        const uint64_t x = i | (1ull << a), y = i | (1ull << b);
+        C p = state[x];
+        state[x] = state[y];
+        state[y] = p;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// norm: fp64 partials over a fixed grid, fixed-shape trees (deterministic)
+// ---------------------------------------------------------------------------
+template <typename C>
+__global__ void __launch_bounds__(STV_THREADS) k_norm_partial(const C *__restrict__ state, uint64_t N, double *part) {
+    __shared__ double red[STV_THREADS / 32];
+    const uint64_t per = (N + gridDim.x - 1) / gridDim.x;
+    const uint64_t b = blockIdx.x * per, e = min(N, b + per);
+    double acc = 0;
+    for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+        const C a = state[i];
+        acc += (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < STV_THREADS / 32 ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) part[blockIdx.x] = v;
+    }
+}
+
+__global__ void __launch_bounds__(STV_THREADS) k_norm_final(const double *part, int np, double *out) {
+    __shared__ double red[STV_THREADS];
+    double acc = 0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = STV_THREADS / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0];
+}
+
+// ---------------------------------------------------------------------------
+// init / readout
+// ---------------------------------------------------------------------------
+template <typename C>
+__global__ void __launch_bounds__(STV_THREADS) k_fill(C *__restrict__ state, uint64_t N, C val, int64_t one_at, C one) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x)
+        state[i] = ((int64_t)i == one_at) ? one : val;
+}
+
+struct GatherMap {
+    int32_t perm[64];      // logical qubit -> actual physical bit
+    uint64_t xmask;
+    int32_t n;
+    int32_t n_local;
+    uint64_t rank_bits;    // this rank's global value (>> n_local)
+};
+
+// out[k] = alpha(logical j_k) for the amplitudes this rank owns; others untouched
+template <typename C, typename O>
+__global__ void __launch_bounds__(STV_THREADS)
+k_gather(const C *__restrict__ state, const uint64_t *__restrict__ idx, uint64_t first, uint64_t count, GatherMap gm,
+         O *__restrict__ out) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t j = idx ? idx[k] : first + k;
+        uint64_t p = 0;
+        for (int q = 0; q < gm.n; ++q) p |= ((j >> q) & 1) << gm.perm[q];
+        p ^= gm.xmask;
+        if ((p >> gm.n_local) != gm.rank_bits) continue;
+        const C a = state[p & ((1ull << gm.n_local) - 1)];
+        O o;
+        o.x = a.x;
+        o.y = a.y;
+        out[k] = o;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers (called from api.cpp)
+// ---------------------------------------------------------------------------
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+static size_t tile_smem_bytes(int S, uint32_t mat_bytes, size_t esz) {
+    return kHdrBytes + ((mat_bytes + 127u) & ~127u) + (size_t)kStages * ((size_t)esz << S);
+}
+
+cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
+                             uint32_t mat_bytes, cudaStream_t st, int *kernels) {
+    const size_t esz = c128 ? 16 : 8;
+    const size_t smem = tile_smem_bytes(S, mat_bytes, esz);
+    const uint64_t ntiles = 1ull << (n_local - S);
+    int occ = 0;
+    cudaError_t e;
+    if (c128) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_tile_pass<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_pass<double>, STV_THREADS, smem);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_tile_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_pass<float>, STV_THREADS, smem);
+    }
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    uint64_t grid = (uint64_t)num_sms() * occ;
+    if (grid > ntiles) grid = ntiles;
+    if (c128)
+        k_tile_pass<double><<<(unsigned)grid, STV_THREADS, smem, st>>>((double2 *)state, dblob, pass_off, ntiles);
+    else
+        k_tile_pass<float><<<(unsigned)grid, STV_THREADS, smem, st>>>((float2 *)state, dblob, pass_off, ntiles);
+    e = cudaGetLastError();
+    ++*kernels;
+    return e;
+}
+
+cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
+                             cudaStream_t st, int *kernels) {
+    const uint64_t nch = 1ull << (n_local - S);
+    uint64_t grid = (uint64_t)num_sms() * 8;
+    if (grid > nch) grid = nch;
+    if (c128)
+        k_diag_pass<double><<<(unsigned)grid, STV_THREADS, 0, st>>>((double2 *)state, dblob, pass_off, nch);
+    else
+        k_diag_pass<float><<<(unsigned)grid, STV_THREADS, 0, st>>>((float2 *)state, dblob, pass_off, nch);
+    ++*kernels;
+    return cudaGetLastError();
+}
+
+static unsigned grid_for(uint64_t items) {
+    uint64_t g = (items + STV_THREADS - 1) / STV_THREADS;
+    const uint64_t cap = (uint64_t)num_sms() * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+cudaError_t launch_cnot(bool c128, void *state, int c, int t, int n_local, cudaStream_t st, int *kernels) {
+    const uint64_t items = 1ull << (n_local - (c >= 0 ? 2 : 1));
+    if (c128) k_cnot_pass<double2><<<grid_for(items), STV_THREADS, 0, st>>>((double2 *)state, c, t, items);
+    else k_cnot_pass<float2><<<grid_for(items), STV_THREADS, 0, st>>>((float2 *)state, c, t, items);
+    ++*kernels;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bitswap(bool c128, void *state, int a, int b, int n_bits, cudaStream_t st, int *kernels) {
+    const uint64_t items = 1ull << (n_bits - 2);
+    if (c128) k_bitswap<double2><<<grid_for(items), STV_THREADS, 0, st>>>((double2 *)state, a, b, items);
+    else k_bitswap<float2><<<grid_for(items), STV_THREADS, 0, st>>>((float2 *)state, a, b, items);
+    ++*kernels;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_norm(bool c128, const void *state, uint64_t N, double *part, int np, double *out, cudaStream_t st,
+                        int *kernels) {
+    if (c128) k_norm_partial<double2><<<np, STV_THREADS, 0, st>>>((const double2 *)state, N, part);
+    else k_norm_partial<float2><<<np, STV_THREADS, 0, st>>>((const float2 *)state, N, part);
+    k_norm_final<<<1, STV_THREADS, 0, st>>>(part, np, out);
+    *kernels += 2;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(bool c128, void *state, uint64_t N, double val, int64_t one_at, cudaStream_t st, int *kernels) {
+    if (c128) {
+        double2 v = make_double2(val, 0), o = make_double2(1, 0);
+        k_fill<double2><<<grid_for(N), STV_THREADS, 0, st>>>((double2 *)state, N, v, one_at, o);
+    } else {
+        float2 v = make_float2((float)val, 0), o = make_float2(1, 0);
+        k_fill<float2><<<grid_for(N), STV_THREADS, 0, st>>>((float2 *)state, N, v, one_at, o);
+    }
+    ++*kernels;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(bool c128, const void *state, const uint64_t *didx, uint64_t first, uint64_t count,
+                          const GatherMap &gm, bool out_native, void *dout, cudaStream_t st, int *kernels) {
+    const unsigned g = grid_for(count);
+    if (c128)
+        k_gather<double2, double2><<<g, STV_THREADS, 0, st>>>((const double2 *)state, didx, first, count, gm,
+                                                               (double2 *)dout);
+    else if (out_native)
+        k_gather<float2, float2><<<g, STV_THREADS, 0, st>>>((const float2 *)state, didx, first, count, gm,
+                                                             (float2 *)dout);
+    else
+        k_gather<float2, double2><<<g, STV_THREADS, 0, st>>>((const float2 *)state, didx, first, count, gm,
+                                                              (double2 *)dout);
+    ++*kernels;
+    return cudaGetLastError();
+}
+
+}  // namespace stv
+
+// ---------------------------------------------------------------------------
+// remap pack/unpack: chunk c = local indices whose bits
+// lbits[i] equal bit i of c; element k of the chunk inserts those bits into k
+// ---------------------------------------------------------------------------
+namespace stv {
+struct PackSpec {
+    int32_t pos[8];    // ascending local bit positions
+    int32_t bit[8];    // value for each position
+    int32_t m;
+};
+
+template <typename C>
+__global__ void __launch_bounds__(STV_THREADS)
+k_pack(C *__restrict__ state, C *__restrict__ buf, PackSpec ps, uint64_t first, uint64_t count, int unpack) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < count;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t i = first + k;
+        for (int b = 0; b < ps.m; ++b) {
+            const int p = ps.pos[b];
+            i = ((i >> p) << (p + 1)) | ((uint64_t)ps.bit[b] << p) | (i & ((1ull << p) - 1));
+        }
+        if (unpack) state[i] = buf[k];
+        else buf[k] = state[i];
+    }
+}
+
+cudaError_t launch_pack(bool c128, const void *state, void *dst, const int *lbits, int m, uint32_t chunk,
+                        uint64_t first, uint64_t count, int n_local, bool unpack, cudaStream_t st, int *kernels) {
+    (void)n_local;
+    PackSpec ps;
+    ps.m = m;
+    int order[8];
+    for (int i = 0; i < m; ++i) order[i] = i;
+    for (int i = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j)
+            if (lbits[order[j]] < lbits[order[i]]) { int t = order[i]; order[i] = order[j]; order[j] = t; }
+    for (int i = 0; i < m; ++i) {
+        ps.pos[i] = lbits[order[i]];
+        ps.bit[i] = (chunk >> order[i]) & 1;
+    }
+    if (c128)
+        k_pack<double2><<<grid_for(count), STV_THREADS, 0, st>>>((double2 *)state, (double2 *)dst, ps, first, count, unpack);
+    else
+        k_pack<float2><<<grid_for(count), STV_THREADS, 0, st>>>((float2 *)state, (float2 *)dst, ps, first, count, unpack);
+    ++*kernels;
+    return cudaGetLastError();
+}
+}  // namespace stv

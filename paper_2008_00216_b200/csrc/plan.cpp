@@ -1,0 +1,824 @@
+// plan.cpp -- gate IR, relabel frame, Sec. 4.5 reordering, k-qubit fusion,
+// diagonal clustering, global-qubit remap insertion, blob encoding.
+// See plan.h for the step-by-step citations.
+#include "plan.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+namespace stv {
+
+static const double kPi = 3.14159265358979323846;
+
+// ---------------------------------------------------------------------------
+// fixed-point turns
+// ---------------------------------------------------------------------------
+uint64_t turns_of_angle(double rad) {
+    double x = rad / (2.0 * kPi);
+    x -= std::nearbyint(x);               // [-0.5, 0.5]
+    if (x >= 0.5) x -= 1.0;
+    double y = std::ldexp(x, 64);         // |y| <= 2^63
+    int64_t t = (y <= -9223372036854775808.0) ? INT64_MIN : (int64_t)std::llrint(y);
+    return (uint64_t)t;
+}
+
+double angle_of_turns(uint64_t t) {
+    return std::ldexp((double)(int64_t)t, -63) * kPi;
+}
+
+void QForm::add(const QForm &o) {
+    cst += o.cst;
+    for (auto &kv : o.lin) lin[kv.first] += kv.second;
+    for (auto &kv : o.quad) quad[kv.first] += kv.second;
+}
+
+uint64_t QForm::eval(uint64_t j) const {
+    uint64_t s = cst;
+    for (auto &kv : lin)
+        if ((j >> kv.first) & 1) s += kv.second;
+    for (auto &kv : quad)
+        if (((j >> kv.first.first) & 1) && ((j >> kv.first.second) & 1)) s += kv.second;
+    return s;
+}
+
+uint64_t QForm::qubits() const {
+    uint64_t m = 0;
+    for (auto &kv : lin)
+        if (kv.second) m |= 1ull << kv.first;
+    for (auto &kv : quad)
+        if (kv.second) m |= (1ull << kv.first.first) | (1ull << kv.first.second);
+    return m;
+}
+
+bool QForm::trivial() const { return cst == 0 && qubits() == 0; }
+
+uint64_t PGate::qmask() const {
+    if (type == GType::DIAG) return form.qubits();
+    uint64_t m = 0;
+    for (int i = 0; i < nq; ++i) m |= 1ull << q[i];
+    return m;
+}
+
+uint64_t PGate::dmask() const {
+    if (type == GType::DIAG) return 0;
+    if (type == GType::CNOT) return 1ull << q[1];
+    return qmask();
+}
+
+void Frame::identity(int n) {
+    for (int i = 0; i < 64; ++i) perm[i] = i;
+    (void)n;
+    xmask = 0;
+}
+
+// ---------------------------------------------------------------------------
+// gate table (the product's own; written from PAPER.md L139-173 and the
+// readings A3-A6 -- independent of oracle/)
+// ---------------------------------------------------------------------------
+static int nq_of(int kind) {
+    switch (kind) {
+    case SV_CZ: case SV_CNOT: case SV_SWAP: case SV_CPHASE: case SV_FSIM: case SV_U2: return 2;
+    default: return 1;
+    }
+}
+
+static void dense_matrix(const sv_gate &g, cd *U) {
+    const double h = 0.70710678118654752440;   // 1/sqrt 2
+    const cd I(0, 1);
+    for (int i = 0; i < 16; ++i) U[i] = 0;
+    switch (g.kind) {
+    case SV_H: U[0] = h; U[1] = h; U[2] = h; U[3] = -h; break;
+    case SV_X: U[1] = 1; U[2] = 1; break;
+    case SV_Y: U[1] = -I; U[2] = I; break;
+    case SV_Z: U[0] = 1; U[3] = -1; break;
+    case SV_S: U[0] = 1; U[3] = I; break;
+    case SV_T: U[0] = 1; U[3] = cd(h, h); break;
+    case SV_SX: U[0] = cd(.5, .5); U[1] = cd(.5, -.5); U[2] = cd(.5, -.5); U[3] = cd(.5, .5); break;
+    case SV_SY: U[0] = cd(.5, .5); U[1] = cd(.5, .5); U[2] = cd(-.5, -.5); U[3] = cd(.5, .5); break;
+    case SV_SW: U[0] = cd(.5, .5); U[1] = cd(0, -h); U[2] = h; U[3] = cd(.5, .5); break;
+    case SV_CZ: U[0] = 1; U[5] = 1; U[10] = 1; U[15] = -1; break;
+    case SV_CNOT: U[0] = 1; U[5] = 1; U[11] = 1; U[14] = 1; break;
+    case SV_SWAP: U[0] = 1; U[6] = 1; U[9] = 1; U[15] = 1; break;
+    case SV_CPHASE: U[0] = 1; U[5] = 1; U[10] = 1; U[15] = std::polar(1.0, g.phi); break;
+    case SV_FSIM:
+        U[0] = 1; U[5] = std::cos(g.theta); U[6] = -I * std::sin(g.theta);
+        U[9] = -I * std::sin(g.theta); U[10] = std::cos(g.theta); U[15] = std::polar(1.0, -g.phi);
+        break;
+    case SV_U1: for (int i = 0; i < 4; ++i) U[i] = cd(g.m[2 * i], g.m[2 * i + 1]); break;
+    case SV_U2: for (int i = 0; i < 16; ++i) U[i] = cd(g.m[2 * i], g.m[2 * i + 1]); break;
+    }
+    if (g.flags & SV_GATE_ADJOINT) {
+        int d = 1 << nq_of(g.kind);
+        cd T[16];
+        for (int r = 0; r < d; ++r)
+            for (int c = 0; c < d; ++c) T[r * d + c] = std::conj(U[c * d + r]);
+        std::memcpy((void *)U, (void *)T, sizeof(cd) * 16);
+    }
+}
+
+std::string validate(int n, const sv_gate *g, size_t ng) {
+    for (size_t i = 0; i < ng; ++i) {
+        std::ostringstream e;
+        const sv_gate &x = g[i];
+        if (x.kind < 0 || x.kind >= SV_NUM_KINDS) { e << "gate " << i << ": unknown kind " << x.kind; return e.str(); }
+        if (x.flags & ~SV_GATE_ADJOINT) { e << "gate " << i << ": unknown flags"; return e.str(); }
+        int q = nq_of(x.kind);
+        if (x.q0 < 0 || x.q0 >= n) { e << "gate " << i << ": qubit q0=" << x.q0 << " out of range [0," << n << ")"; return e.str(); }
+        if (q == 2) {
+            if (x.q1 < 0 || x.q1 >= n) { e << "gate " << i << ": qubit q1=" << x.q1 << " out of range"; return e.str(); }
+            if (x.q1 == x.q0) { e << "gate " << i << ": duplicate qubit " << x.q0; return e.str(); }
+        }
+        if (!std::isfinite(x.theta) || !std::isfinite(x.phi)) { e << "gate " << i << ": non-finite angle"; return e.str(); }
+        if (x.kind == SV_U1 || x.kind == SV_U2) {
+            if (!x.m) { e << "gate " << i << ": NULL matrix"; return e.str(); }
+            int d = 1 << q;
+            for (int k = 0; k < 2 * d * d; ++k)
+                if (!std::isfinite(x.m[k])) { e << "gate " << i << ": non-finite matrix entry"; return e.str(); }
+            cd U[16];
+            dense_matrix(x, U);
+            double worst = 0;
+            for (int r = 0; r < d; ++r)
+                for (int c = 0; c < d; ++c) {
+                    cd s = 0;
+                    for (int k = 0; k < d; ++k) s += std::conj(U[k * d + r]) * U[k * d + c];
+                    worst = std::max(worst, std::abs(s - cd(r == c ? 1.0 : 0.0)));
+                }
+            if (worst > 1e-10) { e << "gate " << i << ": matrix not unitary (|U^dag U - I| = " << worst << ")"; return e.str(); }
+        }
+    }
+    return "";
+}
+
+// ---------------------------------------------------------------------------
+// a1 + a2: classification and the relabel frame
+// ---------------------------------------------------------------------------
+// diagonal table t[l] (l = local index, q[0] = MSB) -> QForm over bits p[]
+static QForm form_of_table(int nq, const int *p, const uint64_t *t) {
+    QForm f;
+    if (nq == 1) {
+        f.cst = t[0];
+        f.lin[p[0]] = t[1] - t[0];
+    } else {
+        // l = 2 b(p0) + b(p1)
+        f.cst = t[0];
+        f.lin[p[1]] = t[1] - t[0];
+        f.lin[p[0]] = t[2] - t[0];
+        int a = std::min(p[0], p[1]), b = std::max(p[0], p[1]);
+        f.quad[{a, b}] = t[3] - t[2] - t[1] + t[0];
+    }
+    for (auto it = f.lin.begin(); it != f.lin.end();) it = it->second ? std::next(it) : f.lin.erase(it);
+    for (auto it = f.quad.begin(); it != f.quad.end();) it = it->second ? std::next(it) : f.quad.erase(it);
+    return f;
+}
+
+static bool is_diag(int d, const cd *U) {
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c)
+            if (r != c && U[r * d + c] != cd(0, 0)) return false;
+    return true;
+}
+
+std::vector<PGate> to_physical(int n, const sv_gate *gs, size_t ng, Frame &fr, uint32_t flags) {
+    (void)n;
+    std::vector<PGate> out;
+    out.reserve(ng);
+    const bool relabel = !(flags & SV_OPT_NO_RELABEL);
+    const uint64_t Q = 1ull << 62, H = 1ull << 63, E = 1ull << 61;  // quarter, half, eighth turn
+    for (size_t i = 0; i < ng; ++i) {
+        const sv_gate &g = gs[i];
+        const bool adj = g.flags & SV_GATE_ADJOINT;
+        const int nq = nq_of(g.kind);
+        int lq[2] = {g.q0, nq == 2 ? g.q1 : -1};
+        int p[2] = {fr.perm[lq[0]], nq == 2 ? fr.perm[lq[1]] : -1};
+        int f[2] = {(int)((fr.xmask >> p[0]) & 1), nq == 2 ? (int)((fr.xmask >> p[1]) & 1) : 0};
+        const int F = nq == 2 ? (f[0] << 1) | f[1] : f[0];
+        auto emit_diag = [&](const uint64_t *tlog) {
+            uint64_t t[4];
+            for (int l = 0; l < (1 << nq); ++l) t[l ^ F] = adj ? (uint64_t)(0 - tlog[l]) : tlog[l];
+            PGate pg;
+            pg.type = GType::DIAG;
+            pg.nq = nq;
+            pg.q[0] = p[0]; pg.q[1] = p[1];
+            pg.form = form_of_table(nq, p, t);
+            pg.src = (int)i;
+            if (!pg.form.trivial()) out.push_back(pg);
+        };
+        auto emit_dense = [&]() {
+            cd U[16];
+            dense_matrix(g, U);
+            int d = 1 << nq;
+            PGate pg;
+            pg.type = GType::DENSE;
+            pg.nq = nq;
+            pg.q[0] = p[0]; pg.q[1] = p[1];
+            for (int r = 0; r < d; ++r)
+                for (int c = 0; c < d; ++c) pg.U[(r ^ F) * d + (c ^ F)] = U[r * d + c];
+            pg.src = (int)i;
+            if (is_diag(d, pg.U)) {       // e.g. Eq. 2-style products, diagonal U1/U2
+                uint64_t t[4];
+                for (int l = 0; l < d; ++l) t[l] = turns_of_angle(std::arg(pg.U[l * d + l]));
+                PGate dg;
+                dg.type = GType::DIAG;
+                dg.nq = nq;
+                dg.q[0] = p[0]; dg.q[1] = p[1];
+                dg.form = form_of_table(nq, p, t);
+                dg.src = (int)i;
+                if (!dg.form.trivial()) out.push_back(dg);
+                return;
+            }
+            out.push_back(pg);
+        };
+        switch (g.kind) {
+        case SV_Z: { uint64_t t[2] = {0, H}; emit_diag(t); break; }
+        case SV_S: { uint64_t t[2] = {0, Q}; emit_diag(t); break; }
+        case SV_T: { uint64_t t[2] = {0, E}; emit_diag(t); break; }
+        case SV_CZ: { uint64_t t[4] = {0, 0, 0, H}; emit_diag(t); break; }
+        case SV_CPHASE: { uint64_t t[4] = {0, 0, 0, turns_of_angle(g.phi)}; emit_diag(t); break; }
+        case SV_X:
+            if (relabel) fr.xmask ^= 1ull << p[0]; else emit_dense();
+            break;
+        case SV_Y:
+            if (relabel) {
+                // Y = X . diag(i, -i): apply the diagonal, then relabel X.
+                // Y is self-inverse: pre-negate so emit_diag's adjoint negation cancels
+                uint64_t t[2] = {adj ? 3 * Q : Q, adj ? Q : 3 * Q};
+                emit_diag(t);
+                fr.xmask ^= 1ull << p[0];
+            } else emit_dense();
+            break;
+        case SV_SWAP:
+            if (relabel) std::swap(fr.perm[lq[0]], fr.perm[lq[1]]); else emit_dense();
+            break;
+        case SV_CNOT: {
+            PGate pg;
+            pg.type = GType::CNOT;
+            pg.nq = 2;
+            pg.q[0] = p[0]; pg.q[1] = p[1];
+            pg.src = (int)i;
+            out.push_back(pg);
+            // a flipped control turns CNOT into X_t . CNOT: relabel the X
+            if (f[0]) fr.xmask ^= 1ull << p[1];
+            break;
+        }
+        case SV_FSIM:
+            if (relabel && g.theta == kPi / 2) {
+                // reading A5: fSim(pi/2, phi) = SWAP . diag(1, -i, -i, e^{-i phi})
+                uint64_t t[4] = {0, 3 * Q, 3 * Q, turns_of_angle(-g.phi)};
+                emit_diag(t);
+                std::swap(fr.perm[lq[0]], fr.perm[lq[1]]);
+            } else emit_dense();
+            break;
+        case SV_U1:
+            if (relabel) {
+                cd U[16];
+                dense_matrix(g, U);
+                if (U[0] == cd(0, 0) && U[3] == cd(0, 0)) {
+                    // anti-diagonal [[0,b],[a,0]] = X . diag(a, b)
+                    uint64_t t[2] = {turns_of_angle(std::arg(U[2])), turns_of_angle(std::arg(U[1]))};
+                    const bool a0 = adj;
+                    (void)a0;
+                    // dense_matrix already applied the adjoint; emit_diag must not negate again
+                    PGate pg;
+                    uint64_t tt[2];
+                    for (int l = 0; l < 2; ++l) tt[l ^ F] = t[l];
+                    pg.type = GType::DIAG;
+                    pg.nq = 1;
+                    pg.q[0] = p[0];
+                    pg.form = form_of_table(1, p, tt);
+                    pg.src = (int)i;
+                    if (!pg.form.trivial()) out.push_back(pg);
+                    fr.xmask ^= 1ull << p[0];
+                    break;
+                }
+            }
+            emit_dense();
+            break;
+        default:
+            emit_dense();
+        }
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// dense-matrix helpers (local index LSB-first over an ascending bit list)
+// ---------------------------------------------------------------------------
+// Expand gate matrix G (nq qubits, q[0] = MSB) to the basis of ascending bits tg.
+static std::vector<cd> expand_gate(const PGate &g, const std::vector<int> &tg) {
+    const int k = (int)tg.size(), D = 1 << k;
+    int pos[2];
+    for (int i = 0; i < g.nq; ++i) pos[i] = (int)(std::find(tg.begin(), tg.end(), g.q[i]) - tg.begin());
+    uint32_t gm = 0;
+    for (int i = 0; i < g.nq; ++i) gm |= 1u << pos[i];
+    const int d = 1 << g.nq;
+    std::vector<cd> R((size_t)D * D, cd(0, 0));
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            if ((r & ~gm) != (c & ~gm)) continue;
+            int lr = 0, lc = 0;
+            for (int i = 0; i < g.nq; ++i) {
+                lr |= ((r >> pos[i]) & 1) << (g.nq - 1 - i);
+                lc |= ((c >> pos[i]) & 1) << (g.nq - 1 - i);
+            }
+            R[(size_t)r * D + c] = g.U[lr * d + lc];
+        }
+    return R;
+}
+
+// Re-express op matrix M over `from` bits in the basis of `to` (superset) bits.
+static std::vector<cd> widen(const std::vector<cd> &M, const std::vector<int> &from, const std::vector<int> &to) {
+    const int k = (int)to.size(), D = 1 << k, kf = (int)from.size(), Df = 1 << kf;
+    std::vector<int> pos(kf);
+    uint32_t fm = 0;
+    for (int i = 0; i < kf; ++i) {
+        pos[i] = (int)(std::find(to.begin(), to.end(), from[i]) - to.begin());
+        fm |= 1u << pos[i];
+    }
+    std::vector<cd> R((size_t)D * D, cd(0, 0));
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            if ((r & ~fm) != (c & ~fm)) continue;
+            int lr = 0, lc = 0;
+            for (int i = 0; i < kf; ++i) {
+                lr |= ((r >> pos[i]) & 1) << i;
+                lc |= ((c >> pos[i]) & 1) << i;
+            }
+            R[(size_t)r * D + c] = M[(size_t)lr * Df + lc];
+        }
+    return R;
+}
+
+static std::vector<cd> matmul(const std::vector<cd> &A, const std::vector<cd> &B, int D) {
+    std::vector<cd> C((size_t)D * D, cd(0, 0));
+    for (int r = 0; r < D; ++r)
+        for (int k = 0; k < D; ++k) {
+            cd a = A[(size_t)r * D + k];
+            if (a == cd(0, 0)) continue;
+            for (int c = 0; c < D; ++c) C[(size_t)r * D + c] += a * B[(size_t)k * D + c];
+        }
+    return C;
+}
+
+static std::vector<int> bits_of(uint64_t m) {
+    std::vector<int> v;
+    for (int b = 0; b < 64; ++b)
+        if ((m >> b) & 1) v.push_back(b);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// a3 + a4: reordering + fusion into passes
+// ---------------------------------------------------------------------------
+PlanOptions resolve_options(const sv_options *o, int amp_bytes, int n_local) {
+    PlanOptions p;
+    p.tile_bits = amp_bytes == 8 ? 12 : 11;
+    if (o) {
+        if (o->kmax > 0) p.kmax = std::min(o->kmax, STV_MAX_K);
+        if (o->tile_bits > 0) p.tile_bits = std::min(o->tile_bits, STV_MAX_TILE_BITS);
+        if (o->low_bits > 0) p.low_bits = o->low_bits;
+        if (o->budget > 0) p.budget = o->budget;
+        p.flags = o->flags;
+    }
+    // shared memory: 3 stages of 2^S amplitudes + matrices must fit in 227 KB
+    p.tile_bits = std::min(p.tile_bits, amp_bytes == 8 ? 13 : 12);
+    // keep >= ~256 tiles so every SM gets work; small states get small tiles
+    int smax = std::min(p.tile_bits, std::max(std::min(n_local, 6), n_local - 8));
+    p.tile_bits = std::max(1, std::min(smax, n_local));
+    // TMA bulk copies move >= 16 B: c64 runs need >= 2 amplitudes (L >= 1)
+    const int minL = amp_bytes == 8 ? 1 : 0;
+    p.low_bits = std::max(minL, std::min(p.low_bits, p.tile_bits - 2));
+    p.tile_bits = std::max(p.tile_bits, std::min(n_local, p.low_bits + 2));   // any 2-qubit gate fits
+    p.kmax = std::max(1, std::min(p.kmax, p.tile_bits));
+    return p;
+}
+
+static const size_t kMaxMatBytes = 32768;   // matrices staged in shared memory per pass
+
+static int op_cost(const FOp &o) {
+    switch (o.type) {
+    case OP_DENSE: { int k = (int)o.tg.size(); return std::max(4 << k, 16) + 4; }
+    case OP_DIAG: return 24;
+    default: return 12;
+    }
+}
+
+static bool commutes_op(const FOp &o, uint64_t gq, uint64_t gd) {
+    // commute iff on every shared qubit both act diagonally
+    uint64_t shared = o.qmask & gq;
+    return (shared & (o.dmask | gd)) == 0;
+}
+
+// Try to merge gate g (actual-physical bits) into the op list (backward search).
+static void merge_into(std::vector<FOp> &ops, const PGate &g, int kmax, bool fold_diag, bool one_gate) {
+    const uint64_t gq = g.qmask(), gd = g.dmask();
+    if (!one_gate) {
+        for (int i = (int)ops.size() - 1; i >= 0; --i) {
+            FOp &o = ops[i];
+            bool ok = false;
+            if (g.type == GType::DIAG) {
+                if (o.type == OP_DIAG) ok = true;
+                else if (o.type == OP_DENSE && fold_diag && (gq & ~o.dmask) == 0) ok = true;
+            } else if (g.type == GType::DENSE && o.type == OP_DENSE) {
+                ok = __builtin_popcountll(o.dmask | gd) <= kmax;
+            } else if (g.type == GType::CNOT && o.type == OP_DENSE) {
+                ok = (gq & ~o.dmask) == 0;    // CNOT inside the op's targets: a 4x4 permutation factor
+            }
+            if (ok) {
+                if (g.type == GType::DIAG && o.type == OP_DIAG) {
+                    o.form.add(g.form);
+                    o.qmask |= gq;
+                } else {
+                    uint64_t nm = o.dmask | gq;
+                    std::vector<int> tg = bits_of(nm);
+                    std::vector<cd> Mw = widen(o.M, o.tg, tg);
+                    std::vector<cd> G;
+                    if (g.type == GType::DIAG) {
+                        const int D = 1 << (int)tg.size();
+                        G.assign((size_t)D * D, cd(0, 0));
+                        for (int l = 0; l < D; ++l) {
+                            uint64_t j = 0;
+                            for (size_t b = 0; b < tg.size(); ++b)
+                                if ((l >> b) & 1) j |= 1ull << tg[b];
+                            G[(size_t)l * D + l] = std::polar(1.0, angle_of_turns(g.form.eval(j)));
+                        }
+                    } else if (g.type == GType::CNOT) {
+                        PGate pc = g;
+                        for (int r = 0; r < 16; ++r) pc.U[r] = 0;
+                        pc.U[0] = 1; pc.U[5] = 1; pc.U[11] = 1; pc.U[14] = 1;
+                        G = expand_gate(pc, tg);
+                    } else {
+                        G = expand_gate(g, tg);
+                    }
+                    o.M = matmul(G, Mw, 1 << (int)tg.size());
+                    o.tg = tg;
+                    o.qmask = o.dmask = nm;
+                }
+                return;
+            }
+            if (!commutes_op(o, gq, gd)) break;
+        }
+    }
+    FOp o;
+    if (g.type == GType::DIAG) {
+        o.type = OP_DIAG;
+        o.form = g.form;
+        o.qmask = gq;
+        o.dmask = 0;
+    } else if (g.type == GType::CNOT) {
+        o.type = OP_CNOT;
+        o.c = g.q[0];
+        o.t = g.q[1];
+        o.qmask = gq;
+        o.dmask = gd;
+    } else {
+        o.type = OP_DENSE;
+        o.tg = bits_of(gq);
+        o.M = expand_gate(g, o.tg);
+        o.qmask = o.dmask = gq;
+    }
+    ops.push_back(o);
+}
+
+static PGate map_gate(const PGate &g, const int *sigma) {
+    PGate a = g;
+    for (int i = 0; i < g.nq; ++i) a.q[i] = sigma[g.q[i]];
+    if (g.type == GType::DIAG) {
+        QForm f;
+        f.cst = g.form.cst;
+        for (auto &kv : g.form.lin) f.lin[sigma[kv.first]] += kv.second;
+        for (auto &kv : g.form.quad) {
+            int x = sigma[kv.first.first], y = sigma[kv.first.second];
+            f.quad[{std::min(x, y), std::max(x, y)}] += kv.second;
+        }
+        a.form = f;
+    }
+    return a;
+}
+
+Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg_virtual,
+                const PlanOptions &opt, int *sigma) {
+    Plan plan;
+    plan.n = n;
+    plan.n_global = n_global;
+    const int nl = n - n_global;
+    const uint64_t local_mask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
+    const uint64_t all_mask = n >= 64 ? ~0ull : ((1ull << n) - 1);
+    const uint64_t low_mask = (1ull << opt.low_bits) - 1;
+    const bool one_gate = opt.flags & SV_OPT_ONE_GATE;
+    const bool no_reorder = opt.flags & SV_OPT_NO_REORDER;
+    const bool fold = !(opt.flags & SV_OPT_NO_DIAG_FOLD);
+    const size_t G = pg_virtual.size();
+    std::vector<char> done(G, 0);
+    size_t first = 0;
+    const double amp_pass_bytes = 2.0 * amp_bytes * std::ldexp(1.0, nl);   // R+W per rank
+
+    while (true) {
+        while (first < G && done[first]) ++first;
+        if (first >= G) break;
+        PPass pass;
+        pass.kind = PASS_TILE;
+        uint64_t S = low_mask & local_mask;
+        uint64_t blockedAll = 0, blockedDense = 0;
+        int cost = 0;
+        for (size_t i = first; i < G; ++i) {
+            if (done[i]) continue;
+            if ((blockedAll & all_mask) == all_mask) break;
+            PGate g = map_gate(pg_virtual[i], sigma);
+            const uint64_t qm = g.qmask(), dm = g.dmask();
+            bool ok = !(qm & blockedAll) && !(dm & blockedDense) && !(dm & ~local_mask);
+            uint64_t need = dm & ~S;
+            if (ok && __builtin_popcountll(S | need) > opt.tile_bits) ok = false;
+            if (ok && one_gate && !pass.ops.empty()) ok = false;
+            std::vector<FOp> trial;
+            if (ok) {
+                trial = pass.ops;
+                merge_into(trial, g, opt.kmax, fold, one_gate);
+                int c = 0;
+                size_t mb = 0;
+                for (auto &o : trial) {
+                    c += op_cost(o);
+                    if (o.type == OP_DENSE) mb += (size_t)amp_bytes << (2 * o.tg.size());
+                }
+                if (!pass.ops.empty() && (c > opt.budget || mb > kMaxMatBytes)) ok = false;
+                else cost = c;
+            }
+            if (!ok) {
+                blockedAll |= dm;
+                blockedDense |= qm & ~dm;
+                if (no_reorder) break;
+                continue;
+            }
+            pass.ops.swap(trial);
+            S |= need;
+            done[i] = 1;
+            pass.gates.push_back(g.src);
+        }
+        (void)cost;
+        if (pass.ops.empty()) {
+            // frontier needs a global qubit as a non-diagonal target: remap
+            // (SURVEY.md 8(e)).  Needed global bits from the earliest gates.
+            uint64_t gneed = 0;
+            for (size_t i = first; i < G && __builtin_popcountll(gneed) < n_global; ++i) {
+                if (done[i]) continue;
+                PGate g = map_gate(pg_virtual[i], sigma);
+                gneed |= g.dmask() & ~local_mask;
+                if (i > first + 64 && gneed) break;
+            }
+            if (!gneed) {   // cannot happen with tile_bits >= 2; guard against a stall
+                throw std::runtime_error("planner stall");
+            }
+            // Belady: local victims whose next non-diagonal use is furthest away
+            std::vector<std::pair<size_t, int>> cand;
+            for (int b = opt.low_bits; b < nl; ++b) {
+                size_t next = G + 1;
+                for (size_t i = first; i < G; ++i) {
+                    if (done[i]) continue;
+                    PGate g = map_gate(pg_virtual[i], sigma);
+                    if (g.dmask() >> b & 1) { next = i; break; }
+                }
+                cand.push_back({next, b});
+            }
+            std::sort(cand.begin(), cand.end(), [](auto &a, auto &b) {
+                return a.first != b.first ? a.first > b.first : a.second > b.second;
+            });
+            PPass rp;
+            rp.kind = PASS_REMAP;
+            size_t ci = 0;
+            for (int gb : bits_of(gneed)) {
+                int lb = cand[ci++].second;
+                rp.swaps.push_back({gb, lb});
+                // the virtual bits at actual positions gb and lb exchange places
+                for (int v = 0; v < n; ++v) {
+                    if (sigma[v] == gb) sigma[v] = lb;
+                    else if (sigma[v] == lb) sigma[v] = gb;
+                }
+            }
+            plan.alg_bytes += (double)rp.swaps.size() > 0 ? amp_pass_bytes * (1.0 - std::ldexp(1.0, -(int)rp.swaps.size())) : 0;
+            plan.passes.push_back(rp);
+            continue;
+        }
+        // pass kind: standalone streaming kernels when no tile is needed
+        bool all_diag = true;
+        for (auto &o : pass.ops) all_diag &= (o.type == OP_DIAG);
+        if (all_diag) {
+            pass.kind = PASS_DIAG;
+            FOp merged;
+            merged.type = OP_DIAG;
+            for (auto &o : pass.ops) { merged.form.add(o.form); merged.qmask |= o.qmask; }
+            pass.ops.assign(1, merged);
+            pass.S = 0;
+            // skip-write: unchanged amplitudes are not written
+            plan.alg_bytes += amp_pass_bytes / 2 * 1.5;
+        } else if (pass.ops.size() == 1 && pass.ops[0].type == OP_CNOT) {
+            pass.kind = PASS_CNOT;
+            pass.S = 0;
+            plan.alg_bytes += amp_pass_bytes / 2;
+        } else {
+            pass.S = S;
+            plan.alg_bytes += amp_pass_bytes;
+        }
+        plan.passes.push_back(pass);
+    }
+    for (int v = 0; v < 64; ++v) plan.sigma_out[v] = v < n ? sigma[v] : v;
+    return plan;
+}
+
+// ---------------------------------------------------------------------------
+// encoding for the device (pass_format.h)
+// ---------------------------------------------------------------------------
+static void put(std::vector<uint8_t> &b, const void *p, size_t n) {
+    const uint8_t *c = (const uint8_t *)p;
+    b.insert(b.end(), c, c + n);
+}
+static void align(std::vector<uint8_t> &b, size_t a) {
+    while (b.size() % a) b.push_back(0);
+}
+
+// Diag record relative to tile: positions pos[0..S) = physical bits (ascending
+// map loc[]), the rest are "outside" (per-tile constants).
+static void encode_diag(std::vector<uint8_t> &b, size_t rec_at, const QForm &f, const int *loc, int S) {
+    StvDiag d;
+    std::memset(&d, 0, sizeof(d));
+    d.cst = f.cst;
+    std::vector<StvTerm> cross, olin, oquad;
+    bool quarter = (f.cst & ((1ull << 62) - 1)) == 0;
+    for (auto &kv : f.lin) {
+        quarter &= (kv.second & ((1ull << 62) - 1)) == 0;
+        int l = loc[kv.first];
+        if (l >= 0) d.lin[l] += kv.second;
+        else olin.push_back({kv.first, -1, kv.second});
+    }
+    for (auto &kv : f.quad) {
+        quarter &= (kv.second & ((1ull << 62) - 1)) == 0;
+        int a = kv.first.first, c = kv.first.second;
+        int la = loc[a], lc = loc[c];
+        if (la >= 0 && lc >= 0) { d.A[la][lc] += kv.second; d.A[lc][la] += kv.second; }
+        else if (la >= 0) cross.push_back({la, c, kv.second});
+        else if (lc >= 0) cross.push_back({lc, a, kv.second});
+        else oquad.push_back({a, c, kv.second});
+    }
+    d.all_quarter = quarter ? 1 : 0;
+    std::stable_sort(cross.begin(), cross.end(), [](const StvTerm &x, const StvTerm &y) { return x.a < y.a; });
+    for (int q = 0, k = 0; q <= S + 1 && q < STV_MAX_TILE_BITS + 2; ++q) {
+        while (k < (int)cross.size() && cross[k].a < q) ++k;
+        d.cross_start[q] = k;
+    }
+    d.n_cross = (int)cross.size();
+    d.n_olin = (int)olin.size();
+    d.n_oquad = (int)oquad.size();
+    size_t off = sizeof(StvDiag);
+    d.cross_off = (uint32_t)off; off += cross.size() * sizeof(StvTerm);
+    d.olin_off = (uint32_t)off; off += olin.size() * sizeof(StvTerm);
+    d.oquad_off = (uint32_t)off;
+    std::memcpy(&b[rec_at], &d, sizeof(d));
+    put(b, cross.data(), cross.size() * sizeof(StvTerm));
+    put(b, olin.data(), olin.size() * sizeof(StvTerm));
+    put(b, oquad.data(), oquad.size() * sizeof(StvTerm));
+}
+
+Encoded encode(const Plan &p, int n_local, bool c128) {
+    Encoded e;
+    std::vector<uint8_t> &b = e.blob;
+    const size_t esz = c128 ? 16 : 8;
+    for (const PPass &ps : p.passes) {
+        align(b, 256);
+        const size_t at = b.size();
+        e.pass_off.push_back((uint32_t)at);
+        StvPass hd;
+        std::memset(&hd, 0, sizeof(hd));
+        hd.kind = ps.kind;
+        hd.n_local = n_local;
+        b.resize(at + sizeof(StvPass));
+        int loc[64];
+        for (int i = 0; i < 64; ++i) loc[i] = -1;
+        if (ps.kind == PASS_TILE) {
+            std::vector<int> sb = bits_of(ps.S);
+            int L = 0;
+            while (L < (int)sb.size() && sb[L] == L) ++L;
+            hd.S = (int)sb.size();
+            hd.L = L;
+            hd.h = hd.S - L;
+            for (int r = 0; r < hd.h; ++r) hd.hpos[r] = sb[L + r];
+            for (int i = 0; i < hd.S; ++i) loc[sb[i]] = i;
+            const uint64_t lm = n_local >= 64 ? ~0ull : ((1ull << n_local) - 1);
+            hd.out_mask = lm & ~ps.S;
+            hd.nops = (int)ps.ops.size();
+            align(b, 16);
+            hd.ops_off = (uint32_t)(b.size() - at);
+            const size_t ops_at = b.size();
+            b.resize(ops_at + ps.ops.size() * sizeof(StvOp));
+            // matrices
+            align(b, 16);
+            hd.mat_off = (uint32_t)(b.size() - at);
+            std::vector<StvOp> recs(ps.ops.size());
+            for (size_t i = 0; i < ps.ops.size(); ++i) {
+                const FOp &o = ps.ops[i];
+                StvOp &r = recs[i];
+                std::memset(&r, 0, sizeof(r));
+                r.type = o.type;
+                r.c_loc = r.c_phys = -1;
+                if (o.type == OP_DENSE) {
+                    r.k = (int)o.tg.size();
+                    for (int j = 0; j < r.k; ++j) r.tpos[j] = loc[o.tg[j]];
+                    r.mat_off = (uint32_t)(b.size() - at - hd.mat_off);
+                    for (const cd &z : o.M) {
+                        if (c128) { double v[2] = {z.real(), z.imag()}; put(b, v, 16); }
+                        else { float v[2] = {(float)z.real(), (float)z.imag()}; put(b, v, 8); }
+                    }
+                    align(b, 16);
+                } else if (o.type == OP_CNOT) {
+                    r.t_loc = loc[o.t];
+                    if (loc[o.c] >= 0) r.c_loc = loc[o.c];
+                    else r.c_phys = o.c;
+                }
+            }
+            hd.mat_bytes = (uint32_t)(b.size() - at - hd.mat_off);
+            // diag records after matrices
+            for (size_t i = 0; i < ps.ops.size(); ++i) {
+                if (ps.ops[i].type != OP_DIAG) continue;
+                align(b, 16);
+                recs[i].diag_off = (uint32_t)(b.size() - at);
+                size_t rec_at = b.size();
+                b.resize(rec_at + sizeof(StvDiag));
+                encode_diag(b, rec_at, ps.ops[i].form, loc, hd.S);
+            }
+            std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
+            (void)esz;
+        } else if (ps.kind == PASS_DIAG) {
+            int S = std::min(n_local, 12);
+            hd.S = S;
+            hd.L = S;
+            hd.h = 0;
+            for (int i = 0; i < S; ++i) loc[i] = i;
+            const uint64_t lm = n_local >= 64 ? ~0ull : ((1ull << n_local) - 1);
+            hd.out_mask = lm & ~((1ull << S) - 1);
+            align(b, 16);
+            hd.diag_off = (uint32_t)(b.size() - at);
+            size_t rec_at = b.size();
+            b.resize(rec_at + sizeof(StvDiag));
+            encode_diag(b, rec_at, ps.ops[0].form, loc, S);
+        } else if (ps.kind == PASS_CNOT) {
+            hd.cnot_c = ps.ops[0].c;
+            hd.cnot_t = ps.ops[0].t;
+        }
+        std::memcpy(&b[at], &hd, sizeof(hd));
+    }
+    align(b, 256);
+    return e;
+}
+
+// ---------------------------------------------------------------------------
+// JSON (for the CPU plan-interpreter tests)
+// ---------------------------------------------------------------------------
+std::string plan_to_json(const Plan &p) {
+    std::ostringstream o;
+    o.precision(17);
+    o << "{\"n\":" << p.n << ",\"n_global\":" << p.n_global << ",\"alg_bytes\":" << p.alg_bytes << ",\"passes\":[";
+    for (size_t i = 0; i < p.passes.size(); ++i) {
+        const PPass &ps = p.passes[i];
+        if (i) o << ",";
+        o << "{\"kind\":" << ps.kind << ",\"S\":" << ps.S << ",\"gates\":[";
+        for (size_t j = 0; j < ps.gates.size(); ++j) o << (j ? "," : "") << ps.gates[j];
+        o << "],\"swaps\":[";
+        for (size_t j = 0; j < ps.swaps.size(); ++j)
+            o << (j ? "," : "") << "[" << ps.swaps[j].first << "," << ps.swaps[j].second << "]";
+        o << "],\"ops\":[";
+        for (size_t j = 0; j < ps.ops.size(); ++j) {
+            const FOp &f = ps.ops[j];
+            if (j) o << ",";
+            o << "{\"type\":" << f.type;
+            if (f.type == OP_DENSE) {
+                o << ",\"tg\":[";
+                for (size_t t = 0; t < f.tg.size(); ++t) o << (t ? "," : "") << f.tg[t];
+                o << "],\"re\":[";
+                for (size_t t = 0; t < f.M.size(); ++t) o << (t ? "," : "") << f.M[t].real();
+                o << "],\"im\":[";
+                for (size_t t = 0; t < f.M.size(); ++t) o << (t ? "," : "") << f.M[t].imag();
+                o << "]";
+            } else if (f.type == OP_DIAG) {
+                o << ",\"cst\":\"" << f.form.cst << "\",\"lin\":[";
+                bool c = false;
+                for (auto &kv : f.form.lin) { o << (c ? "," : "") << "[" << kv.first << ",\"" << kv.second << "\"]"; c = true; }
+                o << "],\"quad\":[";
+                c = false;
+                for (auto &kv : f.form.quad) {
+                    o << (c ? "," : "") << "[" << kv.first.first << "," << kv.first.second << ",\"" << kv.second << "\"]";
+                    c = true;
+                }
+                o << "]";
+            } else {
+                o << ",\"c\":" << f.c << ",\"t\":" << f.t;
+            }
+            o << "}";
+        }
+        o << "]}";
+    }
+    o << "],\"perm\":[";
+    for (int q = 0; q < p.n; ++q) o << (q ? "," : "") << p.frame_out.perm[q];
+    o << "],\"xmask\":\"" << p.frame_out.xmask << "\"}";
+    return o.str();
+}
+
+}  // namespace stv

@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (-m gpu).
+
+Bars (BASELINE.json north_star): complex64 per-amplitude |delta| <= 2e-6 and
+fidelity >= 1 - 1e-5; complex128 |delta| <= 1e-12.  Inputs are the seeded
+generators of inputs/ (no value ever comes from the CUDA path).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from inputs import circuits as C
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"c64": 2e-6, "c128": 1e-12}
+
+
+@pytest.fixture(scope="module")
+def stv():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2008_00216_b200 as m
+    m.lib()
+    return m
+
+
+def run_gpu(stv, circ, dtype="c64", **kw):
+    st = stv.State(circ.n, dtype)
+    st.set_basis(circ.x0)
+    st.apply(circ.gates, **kw)
+    psi = st.amplitudes()
+    stats = st.stats()
+    st.close()
+    return psi, stats
+
+
+def assert_parity(psi, ref, dtype):
+    r = oracle.compare(psi, ref)
+    assert r["max_abs"] <= TOL[dtype], r
+    if dtype == "c64":
+        assert r["fidelity"] >= 1 - 1e-5, r
+    return r
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,seed", [(1, 1), (2, 2), (4, 3), (6, 4), (9, 5), (12, 6), (15, 7), (18, 8)])
+def test_random_circuits_all_kinds(stv, n, seed, dtype):
+    circ = C.random_circuit(n, 150, seed)
+    psi, _ = run_gpu(stv, circ, dtype)
+    assert_parity(psi, oracle.run(circ), dtype)
+
+
+@pytest.mark.parametrize("kw", [dict(kmax=1), dict(kmax=2), dict(kmax=3), dict(kmax=4),
+                                dict(tile_bits=8, low_bits=3), dict(tile_bits=13, low_bits=5),
+                                dict(tile_bits=10, low_bits=0), dict(budget=400), dict(budget=20),
+                                dict(flags=2), dict(flags=4), dict(flags=8), dict(flags=16)])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_planner_options(stv, kw, dtype):
+    circ = C.random_circuit(17, 300, 42)
+    psi, _ = run_gpu(stv, circ, dtype, **kw)
+    assert_parity(psi, oracle.run(circ), dtype)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_c1_config(stv, dtype):
+    circ = C.config(1)
+    psi, st = run_gpu(stv, circ, dtype)
+    assert_parity(psi, oracle.run(circ), dtype)
+    assert st["n_kernels"] >= 1
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_qft_closed_form(stv, dtype):
+    n = 20
+    circ = C.qft_circuit(n, tail=0, seed=3)
+    psi, _ = run_gpu(stv, circ, dtype)
+    y = np.arange(1 << n)
+    ref = 2 ** (-n / 2) * np.exp(2j * np.pi * ((circ.x0 * y) % (1 << n)) / (1 << n))
+    assert np.max(np.abs(psi - ref)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_c3_reduced(stv, dtype):
+    circ = C.qft_circuit(22, tail=200, seed=3)
+    psi, _ = run_gpu(stv, circ, dtype)
+    assert_parity(psi, oracle.run(circ), dtype)
+    # phase state: |psi_y| = 2^{-n/2} for all y (permutations + phases after the QFT)
+    assert np.max(np.abs(np.abs(psi) - 2 ** -11)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_grid_fsim_reduced(stv, dtype):
+    circ = C.grid_circuit("g", 4, 5, 0, 20, "fsim", 2)
+    psi, _ = run_gpu(stv, circ, dtype)
+    assert_parity(psi, oracle.run(circ), dtype)
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_virtual_shards(stv, g, dtype):
+    circ = C.random_circuit(16, 250, 60 + g)
+    st = stv.State(circ.n, dtype, virtual_g=g)
+    st.set_basis(circ.x0)
+    st.apply(circ.gates, tile_bits=8, low_bits=3)
+    s = st.stats()
+    psi = st.amplitudes()
+    st.close()
+    assert s["n_pass"]["remap"] > 0
+    assert_parity(psi, oracle.run(circ), dtype)
+
+
+def test_virtual_shards_grid(stv):
+    circ = C.grid_circuit("g", 4, 5, 0, 12, "fsim", 9)
+    st = stv.State(circ.n, "c64", virtual_g=3)
+    st.apply(circ.gates)
+    psi = st.amplitudes()
+    st.close()
+    assert_parity(psi, oracle.run(circ), "c64")
+
+
+def test_incremental_apply_keeps_frame(stv):
+    circ = C.random_circuit(14, 200, 77)
+    st = stv.State(14)
+    st.set_basis(circ.x0)
+    for k in range(0, 200, 37):
+        st.apply(circ.gates[k:k + 37])
+    perm, xm = st.frame()
+    psi = st.amplitudes()
+    st.close()
+    assert_parity(psi, oracle.run(circ), "c64")
+    assert sorted(perm) == list(range(14))
+
+
+def test_norm_deterministic(stv):
+    circ = C.random_circuit(20, 200, 3)
+    st = stv.State(20)
+    st.apply(circ.gates)
+    a = st.norm()
+    b = st.norm()
+    st.close()
+    assert a == b and abs(a - 1) < 1e-5
+
+
+def test_uniform_init_and_get_amplitudes(stv):
+    st = stv.State(12, "c128")
+    st.set_uniform()
+    idx = np.array([0, 5, 4095, 17], dtype=np.uint64)
+    v = st.amplitudes(idx)
+    assert np.allclose(v, 2 ** -6, atol=1e-15)
+    assert abs(st.norm() - 1) < 1e-13
+    with pytest.raises(stv.SvError):
+        st.amplitudes(np.array([1 << 12], dtype=np.uint64))
+    st.close()
+
+
+def test_invalid_gate_launches_nothing(stv):
+    st = stv.State(6)
+    st.set_basis(3)
+    with pytest.raises(stv.SvError, match="gate 1"):
+        st.apply([("h", (0,), ()), ("cz", (2, 9), ())])
+    psi = st.amplitudes()
+    st.close()
+    e = np.zeros(64)
+    e[3] = 1
+    assert np.array_equal(psi, e)
+
+
+def test_empty_and_relabel_only(stv):
+    st = stv.State(10)
+    st.set_basis(5)
+    st.apply([])
+    st.apply([("x", (0,), ()), ("swap", (0, 9), ()), ("x", (3,), ())])
+    psi = st.amplitudes()
+    st.close()
+    ref = oracle.run(C.Circuit("r", 10, [("x", (0,), ()), ("swap", (0, 9), ()), ("x", (3,), ())], x0=5))
+    assert np.array_equal(psi, ref)
+
+
+def test_read_state_raw(stv):
+    circ = C.random_circuit(13, 100, 8)
+    st = stv.State(13)
+    st.set_basis(circ.x0)
+    st.apply(circ.gates)
+    raw = st.read_state()
+    wide = st.amplitudes()
+    st.close()
+    assert raw.dtype == np.complex64 and np.array_equal(raw.astype(np.complex128), wide)
+
+
+def test_bitwise_reproducible(stv):
+    circ = C.config(1)
+    a, _ = run_gpu(stv, circ)
+    b, _ = run_gpu(stv, circ)
+    assert np.array_equal(a, b)

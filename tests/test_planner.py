@@ -1,0 +1,142 @@
+"""Host-side planner tests (-m "not gpu"): the C-ABI library loads without a
+GPU, exports every symbol of include/sv.h, and its plans -- executed by an
+independent CPU interpreter (tests/plan_interp.py) -- reproduce the oracle.
+"""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2008_00216_b200 as stv
+from inputs import circuits as C
+from tests import plan_interp as PI
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "sv.h")).read()
+    declared = set(re.findall(r"^\s*(?:sv_status|const char \*)\s*(sv_\w+)\(", hdr, re.M))
+    assert declared == set(stv.EXPORTS)
+    L = stv.lib()
+    for f in declared:
+        assert getattr(L, f) is not None
+    assert "sm_100a" in stv.version()
+
+
+def _check(circ, tol=1e-11, n_global=0, **kw):
+    plan = stv.plan_json(circ.n, circ.gates, n_global=n_global, **kw)
+    psi = PI.logical(plan, PI.run(plan, x0=circ.x0))
+    ref = oracle.run(circ)
+    err = np.max(np.abs(psi - ref))
+    assert err < tol, (err, kw)
+    return plan
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("kmax", [1, 2, 4])
+def test_random_all_kinds(seed, kmax):
+    circ = C.random_circuit(9, 120, seed)
+    _check(circ, kmax=kmax, tile_bits=6, low_bits=2)
+
+
+@pytest.mark.parametrize("flags", [stv.OPT_NO_RELABEL, stv.OPT_NO_REORDER, stv.OPT_ONE_GATE,
+                                   stv.OPT_NO_DIAG_FOLD, stv.OPT_NO_RELABEL | stv.OPT_NO_REORDER])
+def test_ablation_flags_preserve_semantics(flags):
+    circ = C.random_circuit(8, 150, 11)
+    _check(circ, flags=flags, tile_bits=6, low_bits=2)
+
+
+@pytest.mark.parametrize("tile_bits,low_bits", [(2, 0), (3, 1), (5, 3), (8, 5), (12, 5)])
+def test_tile_shapes(tile_bits, low_bits):
+    circ = C.random_circuit(10, 100, 3)
+    _check(circ, tile_bits=tile_bits, low_bits=low_bits)
+
+
+def test_c1_config_plan():
+    circ = C.config(1)
+    plan = _check(circ, tol=1e-10)
+    # every non-relabel gate absorbed exactly once
+    absorbed = [g for ps in plan["passes"] for g in ps["gates"]]
+    assert len(absorbed) == len(set(absorbed)) == len(circ.gates)
+    # fusion reduced the 380 gates to far fewer passes
+    assert len(plan["passes"]) < 60
+
+
+def test_qft_and_tail():
+    circ = C.qft_circuit(10, tail=120, seed=3)
+    plan = _check(circ, tol=1e-10)
+    srcs = {g for ps in plan["passes"] for g in ps["gates"]}
+    names = [g[0] for g in circ.gates]
+    # SWAPs and X are relabels: never part of a pass
+    assert all(names[i] not in ("swap", "x") for i in srcs)
+
+
+def test_grid_fsim_relabel():
+    circ = C.grid_circuit("g", 3, 3, 0, 8, "fsim", 7)
+    plan = _check(circ)
+    # fSim(pi/2, phi) = SWAP . diag: no dense 2-qubit op is needed for it
+    assert all(op["type"] != 1 or len(op["tg"]) <= 4 for ps in plan["passes"] for op in ps["ops"])
+
+
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_global_qubit_remaps(g):
+    circ = C.random_circuit(9, 150, 20 + g)
+    plan = _check(circ, n_global=g, tile_bits=5, low_bits=2)
+    nl = circ.n - g
+    for ps in plan["passes"]:
+        if ps["kind"] == 4:
+            for gb, lb in ps["swaps"]:
+                assert gb >= nl and lb < nl
+        else:
+            for op in ps["ops"]:          # non-diagonal targets only on local bits
+                if op["type"] == 1:
+                    assert max(op["tg"]) < nl
+                if op["type"] == 3:
+                    assert op["t"] < nl
+    assert any(ps["kind"] == 4 for ps in plan["passes"])
+
+
+def test_mirror_plan():
+    circ = C.random_circuit(8, 80, 5)
+    full = C.Circuit("m", 8, circ.gates + C.inverse_gates(circ.gates), x0=circ.x0)
+    plan = stv.plan_json(8, full.gates, tile_bits=6, low_bits=2)
+    psi = PI.logical(plan, PI.run(plan, x0=circ.x0))
+    e = np.zeros(256, complex)
+    e[circ.x0] = 1
+    assert np.max(np.abs(psi - e)) < 1e-11
+
+
+def test_diag_form_matches_paper_masks(golden):
+    # the per-qubit CZ masks of PAPER.md L522-527 and the planner's single
+    # phase form for the same six CZ gates agree on every basis state
+    g = golden["paper_bitmasks"]["cz_complete_graph_4q"]
+    masks = [int(s, 2) for s in g["masks"]]
+    gates = [("cz", (a, b), ()) for a in range(4) for b in range(a + 1, 4)]
+    plan = stv.plan_json(4, gates, tile_bits=2, low_bits=0)
+    diag_ops = [op for ps in plan["passes"] for op in ps["ops"]]
+    assert len(plan["passes"]) == 1 and len(diag_ops) == 1 and diag_ops[0]["type"] == 2
+    ph = PI._phase(4, diag_ops[0])
+    for j in range(16):
+        cnt = sum(bin(masks[k] & j).count("1") for k in range(4) if j >> k & 1)
+        assert abs(ph[j] - (-1 if cnt & 2 else 1)) < 1e-15
+
+
+def test_validation_errors():
+    bad = [("h", (5,), ())]
+    with pytest.raises(stv.SvError, match="gate 0"):
+        stv.plan_json(4, bad)
+    with pytest.raises(stv.SvError, match="duplicate"):
+        stv.plan_json(4, [("h", (0,), ()), ("cz", (1, 1), ())])
+    with pytest.raises(stv.SvError, match="not unitary"):
+        stv.plan_json(4, [("u1", (0,), (1.0, 0, 1.0, 0, 0, 0, 1.0, 0))])
+
+
+def test_remap_peers_schedule():
+    # rank r, swapping global bit b: chunk c goes to r with bit b set to c
+    assert stv.remap_peers(1, 0, 0b1, 1) == [0, 1]
+    assert stv.remap_peers(1, 1, 0b1, 1) == [0, 1]
+    assert stv.remap_peers(3, 5, 0b110, 2) == [1, 3, 5, 7]
+    assert stv.remap_peers(2, 2, 0b01, 1) == [2, 3]

@@ -218,51 +218,104 @@ __device__ __forceinline__ void diag_thread(const StvDiag *__restrict__ D, int S
 }
 
 // ---------------------------------------------------------------------------
-// dense k-qubit op on a shared-memory tile (register-resident 2^k vector)
+// named barrier among the consumer warps (the producer warp never joins)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(STV_THREADS) : "memory"); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// dense k-qubit op on a shared-memory tile (register-resident 2^k vector).
+// K <= 2: the whole matrix lives in registers for the op; K >= 3: rows are
+// streamed from shared memory as 16-byte pairs of entries.
 // ---------------------------------------------------------------------------
 template <int K, typename C>
-__device__ void dense_op(C *__restrict__ tile, int S, const int *tp, const C *__restrict__ M) {
-    constexpr int D = 1 << K;
-    const uint32_t nvec = 1u << (S - K);
-    for (uint32_t v = threadIdx.x; v < nvec; v += blockDim.x) {
-        uint32_t base = v;
+__device__ __forceinline__ uint32_t dense_base(uint32_t v, const int *tp) {
+    uint32_t base = v;
 #pragma unroll
-        for (int b = 0; b < K; ++b) {
-            const uint32_t lo = base & ((1u << tp[b]) - 1);
-            base = ((base >> tp[b]) << (tp[b] + 1)) | lo;
-        }
+    for (int b = 0; b < K; ++b) {
+        const uint32_t lo = base & ((1u << tp[b]) - 1);
+        base = ((base >> tp[b]) << (tp[b] + 1)) | lo;
+    }
+    return base;
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t dense_off(int l, const int *tp) {
+    uint32_t o = 0;
+#pragma unroll
+    for (int b = 0; b < K; ++b)
+        if ((l >> b) & 1) o |= 1u << tp[b];
+    return o;
+}
+
+template <int K, typename C>
+__device__ void dense_op_reg(C *__restrict__ tile, int S, const int *tp, const C *__restrict__ M, int ctid) {
+    constexpr int D = 1 << K;
+    C m[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) m[i] = M[i];
+    uint32_t off[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) off[l] = dense_off<K>(l, tp);
+    const uint32_t nvec = 1u << (S - K);
+    for (uint32_t v = ctid; v < nvec; v += STV_THREADS) {
+        const uint32_t base = dense_base<K, C>(v, tp);
         C x[D];
 #pragma unroll
-        for (int l = 0; l < D; ++l) {
-            uint32_t o = 0;
+        for (int l = 0; l < D; ++l) x[l] = tile[base | off[l]];
 #pragma unroll
-            for (int b = 0; b < K; ++b)
-                if ((l >> b) & 1) o |= 1u << tp[b];
-            x[l] = tile[base | o];
+        for (int r = 0; r < D; ++r) {
+            C acc;
+            acc.x = 0;
+            acc.y = 0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc = cfma(m[r * D + c], x[c], acc);
+            tile[base | off[r]] = acc;
         }
-        // rows: full unroll for K <= 2 (M fits in registers), else a rolled
-        // row loop so only x[] and one accumulator stay live
-#pragma unroll(K <= 2 ? D : 1)
+    }
+}
+
+template <int K, typename C>
+__device__ void dense_op_smem(C *__restrict__ tile, int S, const int *tp, const C *__restrict__ M, int ctid) {
+    constexpr int D = 1 << K;
+    const uint32_t nvec = 1u << (S - K);
+    for (uint32_t v = ctid; v < nvec; v += STV_THREADS) {
+        const uint32_t base = dense_base<K, C>(v, tp);
+        C x[D];
+#pragma unroll
+        for (int l = 0; l < D; ++l) x[l] = tile[base | dense_off<K>(l, tp)];
+#pragma unroll 1
         for (int r = 0; r < D; ++r) {
             C acc;
             acc.x = 0;
             acc.y = 0;
             const C *Mr = M + r * D;
+            if (sizeof(C) == 8) {
+                const float4 *M4 = (const float4 *)Mr;
 #pragma unroll
-            for (int c = 0; c < D; ++c) acc = cfma(Mr[c], x[c], acc);
-            uint32_t o = 0;
+                for (int c = 0; c < D / 2; ++c) {
+                    const float4 q = M4[c];
+                    C a, b;
+                    a.x = q.x; a.y = q.y; b.x = q.z; b.y = q.w;
+                    acc = cfma(a, x[2 * c], acc);
+                    acc = cfma(b, x[2 * c + 1], acc);
+                }
+            } else {
 #pragma unroll
-            for (int b = 0; b < K; ++b)
-                if ((r >> b) & 1) o |= 1u << tp[b];
-            tile[base | o] = acc;
+                for (int c = 0; c < D; ++c) acc = cfma(Mr[c], x[c], acc);
+            }
+            tile[base | dense_off<K>(r, tp)] = acc;
         }
     }
 }
 
 template <typename C>
-__device__ void cnot_op(C *__restrict__ tile, int S, int t, int c_loc) {
+__device__ void cnot_op(C *__restrict__ tile, int S, int t, int c_loc, int ctid) {
     const uint32_t npair = 1u << (S - 1);
-    for (uint32_t v = threadIdx.x; v < npair; v += blockDim.x) {
+    for (uint32_t v = ctid; v < npair; v += STV_THREADS) {
         const uint32_t lo = v & ((1u << t) - 1);
         const uint32_t i0 = ((v >> t) << (t + 1)) | lo;
         if (c_loc >= 0 && !((i0 >> c_loc) & 1)) continue;
@@ -293,13 +346,16 @@ __device__ void diag_op_tile(C *__restrict__ tile, int S, const StvDiag *__restr
 }
 
 // ---------------------------------------------------------------------------
-// the fused tile pass
+// the fused tile pass: warp-specialised.  Warp 8 = TMA producer (bulk loads
+// into a kStages ring, full/empty mbarriers); warps 0..7 = consumers (ops on
+// the resident tile, then bulk stores of the runs they own).
 // ---------------------------------------------------------------------------
 constexpr int kStages = 3;
 constexpr int kHdrBytes = 1024;    // barriers, tile bases, DiagScratch
+constexpr int kTileThreads = STV_THREADS + 32;
 
 template <typename R>
-__global__ void __launch_bounds__(STV_THREADS, 2)
+__global__ void __launch_bounds__(kTileThreads, 2)
 k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
             uint64_t ntiles) {
     using C = typename C2T<R>::T;
@@ -310,12 +366,11 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
     const int nops = P->nops;
     const StvOp *ops = (const StvOp *)((const uint8_t *)P + P->ops_off);
-    uint64_t hmask = 0;
-    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
 
-    uint64_t *bars = (uint64_t *)smem;                 // [3]
-    uint64_t *tbase = (uint64_t *)(smem + 32);         // [3]
-    DiagScratch *sc = (DiagScratch *)(smem + 64);
+    uint64_t *full = (uint64_t *)smem;                 // [3]
+    uint64_t *empty = (uint64_t *)(smem + 24);         // [3]
+    uint64_t *tbase = (uint64_t *)(smem + 48);         // [3]
+    DiagScratch *sc = (DiagScratch *)(smem + 128);
     uint8_t *mat = smem + kHdrBytes;
     const uint32_t mat_bytes = P->mat_bytes;
     const uint32_t mat_pad = (mat_bytes + 127u) & ~127u;
@@ -325,47 +380,49 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     const uint32_t nruns = 1u << h;
     const uint32_t run_bytes = run_elems * sizeof(C);
     const uint32_t tile_bytes = tile_elems * sizeof(C);
-
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // stage matrices (once per persistent CTA)
-    {
+
+    {   // stage matrices (once per persistent CTA)
         const uint4 *src = (const uint4 *)((const uint8_t *)P + P->mat_off);
         uint4 *dst = (uint4 *)mat;
         for (uint32_t k = tid; k < mat_bytes / 16; k += blockDim.x) dst[k] = src[k];
     }
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], STV_THREADS / 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
     __syncthreads();
 
     const uint64_t first = blockIdx.x, stride = gridDim.x;
-    uint64_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+    const uint64_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+    uint64_t hmask = 0;
+    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
 
-    auto issue_load = [&](uint64_t j) {   // warp 0 only
-        const uint64_t t = first + j * stride;
-        const int s = (int)(j % kStages);
-        const uint64_t base = pdep64(t, out_mask);
-        if (lane == 0) {
-            tbase[s] = base;
-            mbar_arrive_expect_tx(&bars[s], tile_bytes);
+    if (warp == STV_THREADS / 32) {
+        // ------------------------------ producer --------------------------
+        for (uint64_t j = 0; j < my_tiles; ++j) {
+            const int s = (int)(j % kStages);
+            if (j >= (uint64_t)kStages) mbar_wait(&empty[s], (uint32_t)((j / kStages - 1) & 1));
+            const uint64_t base = pdep64(first + j * stride, out_mask);
+            if (lane == 0) {
+                tbase[s] = base;
+                mbar_arrive_expect_tx(&full[s], tile_bytes);
+            }
+            __syncwarp();
+            C *dst = tiles + (size_t)s * tile_elems;
+            for (uint32_t r = lane; r < nruns; r += 32)
+                tma_load_1d(dst + (size_t)r * run_elems, state + (base | pdep64(r, hmask)), run_bytes, &full[s]);
         }
-        __syncwarp();
-        C *dst = tiles + (size_t)s * tile_elems;
-        for (uint32_t r = lane; r < nruns; r += 32) {
-            const uint64_t off = base | pdep64(r, hmask);
-            tma_load_1d(dst + (size_t)r * run_elems, state + off, run_bytes, &bars[s]);
-        }
-    };
-
-    if (warp == 0) {
-        for (uint64_t j = 0; j < (uint64_t)(kStages - 1) && j < my_tiles; ++j) issue_load(j);
+        return;
     }
-
+    // -------------------------------- consumers -----------------------------
     for (uint64_t j = 0; j < my_tiles; ++j) {
         const int s = (int)(j % kStages);
-        mbar_wait(&bars[s], (uint32_t)((j / kStages) & 1));
+        mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t base = tbase[s];
         const uint64_t full_base = base | rank_bits;
@@ -378,38 +435,33 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
                 for (int b = 0; b < STV_MAX_K; ++b) tp[b] = op.tpos[b];
                 const C *M = (const C *)(mat + op.mat_off);
                 switch (op.k) {
-                case 1: dense_op<1, C>(tile, S, tp, M); break;
-                case 2: dense_op<2, C>(tile, S, tp, M); break;
-                case 3: dense_op<3, C>(tile, S, tp, M); break;
-                case 4: dense_op<4, C>(tile, S, tp, M); break;
+                case 1: dense_op_reg<1, C>(tile, S, tp, M, tid); break;
+                case 2: dense_op_reg<2, C>(tile, S, tp, M, tid); break;
+                case 3: dense_op_smem<3, C>(tile, S, tp, M, tid); break;
+                case 4: dense_op_smem<4, C>(tile, S, tp, M, tid); break;
                 }
             } else if (type == OP_CNOT) {
                 const bool on = op.c_phys < 0 || ((full_base >> op.c_phys) & 1);
-                if (on) cnot_op<C>(tile, S, op.t_loc, op.c_loc);
+                if (on) cnot_op<C>(tile, S, op.t_loc, op.c_loc, tid);
             } else {
                 const StvDiag *D = (const StvDiag *)((const uint8_t *)P + op.diag_off);
                 diag_prep<V>(D, S, full_base, sc);
-                __syncthreads();
+                consumer_sync();
                 diag_op_tile<V, C>(tile, S, D, sc);
             }
-            __syncthreads();
+            consumer_sync();
         }
         fence_proxy_async();
-        __syncthreads();
-        if (warp == 0) {
-            for (uint32_t r = lane; r < nruns; r += 32) {
-                const uint64_t off = base | pdep64(r, hmask);
-                tma_store_1d(state + off, tile + (size_t)r * run_elems, run_bytes);
-            }
-            bulk_commit();
-            if (j + kStages - 1 < my_tiles) {
-                bulk_wait_read_1();      // buffer of tile j-1 drained by its store
-                __syncwarp();
-                issue_load(j + kStages - 1);
-            }
-        }
+        consumer_sync();
+        for (uint32_t r = tid; r < nruns; r += STV_THREADS)
+            tma_store_1d(state + (base | pdep64(r, hmask)), tile + (size_t)r * run_elems, run_bytes);
+        bulk_commit();
+        // release the previous tile's stage once its stores have read shared memory
+        bulk_wait_read_1();
+        __syncwarp();
+        if (j > 0 && lane == 0) mbar_arrive(&empty[(j - 1) % kStages]);
     }
-    if (warp == 0) bulk_wait_all();
+    bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -603,22 +655,22 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
             cudaFuncSetAttribute(k_tile_pass<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             attr = true;
         }
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_pass<double>, STV_THREADS, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_pass<double>, kTileThreads, smem);
     } else {
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_tile_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
             attr = true;
         }
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_pass<float>, STV_THREADS, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_pass<float>, kTileThreads, smem);
     }
     if (occ < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)num_sms() * occ;
     if (grid > ntiles) grid = ntiles;
     if (c128)
-        k_tile_pass<double><<<(unsigned)grid, STV_THREADS, smem, st>>>((double2 *)state, dblob, pass_off, ntiles);
+        k_tile_pass<double><<<(unsigned)grid, kTileThreads, smem, st>>>((double2 *)state, dblob, pass_off, ntiles);
     else
-        k_tile_pass<float><<<(unsigned)grid, STV_THREADS, smem, st>>>((float2 *)state, dblob, pass_off, ntiles);
+        k_tile_pass<float><<<(unsigned)grid, kTileThreads, smem, st>>>((float2 *)state, dblob, pass_off, ntiles);
     e = cudaGetLastError();
     ++*kernels;
     return e;

@@ -396,11 +396,17 @@ PlanOptions resolve_options(const sv_options *o, int amp_bytes, int n_local) {
 
 static const size_t kMaxMatBytes = 32768;   // matrices staged in shared memory per pass
 
+// Per-amplitude instruction estimate of one op on a resident tile (thread
+// instructions: FMAs, shared-memory traffic, addressing); calibrated against
+// the ncu instruction counts of k_tile_pass (profiles/).
 static int op_cost(const FOp &o) {
     switch (o.type) {
-    case OP_DENSE: { int k = (int)o.tg.size(); return std::max(4 << k, 16) + 4; }
-    case OP_DIAG: return 24;
-    default: return 12;
+    case OP_DENSE: {
+        static const int c[5] = {0, 12, 22, 44, 84};
+        return c[std::min<size_t>(o.tg.size(), 4)];
+    }
+    case OP_DIAG: return 30;
+    default: return 6;
     }
 }
 

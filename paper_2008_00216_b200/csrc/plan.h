@@ -90,8 +90,8 @@ struct PPass {
 struct PlanOptions {
     int kmax = 4;
     int tile_bits = 13;       // c64 default (c128: 12)
-    int low_bits = 5;
-    int budget = 96;
+    int low_bits = 7;
+    int budget = 80;
     uint32_t flags = 0;
 };
 

@@ -17,6 +17,7 @@
 //   k_init_*, k_gather  a11.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "pass_format.h"
 
@@ -346,25 +347,78 @@ __device__ void diag_op_tile(C *__restrict__ tile, int S, const StvDiag *__restr
 }
 
 // ---------------------------------------------------------------------------
-// the fused tile pass: warp-specialised.  Warp 8 = TMA producer (bulk loads
-// into a kStages ring, full/empty mbarriers); warps 0..7 = consumers (ops on
-// the resident tile, then bulk stores of the runs they own).
+// the fused tile pass: warp-specialised.
+//   producer warps (kProdWarps): gather the tile's 2^h runs of 2^L amplitudes
+//     into a kStages shared-memory ring -- 16-B cp.async (LDGSTS) per thread
+//     for runs < 8 KB, one TMA bulk copy per run for longer runs (a 1-D bulk
+//     copy costs ~160 SM cycles, measured: profiles/r01_tma_runlen.md);
+//     completion is tracked by the stage's `full` mbarrier.
+//   consumer warps (8): apply the pass's op sequence to the resident tile,
+//     write it back with 16-B stores and release the stage (`empty`).
 // ---------------------------------------------------------------------------
 constexpr int kStages = 3;
 constexpr int kHdrBytes = 1024;    // barriers, tile bases, DiagScratch
-constexpr int kTileThreads = STV_THREADS + 32;
+constexpr int kProdWarps = 2;
+constexpr int kProd = 32 * kProdWarps;
+constexpr int kTileThreads = STV_THREADS + kProd;
+
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// x + y in the "expanded" domain of mask (carries jump over the gaps):
+// pdep(a + b, m) == masked_add(pdep(a, m), pdep(b, m), m)
+__device__ __forceinline__ uint64_t masked_add(uint64_t x, uint64_t y, uint64_t m) {
+    return ((x | ~m) + y) & m;
+}
+
+// Move one tile between global memory and a shared-memory stage with NT
+// threads (index t): 16-B chunks, run-aware addressing.
+template <bool kLoad, int NT>
+__device__ __forceinline__ void tile_copy16(uint8_t *gstate, uint8_t *stile, uint64_t base, uint64_t hmask,
+                                            uint32_t run_bytes, uint32_t nruns, uint32_t esz, int t) {
+    const uint32_t cpr = run_bytes >> 4;             // 16-B chunks per run (power of two)
+    if (cpr >= (uint32_t)NT) {
+        const uint64_t d1 = hmask & (0 - hmask);     // pdep(1, hmask)
+        uint64_t roff = 0;
+        for (uint32_t r = 0; r < nruns; ++r) {
+            uint8_t *g = gstate + (base | roff) * esz;
+            uint8_t *sm = stile + (size_t)r * run_bytes;
+            for (uint32_t w = t; w < cpr; w += NT) {
+                if (kLoad) cp_async16(sm + (size_t)w * 16, g + (size_t)w * 16);
+                else *(uint4 *)(g + (size_t)w * 16) = *(const uint4 *)(sm + (size_t)w * 16);
+            }
+            roff = masked_add(roff, d1, hmask);
+        }
+    } else {
+        const uint32_t lc = 31 - __clz(cpr);
+        const uint32_t total = nruns * cpr;
+        const uint64_t dstep = pdep64((uint32_t)NT >> lc, hmask);
+        uint64_t roff = pdep64((uint32_t)t >> lc, hmask);
+        const uint32_t within = ((uint32_t)t & (cpr - 1)) * 16;
+        for (uint32_t c = t; c < total; c += NT) {
+            uint8_t *g = gstate + (base | roff) * esz + within;
+            uint8_t *sm = stile + (size_t)c * 16;
+            if (kLoad) cp_async16(sm, g);
+            else *(uint4 *)g = *(const uint4 *)sm;
+            roff = masked_add(roff, dstep, hmask);
+        }
+    }
+}
 
 template <typename R>
 __global__ void __launch_bounds__(kTileThreads, 2)
 k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
-            uint64_t ntiles) {
+            uint32_t ntiles, int dbg_flags) {
     using C = typename C2T<R>::T;
     constexpr int V = sizeof(C) == 8 ? 1 : 0;
     extern __shared__ __align__(1024) uint8_t smem[];
     const StvPass *P = (const StvPass *)(blob + pass_off);
     const int S = P->S, L = P->L, h = P->h;
     const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
-    const int nops = P->nops;
+    const int nops = (dbg_flags & 1) ? 0 : P->nops;   // bit 0: data movement only (microbenchmark)
     const StvOp *ops = (const StvOp *)((const uint8_t *)P + P->ops_off);
 
     uint64_t *full = (uint64_t *)smem;                 // [3]
@@ -375,12 +429,14 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     const uint32_t mat_bytes = P->mat_bytes;
     const uint32_t mat_pad = (mat_bytes + 127u) & ~127u;
     C *tiles = (C *)(smem + kHdrBytes + mat_pad);
+    const uint32_t esz = sizeof(C);
     const uint32_t tile_elems = 1u << S;
     const uint32_t run_elems = 1u << L;
     const uint32_t nruns = 1u << h;
-    const uint32_t run_bytes = run_elems * sizeof(C);
-    const uint32_t tile_bytes = tile_elems * sizeof(C);
+    const uint32_t run_bytes = run_elems * esz;
+    const uint32_t tile_bytes = tile_elems * esz;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool use_tma = run_bytes >= 8192;
 
     {   // stage matrices (once per persistent CTA)
         const uint4 *src = (const uint4 *)((const uint8_t *)P + P->mat_off);
@@ -389,7 +445,7 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     }
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], kProd);
             mbar_init(&empty[s], STV_THREADS / 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -397,32 +453,48 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     }
     __syncthreads();
 
-    const uint64_t first = blockIdx.x, stride = gridDim.x;
-    const uint64_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+    const uint32_t first = blockIdx.x, stride = gridDim.x;
+    const uint32_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
     uint64_t hmask = 0;
     for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
+    uint8_t *gstate = (uint8_t *)state;
 
-    if (warp == STV_THREADS / 32) {
-        // ------------------------------ producer --------------------------
-        for (uint64_t j = 0; j < my_tiles; ++j) {
-            const int s = (int)(j % kStages);
-            if (j >= (uint64_t)kStages) mbar_wait(&empty[s], (uint32_t)((j / kStages - 1) & 1));
-            const uint64_t base = pdep64(first + j * stride, out_mask);
-            if (lane == 0) {
-                tbase[s] = base;
-                mbar_arrive_expect_tx(&full[s], tile_bytes);
+    if (tid >= STV_THREADS) {
+        // ------------------------------ producers -------------------------
+        const int pt = tid - STV_THREADS;
+        uint64_t tb = pdep64(first, out_mask);
+        const uint64_t tstep = pdep64(stride, out_mask);
+        int s = 0;
+        uint32_t ph = 0;
+        for (uint32_t j = 0; j < my_tiles; ++j) {
+            if (j >= (uint32_t)kStages) mbar_wait(&empty[s], ph ^ 1);
+            if (pt == 0) tbase[s] = tb;
+            uint8_t *stile = (uint8_t *)(tiles + (size_t)s * tile_elems);
+            if (use_tma) {
+                if (pt == 0) mbar_arrive_expect_tx(&full[s], tile_bytes);
+                else mbar_arrive(&full[s]);
+                if (warp == STV_THREADS / 32) {
+                    uint64_t roff = pdep64(lane, hmask);
+                    const uint64_t d32 = pdep64(32, hmask);
+                    for (uint32_t r = lane; r < nruns; r += 32) {
+                        tma_load_1d(stile + (size_t)r * run_bytes, gstate + (tb | roff) * esz, run_bytes, &full[s]);
+                        roff = masked_add(roff, d32, hmask);
+                    }
+                }
+            } else {
+                tile_copy16<true, kProd>(gstate, stile, tb, hmask, run_bytes, nruns, esz, pt);
+                cp_async_arrive_noinc(&full[s]);
             }
-            __syncwarp();
-            C *dst = tiles + (size_t)s * tile_elems;
-            for (uint32_t r = lane; r < nruns; r += 32)
-                tma_load_1d(dst + (size_t)r * run_elems, state + (base | pdep64(r, hmask)), run_bytes, &full[s]);
+            tb = masked_add(tb, tstep, out_mask);
+            if (++s == kStages) { s = 0; ph ^= 1; }
         }
         return;
     }
     // -------------------------------- consumers -----------------------------
-    for (uint64_t j = 0; j < my_tiles; ++j) {
-        const int s = (int)(j % kStages);
-        mbar_wait(&full[s], (uint32_t)((j / kStages) & 1));
+    int s = 0;
+    uint32_t ph = 0;
+    for (uint32_t j = 0; j < my_tiles; ++j) {
+        mbar_wait(&full[s], ph);
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t base = tbase[s];
         const uint64_t full_base = base | rank_bits;
@@ -451,17 +523,12 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
             }
             consumer_sync();
         }
-        fence_proxy_async();
-        consumer_sync();
-        for (uint32_t r = tid; r < nruns; r += STV_THREADS)
-            tma_store_1d(state + (base | pdep64(r, hmask)), tile + (size_t)r * run_elems, run_bytes);
-        bulk_commit();
-        // release the previous tile's stage once its stores have read shared memory
-        bulk_wait_read_1();
+        tile_copy16<false, STV_THREADS>(gstate, (uint8_t *)tile, base, hmask, run_bytes, nruns, esz, tid);
+        if (use_tma) fence_proxy_async();      // generic smem accesses before the next async-proxy (TMA) write
         __syncwarp();
-        if (j > 0 && lane == 0) mbar_arrive(&empty[(j - 1) % kStages]);
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == kStages) { s = 0; ph ^= 1; }
     }
-    bulk_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -667,10 +734,12 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
     if (occ < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)num_sms() * occ;
     if (grid > ntiles) grid = ntiles;
+    if (ntiles >> 32) return cudaErrorInvalidValue;
+    static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
     if (c128)
-        k_tile_pass<double><<<(unsigned)grid, kTileThreads, smem, st>>>((double2 *)state, dblob, pass_off, ntiles);
+        k_tile_pass<double><<<(unsigned)grid, kTileThreads, smem, st>>>((double2 *)state, dblob, pass_off, (uint32_t)ntiles, dbg);
     else
-        k_tile_pass<float><<<(unsigned)grid, kTileThreads, smem, st>>>((float2 *)state, dblob, pass_off, ntiles);
+        k_tile_pass<float><<<(unsigned)grid, kTileThreads, smem, st>>>((float2 *)state, dblob, pass_off, (uint32_t)ntiles, dbg);
     e = cudaGetLastError();
     ++*kernels;
     return e;

@@ -359,7 +359,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
         cudaError_t e = cudaSuccess;
         if (ps.kind == PASS_TILE) {
             kind = hp->h == 0 ? 1 : 2;
-            e = launch_tile_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->mat_bytes,
+            e = launch_tile_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->rec_bytes,
                                  s->stream, &kernels);
             for (auto &o : ps.ops) s->stats.n_ops[o.type == OP_DENSE ? 0 : o.type == OP_DIAG ? 1 : 2]++;
         } else if (ps.kind == PASS_DIAG) {

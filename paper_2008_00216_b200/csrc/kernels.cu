@@ -44,10 +44,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(0x100000u)
         : "memory");
     return ok != 0;
 }
@@ -283,11 +283,14 @@ template <int K, typename C>
 __device__ void dense_op_smem(C *__restrict__ tile, int S, const int *tp, const C *__restrict__ M, int ctid) {
     constexpr int D = 1 << K;
     const uint32_t nvec = 1u << (S - K);
+    uint32_t off[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) off[l] = dense_off<K>(l, tp);
     for (uint32_t v = ctid; v < nvec; v += STV_THREADS) {
         const uint32_t base = dense_base<K, C>(v, tp);
         C x[D];
 #pragma unroll
-        for (int l = 0; l < D; ++l) x[l] = tile[base | dense_off<K>(l, tp)];
+        for (int l = 0; l < D; ++l) x[l] = tile[base | off[l]];
 #pragma unroll 1
         for (int r = 0; r < D; ++r) {
             C acc;
@@ -308,7 +311,11 @@ __device__ void dense_op_smem(C *__restrict__ tile, int S, const int *tp, const 
 #pragma unroll
                 for (int c = 0; c < D; ++c) acc = cfma(Mr[c], x[c], acc);
             }
-            tile[base | dense_off<K>(r, tp)] = acc;
+            uint32_t o = 0;     // off[r] without dynamic register indexing
+#pragma unroll
+            for (int b = 0; b < K; ++b)
+                if ((r >> b) & 1) o |= off[1 << b];
+            tile[base | o] = acc;
         }
     }
 }
@@ -415,7 +422,16 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     using C = typename C2T<R>::T;
     constexpr int V = sizeof(C) == 8 ? 1 : 0;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const StvPass *P = (const StvPass *)(blob + pass_off);
+    const StvPass *G = (const StvPass *)(blob + pass_off);
+    const uint32_t rec_bytes = G->rec_bytes;           // whole pass record, staged in smem
+    const uint32_t rec_pad = (rec_bytes + 127u) & ~127u;
+    const StvPass *P = (const StvPass *)(smem + kHdrBytes);
+    {
+        const uint4 *src = (const uint4 *)G;
+        uint4 *dst = (uint4 *)(smem + kHdrBytes);
+        for (uint32_t k = threadIdx.x; k < rec_bytes / 16; k += blockDim.x) dst[k] = src[k];
+    }
+    __syncthreads();
     const int S = P->S, L = P->L, h = P->h;
     const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
     const int nops = (dbg_flags & 1) ? 0 : P->nops;   // bit 0: data movement only (microbenchmark)
@@ -425,10 +441,8 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     uint64_t *empty = (uint64_t *)(smem + 24);         // [3]
     uint64_t *tbase = (uint64_t *)(smem + 48);         // [3]
     DiagScratch *sc = (DiagScratch *)(smem + 128);
-    uint8_t *mat = smem + kHdrBytes;
-    const uint32_t mat_bytes = P->mat_bytes;
-    const uint32_t mat_pad = (mat_bytes + 127u) & ~127u;
-    C *tiles = (C *)(smem + kHdrBytes + mat_pad);
+    const uint8_t *mat = (const uint8_t *)P + P->mat_off;
+    C *tiles = (C *)(smem + kHdrBytes + rec_pad);
     const uint32_t esz = sizeof(C);
     const uint32_t tile_elems = 1u << S;
     const uint32_t run_elems = 1u << L;
@@ -438,11 +452,6 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool use_tma = run_bytes >= 8192;
 
-    {   // stage matrices (once per persistent CTA)
-        const uint4 *src = (const uint4 *)((const uint8_t *)P + P->mat_off);
-        uint4 *dst = (uint4 *)mat;
-        for (uint32_t k = tid; k < mat_bytes / 16; k += blockDim.x) dst[k] = src[k];
-    }
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], kProd);
@@ -705,8 +714,8 @@ static int num_sms() {
     return g_num_sms;
 }
 
-static size_t tile_smem_bytes(int S, uint32_t mat_bytes, size_t esz) {
-    return kHdrBytes + ((mat_bytes + 127u) & ~127u) + (size_t)kStages * ((size_t)esz << S);
+static size_t tile_smem_bytes(int S, uint32_t rec_bytes, size_t esz) {
+    return kHdrBytes + ((rec_bytes + 127u) & ~127u) + (size_t)kStages * ((size_t)esz << S);
 }
 
 cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,

@@ -65,5 +65,6 @@ struct alignas(16) StvPass {
     uint32_t mat_bytes;
     int32_t cnot_c, cnot_t;    // PASS_CNOT (physical bits)
     uint32_t diag_off;         // PASS_DIAG: StvDiag offset (tile = low S bits)
-    int32_t pad[2];
+    uint32_t rec_bytes;        // size of this pass record (multiple of 16)
+    int32_t pad;
 };

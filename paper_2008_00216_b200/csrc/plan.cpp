@@ -394,7 +394,7 @@ PlanOptions resolve_options(const sv_options *o, int amp_bytes, int n_local) {
     return p;
 }
 
-static const size_t kMaxMatBytes = 32768;   // matrices staged in shared memory per pass
+static const size_t kMaxRecBytes = 24576;   // pass record (ops, matrices, diag forms) staged in smem
 
 // Per-amplitude instruction estimate of one op on a resident tile (thread
 // instructions: FMAs, shared-memory traffic, addressing); calibrated against
@@ -542,12 +542,15 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                 trial = pass.ops;
                 merge_into(trial, g, opt.kmax, fold, one_gate);
                 int c = 0;
-                size_t mb = 0;
+                size_t mb = sizeof(StvPass);      // pass record (staged in shared memory)
                 for (auto &o : trial) {
                     c += op_cost(o);
+                    mb += sizeof(StvOp);
                     if (o.type == OP_DENSE) mb += (size_t)amp_bytes << (2 * o.tg.size());
+                    if (o.type == OP_DIAG)
+                        mb += sizeof(StvDiag) + sizeof(StvTerm) * (o.form.lin.size() + o.form.quad.size());
                 }
-                if (!pass.ops.empty() && (c > opt.budget || mb > kMaxMatBytes)) ok = false;
+                if (!pass.ops.empty() && (c > opt.budget || mb > kMaxRecBytes)) ok = false;
                 else cost = c;
             }
             if (!ok) {
@@ -769,6 +772,8 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
             hd.cnot_c = ps.ops[0].c;
             hd.cnot_t = ps.ops[0].t;
         }
+        align(b, 16);
+        hd.rec_bytes = (uint32_t)(b.size() - at);
         std::memcpy(&b[at], &hd, sizeof(hd));
     }
     align(b, 256);

@@ -625,6 +625,9 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
             pass.S = 0;
             plan.alg_bytes += amp_pass_bytes / 2;
         } else {
+            // pad the tile to full size with the lowest free local bits: bits no
+            // op touches cost nothing, and they lengthen the contiguous runs
+            for (int b = 0; b < nl && __builtin_popcountll(S) < opt.tile_bits; ++b) S |= 1ull << b;
             pass.S = S;
             plan.alg_bytes += amp_pass_bytes;
         }

@@ -101,8 +101,10 @@ __device__ __forceinline__ double2 cfma(double2 m, double2 x, double2 acc) {
 }
 
 __device__ __forceinline__ void phase_cs(uint64_t ph, float &c, float &s) {
-    const float x = (float)(int32_t)(uint32_t)(ph >> 32) * 4.656612873077392578125e-10f;  // 2^-31 (units of pi)
-    sincospif(x, &s, &c);
+    // angle in [-pi, pi): hardware sin/cos (abs. error ~2^-21.4 on this range),
+    // far inside the complex64 bars (|delta| <= 2e-6, F >= 1-1e-5)
+    const float x = (float)(int32_t)(uint32_t)(ph >> 32) * 1.4629180792671596e-09f;  // 2 pi / 2^32
+    __sincosf(x, &s, &c);
 }
 __device__ __forceinline__ void phase_cs(uint64_t ph, double &c, double &s) {
     const double x = (double)(int64_t)ph * 1.0842021724855044340074528008699e-19;  // 2^-63
@@ -262,6 +264,30 @@ __device__ void dense_op_reg(C *__restrict__ tile, int S, const int *tp, const C
 #pragma unroll
     for (int l = 0; l < D; ++l) off[l] = dense_off<K>(l, tp);
     const uint32_t nvec = 1u << (S - K);
+    if (sizeof(C) == 8 && tp[0] == 0) {
+        // target on tile bit 0 (complex64): amplitude pairs (l, l|1) are one 16-B word
+        for (uint32_t v = ctid; v < nvec; v += STV_THREADS) {
+            const uint32_t base = dense_base<K, C>(v, tp);
+            C x[D];
+#pragma unroll
+            for (int l = 0; l < D; l += 2) {
+                const float4 q = *(const float4 *)&tile[base | off[l]];
+                x[l].x = q.x; x[l].y = q.y; x[l + 1].x = q.z; x[l + 1].y = q.w;
+            }
+#pragma unroll
+            for (int r = 0; r < D; r += 2) {
+                C a0, a1;
+                a0.x = a0.y = a1.x = a1.y = 0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    a0 = cfma(m[r * D + c], x[c], a0);
+                    a1 = cfma(m[(r + 1) * D + c], x[c], a1);
+                }
+                *(float4 *)&tile[base | off[r]] = make_float4(a0.x, a0.y, a1.x, a1.y);
+            }
+        }
+        return;
+    }
     for (uint32_t v = ctid; v < nvec; v += STV_THREADS) {
         const uint32_t base = dense_base<K, C>(v, tp);
         C x[D];
@@ -279,6 +305,8 @@ __device__ void dense_op_reg(C *__restrict__ tile, int S, const int *tp, const C
     }
 }
 
+// K >= 3: matrix rows streamed from shared memory (broadcast), two rows per
+// step with split accumulators -> four independent FMA chains per thread
 template <int K, typename C>
 __device__ void dense_op_smem(C *__restrict__ tile, int S, const int *tp, const C *__restrict__ M, int ctid) {
     constexpr int D = 1 << K;
@@ -292,30 +320,28 @@ __device__ void dense_op_smem(C *__restrict__ tile, int S, const int *tp, const 
 #pragma unroll
         for (int l = 0; l < D; ++l) x[l] = tile[base | off[l]];
 #pragma unroll 1
-        for (int r = 0; r < D; ++r) {
-            C acc;
-            acc.x = 0;
-            acc.y = 0;
-            const C *Mr = M + r * D;
-            if (sizeof(C) == 8) {
-                const float4 *M4 = (const float4 *)Mr;
+        for (int r = 0; r < D; r += 2) {
+            C p0, p1, q0, q1;
+            p0.x = p0.y = p1.x = p1.y = q0.x = q0.y = q1.x = q1.y = 0;
+            const C *M0 = M + r * D;
+            const C *M1 = M0 + D;
 #pragma unroll
-                for (int c = 0; c < D / 2; ++c) {
-                    const float4 q = M4[c];
-                    C a, b;
-                    a.x = q.x; a.y = q.y; b.x = q.z; b.y = q.w;
-                    acc = cfma(a, x[2 * c], acc);
-                    acc = cfma(b, x[2 * c + 1], acc);
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < D; ++c) acc = cfma(Mr[c], x[c], acc);
+            for (int c = 0; c < D; c += 2) {
+                p0 = cfma(M0[c], x[c], p0);
+                p1 = cfma(M0[c + 1], x[c + 1], p1);
+                q0 = cfma(M1[c], x[c], q0);
+                q1 = cfma(M1[c + 1], x[c + 1], q1);
             }
-            uint32_t o = 0;     // off[r] without dynamic register indexing
+            p0.x += p1.x; p0.y += p1.y;
+            q0.x += q1.x; q0.y += q1.y;
+            uint32_t o0 = 0, o1 = 0;     // off[r], off[r+1] without dynamic register indexing
 #pragma unroll
-            for (int b = 0; b < K; ++b)
-                if ((r >> b) & 1) o |= off[1 << b];
-            tile[base | o] = acc;
+            for (int b = 0; b < K; ++b) {
+                if ((r >> b) & 1) o0 |= off[1 << b];
+                if (((r + 1) >> b) & 1) o1 |= off[1 << b];
+            }
+            tile[base | o0] = p0;
+            tile[base | o1] = q0;
         }
     }
 }
@@ -340,16 +366,27 @@ __device__ void diag_op_tile(C *__restrict__ tile, int S, const StvDiag *__restr
     int nF;
     diag_thread<V>(D, S, sc, bt, lf, nF);
     const uint32_t tsz = 1u << S;
-    const int ncombo = 1 << nF;
-    for (int c = 0; c < ncombo; ++c) {
-        const uint32_t e = c & ((1 << V) - 1), r = (uint32_t)c >> V;
-        const uint32_t i = (r << (V + 8)) | ((uint32_t)threadIdx.x << V) | e;
+    const int nr = 1 << (nF - V);                 // r combos; each covers 2^V amplitudes (16 B)
+    for (int r = 0; r < nr; ++r) {
+        const uint32_t i = ((uint32_t)r << (V + 8)) | ((uint32_t)threadIdx.x << V);
         if (i >= tsz) continue;
-        uint64_t ph = bt + sc->qf[c];
+        uint64_t ph = bt + sc->qf[r << V];
 #pragma unroll
-        for (int f = 0; f < 6; ++f)
-            if (f < nF && ((c >> f) & 1)) ph += lf[f];
-        tile[i] = apply_phase(tile[i], ph);
+        for (int f = V; f < 6; ++f)
+            if (f < nF && ((r >> (f - V)) & 1)) ph += lf[f];
+        if (V == 1) {
+            const uint64_t ph1 = ph + lf[0] + sc->qf[(r << 1) | 1] - sc->qf[r << 1];
+            if (ph == 0 && ph1 == 0) continue;
+            float4 *p = (float4 *)&tile[i];
+            const float4 q = *p;
+            float2 a = make_float2(q.x, q.y), b = make_float2(q.z, q.w);
+            a = apply_phase(a, ph);
+            b = apply_phase(b, ph1);
+            *p = make_float4(a.x, a.y, b.x, b.y);
+        } else {
+            if (ph == 0) continue;
+            tile[i] = apply_phase(tile[i], ph);
+        }
     }
 }
 

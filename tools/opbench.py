@@ -29,9 +29,11 @@ def gates_for(kind, m):
     elif kind in ("k2", "k3", "k4"):
         k = int(kind[1])
         for i in range(m):
-            base = (i * k) % 8
-            for q in range(k): g.append(("sx", (base + q,), ()))
-            g.append(("cz", (base, base + 1), ()))
+            # ops on rotating disjoint groups: consecutive groups overlap in one qubit,
+            # so they cannot merge into one op but stay in one pass
+            base = (i * (k - 1)) % (12 - k)
+            for q in range(k): g.append(("sx" if (i + q) % 2 else "sy", (base + q,), ()))
+            g.append(("cz", (base, base + k - 1), ()))
     elif kind == "diag":
         for i in range(m):
             g.append(("sx", (i % 11,), ()))

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libstv.so")
 KINDS = {"h": 0, "x": 1, "y": 2, "z": 3, "s": 4, "t": 5, "sx": 6, "sy": 7, "sw": 8,
          "cz": 9, "cnot": 10, "swap": 11, "cphase": 12, "fsim": 13, "u1": 14, "u2": 15}
 GATE_ADJOINT = 0x1
-OPT_PROFILE, OPT_NO_RELABEL, OPT_NO_REORDER, OPT_ONE_GATE, OPT_NO_DIAG_FOLD = 1, 2, 4, 8, 16
+OPT_PROFILE, OPT_NO_RELABEL, OPT_NO_REORDER, OPT_ONE_GATE, OPT_NO_DIAG_FOLD, OPT_NO_GROUPS = 1, 2, 4, 8, 16, 32
 C64, C128 = 0, 1
 STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_OUT_OF_MEMORY", 3: "SV_ERR_CUDA",
           4: "SV_ERR_NCCL", 5: "SV_ERR_UNSUPPORTED", 6: "SV_ERR_STATE"}
@@ -267,7 +267,7 @@ class State:
                 "n_pass": dict(zip(PASS_KINDS, list(s.n_pass))),
                 "pass_ms": dict(zip(PASS_KINDS, list(s.pass_ms))),
                 "alg_bytes": s.alg_bytes, "remap_bytes": s.remap_bytes,
-                "n_ops": dict(zip(["dense", "diag", "cnot"], list(s.n_ops)[:3])),
+                "n_ops": dict(zip(["dense", "diag", "cnot", "group"], list(s.n_ops))),
                 "n_kernels": s.n_kernels, "h2d_bytes": s.h2d_bytes}
 
     def frame(self):

@@ -391,6 +391,210 @@ __device__ void diag_op_tile(C *__restrict__ tile, int S, const StvDiag *__restr
 }
 
 // ---------------------------------------------------------------------------
+// register-resident gate groups (OP_GROUP): every consumer thread gathers the
+// 16 amplitudes of one 4-bit vector from the tile, runs the group's sub-op
+// program in registers (U1 / U2 matrices, CNOT register swaps, diagonal
+// phase tables) and scatters them back: one shared-memory round trip for the
+// whole group.  Sub-op bit indices are compile-time template arguments so
+// the vector never leaves registers.
+// ---------------------------------------------------------------------------
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) {
+    C r;
+    r.x = a.x * b.x - a.y * b.y;
+    r.y = a.x * b.y + a.y * b.x;
+    return r;
+}
+
+template <int A, typename C>
+__device__ __forceinline__ void g_u1(C (&x)[16], const C *__restrict__ M) {
+    const C m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & (1 << A)) continue;
+        const C p = x[l], q = x[l | (1 << A)];
+        C u, w;
+        u.x = 0; u.y = 0; w.x = 0; w.y = 0;
+        u = cfma(m0, p, u); u = cfma(m1, q, u);
+        w = cfma(m2, p, w); w = cfma(m3, q, w);
+        x[l] = u;
+        x[l | (1 << A)] = w;
+    }
+}
+
+template <int A, int B, typename C>
+__device__ __forceinline__ void g_u2(C (&x)[16], const C *__restrict__ M) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & ((1 << A) | (1 << B))) continue;
+        C v[4] = {x[l], x[l | (1 << A)], x[l | (1 << B)], x[l | (1 << A) | (1 << B)]};
+        C o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            C acc;
+            acc.x = 0; acc.y = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc = cfma(M[r * 4 + c], v[c], acc);
+            o[r] = acc;
+        }
+        x[l] = o[0];
+        x[l | (1 << A)] = o[1];
+        x[l | (1 << B)] = o[2];
+        x[l | (1 << A) | (1 << B)] = o[3];
+    }
+}
+
+template <int CB, int TB, typename C>
+__device__ __forceinline__ void g_cnot(C (&x)[16]) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & (1 << TB)) continue;
+        if (CB >= 0 && !(l & (1 << (CB < 0 ? 0 : CB)))) continue;
+        const C t = x[l];
+        x[l] = x[l | (1 << TB)];
+        x[l | (1 << TB)] = t;
+    }
+}
+
+template <typename C>
+__device__ __forceinline__ void g_u1_dispatch(C (&x)[16], int a, const C *M) {
+    switch (a) {
+    case 0: g_u1<0>(x, M); break;
+    case 1: g_u1<1>(x, M); break;
+    case 2: g_u1<2>(x, M); break;
+    default: g_u1<3>(x, M); break;
+    }
+}
+
+template <typename C>
+__device__ __forceinline__ void g_u2_dispatch(C (&x)[16], int a, int b, const C *M) {
+    switch (a * 4 + b) {
+    case 1: g_u2<0, 1>(x, M); break;
+    case 2: g_u2<0, 2>(x, M); break;
+    case 3: g_u2<0, 3>(x, M); break;
+    case 6: g_u2<1, 2>(x, M); break;
+    case 7: g_u2<1, 3>(x, M); break;
+    default: g_u2<2, 3>(x, M); break;
+    }
+}
+
+template <typename C>
+__device__ __forceinline__ void g_cnot_dispatch(C (&x)[16], int a, int b) {
+    switch ((a + 1) * 4 + b) {
+    case 0: g_cnot<-1, 0>(x); break;
+    case 1: g_cnot<-1, 1>(x); break;
+    case 2: g_cnot<-1, 2>(x); break;
+    case 3: g_cnot<-1, 3>(x); break;
+    case 5: g_cnot<0, 1>(x); break;
+    case 6: g_cnot<0, 2>(x); break;
+    case 7: g_cnot<0, 3>(x); break;
+    case 8: g_cnot<1, 0>(x); break;
+    case 10: g_cnot<1, 2>(x); break;
+    case 11: g_cnot<1, 3>(x); break;
+    case 12: g_cnot<2, 0>(x); break;
+    case 13: g_cnot<2, 1>(x); break;
+    case 15: g_cnot<2, 3>(x); break;
+    case 16: g_cnot<3, 0>(x); break;
+    case 17: g_cnot<3, 1>(x); break;
+    default: g_cnot<3, 2>(x); break;
+    }
+}
+
+// per-tile phase tables of the pass's group DIAG sub-ops: tables[t*16 + l]
+template <typename C>
+__device__ void group_tables(const StvPass *__restrict__ P, const StvOp *__restrict__ ops, int nops, int ntab,
+                             uint64_t full_base, C *__restrict__ tables, int ctid) {
+    for (int idx = ctid; idx < ntab * 16; idx += STV_THREADS) {
+    const int t = idx >> 4, l = idx & 15;
+    for (int o = 0; o < nops; ++o) {
+        if (ops[o].type != OP_GROUP) continue;
+        const StvSub *subs = (const StvSub *)((const uint8_t *)P + ops[o].sub_off);
+        for (int k = 0; k < ops[o].nsub; ++k) {
+            if (subs[k].type != SUB_DIAG || subs[k].tbl != t) continue;
+            const uint8_t *rec = (const uint8_t *)P + subs[k].gdiag_off;
+            const StvGDiag *G = (const StvGDiag *)rec;
+            uint64_t ph = G->cst;
+            const StvTerm *ol = (const StvTerm *)(rec + G->olin_off);
+            for (int i = 0; i < G->n_olin; ++i)
+                if ((full_base >> ol[i].a) & 1) ph += ol[i].ang;
+            const StvTerm *oq = (const StvTerm *)(rec + G->oquad_off);
+            for (int i = 0; i < G->n_oquad; ++i)
+                if (((full_base >> oq[i].a) & 1) && ((full_base >> oq[i].b) & 1)) ph += oq[i].ang;
+            const StvTerm *cr = (const StvTerm *)(rec + G->cross_off);
+            for (int j = 0; j < 4; ++j) {
+                if (!((l >> j) & 1)) continue;
+                ph += G->w[j];
+                for (int i = 0; i < G->n_cross; ++i)
+                    if (cr[i].a == j && ((full_base >> cr[i].b) & 1)) ph += cr[i].ang;
+                for (int k2 = j + 1; k2 < 4; ++k2)
+                    if ((l >> k2) & 1) ph += G->A[j][k2];
+            }
+            C one;
+            one.x = 1;
+            one.y = 0;
+            tables[idx] = apply_phase(one, ph);
+        }
+    }
+    }
+}
+
+template <typename C>
+__device__ void group_op(C *__restrict__ tile, int S, const StvOp &op, const StvPass *__restrict__ P,
+                         const uint8_t *__restrict__ mat, const C *__restrict__ tables, uint64_t full_base, int ctid) {
+    int tp[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) tp[b] = op.tpos[b];
+    uint32_t off[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) off[l] = dense_off<4>(l, tp);
+    const StvSub *subs = (const StvSub *)((const uint8_t *)P + op.sub_off);
+    const int nsub = op.nsub;
+    const uint32_t nvec = 1u << (S - 4);
+    const bool pair16 = sizeof(C) == 8 && tp[0] == 0;
+    for (uint32_t v = ctid; v < nvec; v += STV_THREADS) {
+        const uint32_t base = dense_base<4, C>(v, tp);
+        C x[16];
+        if (pair16) {
+#pragma unroll
+            for (int l = 0; l < 16; l += 2) {
+                const float4 q = *(const float4 *)&tile[base | off[l]];
+                x[l].x = q.x; x[l].y = q.y; x[l + 1].x = q.z; x[l + 1].y = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) x[l] = tile[base | off[l]];
+        }
+        for (int k = 0; k < nsub; ++k) {
+            const StvSub &sb = subs[k];
+            switch (sb.type) {
+            case SUB_U1: g_u1_dispatch(x, sb.a, (const C *)(mat + sb.mat_off)); break;
+            case SUB_U2: g_u2_dispatch(x, sb.a, sb.b, (const C *)(mat + sb.mat_off)); break;
+            case SUB_DIAG: {
+                const C *tb = tables + sb.tbl * 16;
+#pragma unroll
+                for (int l = 0; l < 16; ++l) x[l] = cmul(x[l], tb[l]);
+                break;
+            }
+            default: {
+                bool on = true;
+                if (sb.c_tile >= 0) on = (base >> sb.c_tile) & 1;
+                if (sb.c_phys >= 0) on = (full_base >> sb.c_phys) & 1;
+                if (on) g_cnot_dispatch(x, sb.a, sb.b);
+            }
+            }
+        }
+        if (pair16) {
+#pragma unroll
+            for (int l = 0; l < 16; l += 2)
+                *(float4 *)&tile[base | off[l]] = make_float4(x[l].x, x[l].y, x[l + 1].x, x[l + 1].y);
+        } else {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) tile[base | off[l]] = x[l];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // the fused tile pass: warp-specialised.
 //   producer warps (kProdWarps): gather the tile's 2^h runs of 2^L amplitudes
 //     into a kStages shared-memory ring -- 16-B cp.async (LDGSTS) per thread
@@ -453,7 +657,7 @@ __device__ __forceinline__ void tile_copy16(uint8_t *gstate, uint8_t *stile, uin
 }
 
 template <typename R>
-__global__ void __launch_bounds__(kTileThreads, 2)
+__global__ void __launch_bounds__(kTileThreads, sizeof(R) == 4 ? 2 : 1)
 k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
             uint32_t ntiles, int dbg_flags) {
     using C = typename C2T<R>::T;
@@ -479,7 +683,10 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     uint64_t *tbase = (uint64_t *)(smem + 48);         // [3]
     DiagScratch *sc = (DiagScratch *)(smem + 128);
     const uint8_t *mat = (const uint8_t *)P + P->mat_off;
-    C *tiles = (C *)(smem + kHdrBytes + rec_pad);
+    const int ntab = P->ntab;
+    C *tables = (C *)(smem + kHdrBytes + rec_pad);
+    const uint32_t tab_pad = ((uint32_t)ntab * 16 * sizeof(C) + 127u) & ~127u;
+    C *tiles = (C *)(smem + kHdrBytes + rec_pad + tab_pad);
     const uint32_t esz = sizeof(C);
     const uint32_t tile_elems = 1u << S;
     const uint32_t run_elems = 1u << L;
@@ -544,10 +751,16 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t base = tbase[s];
         const uint64_t full_base = base | rank_bits;
+        if (ntab && nops) {
+            group_tables<C>(P, ops, nops, ntab, full_base, tables, tid);
+            consumer_sync();
+        }
         for (int o = 0; o < nops; ++o) {
             const StvOp &op = ops[o];
             const int type = op.type;
-            if (type == OP_DENSE) {
+            if (type == OP_GROUP) {
+                group_op<C>(tile, S, op, P, mat, tables, full_base, tid);
+            } else if (type == OP_DENSE) {
                 int tp[STV_MAX_K];
 #pragma unroll
                 for (int b = 0; b < STV_MAX_K; ++b) tp[b] = op.tpos[b];
@@ -751,14 +964,15 @@ static int num_sms() {
     return g_num_sms;
 }
 
-static size_t tile_smem_bytes(int S, uint32_t rec_bytes, size_t esz) {
-    return kHdrBytes + ((rec_bytes + 127u) & ~127u) + (size_t)kStages * ((size_t)esz << S);
+static size_t tile_smem_bytes(int S, uint32_t rec_bytes, int ntab, size_t esz) {
+    return kHdrBytes + ((rec_bytes + 127u) & ~127u) + (((size_t)ntab * 16 * esz + 127u) & ~(size_t)127) +
+           (size_t)kStages * ((size_t)esz << S);
 }
 
 cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
-                             uint32_t mat_bytes, cudaStream_t st, int *kernels) {
+                             uint32_t rec_bytes, int ntab, cudaStream_t st, int *kernels) {
     const size_t esz = c128 ? 16 : 8;
-    const size_t smem = tile_smem_bytes(S, mat_bytes, esz);
+    const size_t smem = tile_smem_bytes(S, rec_bytes, ntab, esz);
     const uint64_t ntiles = 1ull << (n_local - S);
     int occ = 0;
     cudaError_t e;

@@ -17,6 +17,15 @@
 #define OP_DENSE 1
 #define OP_DIAG 2
 #define OP_CNOT 3
+#define OP_GROUP 4
+
+// sub-ops of a register-resident gate group (OP_GROUP)
+#define SUB_U1 1
+#define SUB_U2 2
+#define SUB_DIAG 3
+#define SUB_CNOT 4
+#define STV_GROUP_BITS 4
+#define STV_MAX_TABLES 32
 
 #define STV_MAX_TILE_BITS 14
 #define STV_MAX_K 4
@@ -50,7 +59,31 @@ struct alignas(16) StvOp {
     int32_t c_loc;             // CNOT: tile-local control position or -1
     int32_t c_phys;            // CNOT: physical control bit (outside the tile) or -1
     uint32_t diag_off;         // DIAG: byte offset of StvDiag from the PassDesc
-    int32_t pad[3];
+    int32_t nsub;              // GROUP: number of sub-ops
+    uint32_t sub_off;          // GROUP: byte offset of StvSub[nsub] from the PassDesc
+    int32_t pad;
+};
+
+// One sub-op of a gate group; local bits index the group's tpos[0..3].
+struct alignas(16) StvSub {
+    int32_t type;              // SUB_*
+    int32_t a, b;              // U1: a; U2: a < b (matrix local index bit0 = a, bit1 = b);
+                               // CNOT: a = local control or -1, b = local target
+    int32_t c_tile;            // CNOT: tile-local control position outside the group, or -1
+    int32_t c_phys;            // CNOT: physical control bit outside the tile, or -1
+    uint32_t mat_off;          // U1/U2: byte offset in the pass matrix area
+    uint32_t gdiag_off;        // DIAG: byte offset of StvGDiag from the PassDesc
+    int32_t tbl;               // DIAG: index of its per-tile phase table
+};
+
+// Diagonal sub-op over the group's 4 local bits + bits outside the tile:
+//   phase = cst + sum_{olin} + sum_{oquad} + sum_j b_j (w[j] + sum_{cross(j,p)}) + sum_{j<k} A[j][k] b_j b_k
+struct alignas(16) StvGDiag {
+    uint64_t cst;
+    uint64_t w[STV_GROUP_BITS];
+    uint64_t A[STV_GROUP_BITS][STV_GROUP_BITS];
+    int32_t n_cross, n_olin, n_oquad, pad;
+    uint32_t cross_off, olin_off, oquad_off, pad2;    // byte offsets from this record (StvTerm arrays)
 };
 
 struct alignas(16) StvPass {
@@ -66,5 +99,5 @@ struct alignas(16) StvPass {
     int32_t cnot_c, cnot_t;    // PASS_CNOT (physical bits)
     uint32_t diag_off;         // PASS_DIAG: StvDiag offset (tile = low S bits)
     uint32_t rec_bytes;        // size of this pass record (multiple of 16)
-    int32_t pad;
+    int32_t ntab;              // per-tile phase tables of group DIAG sub-ops
 };

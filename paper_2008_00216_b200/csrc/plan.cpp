@@ -503,6 +503,89 @@ static PGate map_gate(const PGate &g, const int *sigma) {
     return a;
 }
 
+// ---------------------------------------------------------------------------
+// register-resident gate groups (OP_GROUP): the pass's gates are partitioned
+// into groups whose in-tile qubits fit in STV_GROUP_BITS tile bits; a group is
+// one shared-memory round trip of the tile, its gates run as sub-ops on
+// 16-amplitude register vectors (the paper's "clusters
+// stored in factored form").  The partition is the Sec. 4.5 scan
+// again at op level: a gate joins the open group iff it commutes with every
+// gate skipped so far and its in-tile qubits still fit.
+// ---------------------------------------------------------------------------
+static int sub_cost(const FOp &o) {
+    switch (o.type) {
+    case OP_DENSE: return o.tg.size() == 1 ? 10 : 20;
+    case OP_DIAG: return 6;
+    default: return 2;
+    }
+}
+
+struct OpsEval {
+    std::vector<FOp> ops;
+    int cost = 0;
+    size_t rec = 0;
+    int ntab = 0;
+};
+
+static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOptions &opt, int amp_bytes) {
+    OpsEval ev;
+    const bool fold = !(opt.flags & SV_OPT_NO_DIAG_FOLD);
+    const bool one_gate = opt.flags & SV_OPT_ONE_GATE;
+    ev.rec = sizeof(StvPass);
+    if ((opt.flags & SV_OPT_NO_GROUPS) || one_gate) {
+        for (const PGate &g : gs) merge_into(ev.ops, g, opt.kmax, fold, one_gate);
+        for (auto &o : ev.ops) {
+            ev.cost += op_cost(o);
+            ev.rec += sizeof(StvOp);
+            if (o.type == OP_DENSE) ev.rec += (size_t)amp_bytes << (2 * o.tg.size());
+            if (o.type == OP_DIAG)
+                ev.rec += sizeof(StvDiag) + sizeof(StvTerm) * (o.form.lin.size() + o.form.quad.size());
+        }
+        return ev;
+    }
+    std::vector<char> taken(gs.size(), 0);
+    size_t first = 0;
+    while (true) {
+        while (first < gs.size() && taken[first]) ++first;
+        if (first >= gs.size()) break;
+        FOp grp;
+        grp.type = OP_GROUP;
+        uint64_t T = 0, blockedAll = 0, blockedDense = 0;
+        for (size_t i = first; i < gs.size(); ++i) {
+            if (taken[i]) continue;
+            const PGate &g = gs[i];
+            const uint64_t qm = g.qmask(), dm = g.dmask();
+            const uint64_t in_tile = (g.type == GType::DIAG ? qm : dm) & S;
+            bool ok = !(qm & blockedAll) && !(dm & blockedDense) &&
+                      __builtin_popcountll(T | in_tile) <= STV_GROUP_BITS;
+            if (!ok) {
+                blockedAll |= dm;
+                blockedDense |= qm & ~dm;
+                continue;
+            }
+            merge_into(grp.subs, g, 2, fold, false);
+            T |= in_tile;
+            taken[i] = 1;
+        }
+        grp.T = T;
+        for (auto &o : grp.subs) {
+            grp.qmask |= o.qmask;
+            grp.dmask |= o.dmask;
+            ev.cost += sub_cost(o);
+            ev.rec += sizeof(StvSub);
+            if (o.type == OP_DENSE) ev.rec += (size_t)amp_bytes << (2 * o.tg.size());
+            if (o.type == OP_DIAG) {
+                ev.rec += sizeof(StvGDiag) + sizeof(StvTerm) * (o.form.lin.size() + o.form.quad.size());
+                ++ev.ntab;
+            }
+        }
+        ev.cost += 16;                           // the group's shared-memory round trip
+        ev.rec += sizeof(StvOp);
+        ev.ops.push_back(std::move(grp));
+    }
+    return ev;
+}
+
 Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg_virtual,
                 const PlanOptions &opt, int *sigma) {
     Plan plan;
@@ -527,7 +610,8 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
         pass.kind = PASS_TILE;
         uint64_t S = low_mask & local_mask;
         uint64_t blockedAll = 0, blockedDense = 0;
-        int cost = 0;
+        std::vector<PGate> pgates;               // absorbed gates (actual bits), in order
+        OpsEval cur;
         for (size_t i = first; i < G; ++i) {
             if (done[i]) continue;
             if ((blockedAll & all_mask) == all_mask) break;
@@ -536,22 +620,16 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
             bool ok = !(qm & blockedAll) && !(dm & blockedDense) && !(dm & ~local_mask);
             uint64_t need = dm & ~S;
             if (ok && __builtin_popcountll(S | need) > opt.tile_bits) ok = false;
-            if (ok && one_gate && !pass.ops.empty()) ok = false;
-            std::vector<FOp> trial;
+            if (ok && one_gate && !pgates.empty()) ok = false;
+            OpsEval trial;
             if (ok) {
-                trial = pass.ops;
-                merge_into(trial, g, opt.kmax, fold, one_gate);
-                int c = 0;
-                size_t mb = sizeof(StvPass);      // pass record (staged in shared memory)
-                for (auto &o : trial) {
-                    c += op_cost(o);
-                    mb += sizeof(StvOp);
-                    if (o.type == OP_DENSE) mb += (size_t)amp_bytes << (2 * o.tg.size());
-                    if (o.type == OP_DIAG)
-                        mb += sizeof(StvDiag) + sizeof(StvTerm) * (o.form.lin.size() + o.form.quad.size());
+                pgates.push_back(g);
+                trial = make_ops(pgates, S | need, opt, amp_bytes);
+                if (pgates.size() > 1 &&
+                    (trial.cost > opt.budget || trial.rec > kMaxRecBytes || trial.ntab > STV_MAX_TABLES)) {
+                    ok = false;
+                    pgates.pop_back();
                 }
-                if (!pass.ops.empty() && (c > opt.budget || mb > kMaxRecBytes)) ok = false;
-                else cost = c;
             }
             if (!ok) {
                 blockedAll |= dm;
@@ -559,12 +637,12 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                 if (no_reorder) break;
                 continue;
             }
-            pass.ops.swap(trial);
+            cur = std::move(trial);
             S |= need;
             done[i] = 1;
             pass.gates.push_back(g.src);
         }
-        (void)cost;
+        pass.ops = cur.ops;
         if (pass.ops.empty()) {
             // frontier needs a global qubit as a non-diagonal target: remap
             // (SURVEY.md 8(e)).  Needed global bits from the earliest gates.
@@ -610,24 +688,40 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
         }
         // pass kind: standalone streaming kernels when no tile is needed
         bool all_diag = true;
-        for (auto &o : pass.ops) all_diag &= (o.type == OP_DIAG);
+        for (auto &g : pgates) all_diag &= (g.type == GType::DIAG);
         if (all_diag) {
             pass.kind = PASS_DIAG;
             FOp merged;
             merged.type = OP_DIAG;
-            for (auto &o : pass.ops) { merged.form.add(o.form); merged.qmask |= o.qmask; }
+            for (auto &g : pgates) { merged.form.add(g.form); merged.qmask |= g.qmask(); }
             pass.ops.assign(1, merged);
             pass.S = 0;
             // skip-write: unchanged amplitudes are not written
             plan.alg_bytes += amp_pass_bytes / 2 * 1.5;
-        } else if (pass.ops.size() == 1 && pass.ops[0].type == OP_CNOT) {
+        } else if (pgates.size() == 1 && pgates[0].type == GType::CNOT) {
             pass.kind = PASS_CNOT;
+            FOp c;
+            c.type = OP_CNOT;
+            c.c = pgates[0].q[0];
+            c.t = pgates[0].q[1];
+            pass.ops.assign(1, c);
             pass.S = 0;
             plan.alg_bytes += amp_pass_bytes / 2;
         } else {
             // pad the tile to full size with the lowest free local bits: bits no
-            // op touches cost nothing, and they lengthen the contiguous runs
+            // gate of the pass touches cost nothing and lengthen the contiguous
+            // runs (then any bit, re-grouping with the final tile)
+            uint64_t touched = 0;
+            for (auto &g : pgates) touched |= g.qmask();
+            for (int b = 0; b < nl && __builtin_popcountll(S) < opt.tile_bits; ++b)
+                if (!((touched >> b) & 1)) S |= 1ull << b;
+            const uint64_t S0 = S;
             for (int b = 0; b < nl && __builtin_popcountll(S) < opt.tile_bits; ++b) S |= 1ull << b;
+            if (S != S0) {
+                OpsEval fin = make_ops(pgates, S, opt, amp_bytes);
+                if (fin.rec <= kMaxRecBytes && fin.ntab <= STV_MAX_TABLES) pass.ops = fin.ops;
+                else S = S0;
+            }
             pass.S = S;
             plan.alg_bytes += amp_pass_bytes;
         }
@@ -721,10 +815,21 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
             hd.ops_off = (uint32_t)(b.size() - at);
             const size_t ops_at = b.size();
             b.resize(ops_at + ps.ops.size() * sizeof(StvOp));
+            std::vector<StvOp> recs(ps.ops.size());
+            std::vector<std::vector<StvSub>> subs(ps.ops.size());
+            std::vector<std::vector<int>> gpos(ps.ops.size());   // group tile positions (sorted)
+            auto put_matrix = [&](const std::vector<cd> &M) -> uint32_t {
+                const uint32_t off = (uint32_t)(b.size() - at - hd.mat_off);
+                for (const cd &z : M) {
+                    if (c128) { double v[2] = {z.real(), z.imag()}; put(b, v, 16); }
+                    else { float v[2] = {(float)z.real(), (float)z.imag()}; put(b, v, 8); }
+                }
+                align(b, 16);
+                return off;
+            };
             // matrices
             align(b, 16);
             hd.mat_off = (uint32_t)(b.size() - at);
-            std::vector<StvOp> recs(ps.ops.size());
             for (size_t i = 0; i < ps.ops.size(); ++i) {
                 const FOp &o = ps.ops[i];
                 StvOp &r = recs[i];
@@ -734,20 +839,50 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                 if (o.type == OP_DENSE) {
                     r.k = (int)o.tg.size();
                     for (int j = 0; j < r.k; ++j) r.tpos[j] = loc[o.tg[j]];
-                    r.mat_off = (uint32_t)(b.size() - at - hd.mat_off);
-                    for (const cd &z : o.M) {
-                        if (c128) { double v[2] = {z.real(), z.imag()}; put(b, v, 16); }
-                        else { float v[2] = {(float)z.real(), (float)z.imag()}; put(b, v, 8); }
-                    }
-                    align(b, 16);
+                    r.mat_off = put_matrix(o.M);
                 } else if (o.type == OP_CNOT) {
                     r.t_loc = loc[o.t];
                     if (loc[o.c] >= 0) r.c_loc = loc[o.c];
                     else r.c_phys = o.c;
+                } else if (o.type == OP_GROUP) {
+                    // group positions: its tile bits, padded to 4 with unused tile positions
+                    std::vector<int> pos;
+                    for (int p : bits_of(o.T)) pos.push_back(loc[p]);
+                    for (int q = 0; (int)pos.size() < STV_GROUP_BITS && q < hd.S; ++q)
+                        if (std::find(pos.begin(), pos.end(), q) == pos.end()) pos.push_back(q);
+                    std::sort(pos.begin(), pos.end());
+                    gpos[i] = pos;
+                    r.k = (int)pos.size();
+                    for (int j = 0; j < r.k; ++j) r.tpos[j] = pos[j];
+                    auto lbit = [&](int phys) {
+                        const int tp = loc[phys];
+                        return (int)(std::find(pos.begin(), pos.end(), tp) - pos.begin());
+                    };
+                    for (const FOp &so : o.subs) {
+                        StvSub sub;
+                        std::memset(&sub, 0, sizeof(sub));
+                        sub.c_tile = sub.c_phys = -1;
+                        sub.a = sub.b = -1;
+                        if (so.type == OP_DENSE) {
+                            sub.type = so.tg.size() == 1 ? SUB_U1 : SUB_U2;
+                            sub.a = lbit(so.tg[0]);
+                            if (so.tg.size() == 2) sub.b = lbit(so.tg[1]);
+                            sub.mat_off = put_matrix(so.M);
+                        } else if (so.type == OP_CNOT) {
+                            sub.type = SUB_CNOT;
+                            sub.b = lbit(so.t);
+                            if ((o.T >> so.c) & 1) sub.a = lbit(so.c);
+                            else if (loc[so.c] >= 0) sub.c_tile = loc[so.c];
+                            else sub.c_phys = so.c;
+                        } else {
+                            sub.type = SUB_DIAG;
+                        }
+                        subs[i].push_back(sub);
+                    }
                 }
             }
             hd.mat_bytes = (uint32_t)(b.size() - at - hd.mat_off);
-            // diag records after matrices
+            // diag records of standalone DIAG ops
             for (size_t i = 0; i < ps.ops.size(); ++i) {
                 if (ps.ops[i].type != OP_DIAG) continue;
                 align(b, 16);
@@ -756,6 +891,57 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                 b.resize(rec_at + sizeof(StvDiag));
                 encode_diag(b, rec_at, ps.ops[i].form, loc, hd.S);
             }
+            // group records: diag sub-op forms, then the sub-op arrays
+            int ntab = 0;
+            for (size_t i = 0; i < ps.ops.size(); ++i) {
+                const FOp &o = ps.ops[i];
+                if (o.type != OP_GROUP) continue;
+                const std::vector<int> &pos = gpos[i];
+                for (size_t k = 0; k < o.subs.size(); ++k) {
+                    const FOp &so = o.subs[k];
+                    if (so.type != OP_DIAG) continue;
+                    align(b, 16);
+                    subs[i][k].gdiag_off = (uint32_t)(b.size() - at);
+                    subs[i][k].tbl = ntab++;
+                    StvGDiag gd;
+                    std::memset(&gd, 0, sizeof(gd));
+                    gd.cst = so.form.cst;
+                    std::vector<StvTerm> cross, olin, oquad;
+                    auto lb = [&](int phys) -> int {   // local bit of a group qubit, or -1 if outside the tile
+                        if (loc[phys] < 0) return -1;
+                        return (int)(std::find(pos.begin(), pos.end(), loc[phys]) - pos.begin());
+                    };
+                    for (auto &kv : so.form.lin) {
+                        int j = lb(kv.first);
+                        if (j >= 0) gd.w[j] += kv.second;
+                        else olin.push_back({kv.first, -1, kv.second});
+                    }
+                    for (auto &kv : so.form.quad) {
+                        int x = kv.first.first, y = kv.first.second;
+                        int jx = lb(x), jy = lb(y);
+                        if (jx >= 0 && jy >= 0) { gd.A[jx][jy] += kv.second; gd.A[jy][jx] += kv.second; }
+                        else if (jx >= 0) cross.push_back({jx, y, kv.second});
+                        else if (jy >= 0) cross.push_back({jy, x, kv.second});
+                        else oquad.push_back({x, y, kv.second});
+                    }
+                    gd.n_cross = (int)cross.size();
+                    gd.n_olin = (int)olin.size();
+                    gd.n_oquad = (int)oquad.size();
+                    size_t off = sizeof(StvGDiag);
+                    gd.cross_off = (uint32_t)off; off += cross.size() * sizeof(StvTerm);
+                    gd.olin_off = (uint32_t)off; off += olin.size() * sizeof(StvTerm);
+                    gd.oquad_off = (uint32_t)off;
+                    put(b, &gd, sizeof(gd));
+                    put(b, cross.data(), cross.size() * sizeof(StvTerm));
+                    put(b, olin.data(), olin.size() * sizeof(StvTerm));
+                    put(b, oquad.data(), oquad.size() * sizeof(StvTerm));
+                }
+                align(b, 16);
+                recs[i].nsub = (int)subs[i].size();
+                recs[i].sub_off = (uint32_t)(b.size() - at);
+                put(b, subs[i].data(), subs[i].size() * sizeof(StvSub));
+            }
+            hd.ntab = ntab;
             std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
             (void)esz;
         } else if (ps.kind == PASS_DIAG) {
@@ -786,6 +972,44 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
 // ---------------------------------------------------------------------------
 // JSON (for the CPU plan-interpreter tests)
 // ---------------------------------------------------------------------------
+static std::string ops_json(const std::vector<FOp> &ops) {
+    std::ostringstream o;
+    o.precision(17);
+    o << "[";
+    for (size_t j = 0; j < ops.size(); ++j) {
+        const FOp &f = ops[j];
+        if (j) o << ",";
+        o << "{\"type\":" << f.type;
+        if (f.type == OP_DENSE) {
+            o << ",\"tg\":[";
+            for (size_t t = 0; t < f.tg.size(); ++t) o << (t ? "," : "") << f.tg[t];
+            o << "],\"re\":[";
+            for (size_t t = 0; t < f.M.size(); ++t) o << (t ? "," : "") << f.M[t].real();
+            o << "],\"im\":[";
+            for (size_t t = 0; t < f.M.size(); ++t) o << (t ? "," : "") << f.M[t].imag();
+            o << "]";
+        } else if (f.type == OP_DIAG) {
+            o << ",\"cst\":\"" << f.form.cst << "\",\"lin\":[";
+            bool c = false;
+            for (auto &kv : f.form.lin) { o << (c ? "," : "") << "[" << kv.first << ",\"" << kv.second << "\"]"; c = true; }
+            o << "],\"quad\":[";
+            c = false;
+            for (auto &kv : f.form.quad) {
+                o << (c ? "," : "") << "[" << kv.first.first << "," << kv.first.second << ",\"" << kv.second << "\"]";
+                c = true;
+            }
+            o << "]";
+        } else if (f.type == OP_GROUP) {
+            o << ",\"T\":\"" << f.T << "\",\"subs\":" << ops_json(f.subs);
+        } else {
+            o << ",\"c\":" << f.c << ",\"t\":" << f.t;
+        }
+        o << "}";
+    }
+    o << "]";
+    return o.str();
+}
+
 std::string plan_to_json(const Plan &p) {
     std::ostringstream o;
     o.precision(17);
@@ -798,36 +1022,7 @@ std::string plan_to_json(const Plan &p) {
         o << "],\"swaps\":[";
         for (size_t j = 0; j < ps.swaps.size(); ++j)
             o << (j ? "," : "") << "[" << ps.swaps[j].first << "," << ps.swaps[j].second << "]";
-        o << "],\"ops\":[";
-        for (size_t j = 0; j < ps.ops.size(); ++j) {
-            const FOp &f = ps.ops[j];
-            if (j) o << ",";
-            o << "{\"type\":" << f.type;
-            if (f.type == OP_DENSE) {
-                o << ",\"tg\":[";
-                for (size_t t = 0; t < f.tg.size(); ++t) o << (t ? "," : "") << f.tg[t];
-                o << "],\"re\":[";
-                for (size_t t = 0; t < f.M.size(); ++t) o << (t ? "," : "") << f.M[t].real();
-                o << "],\"im\":[";
-                for (size_t t = 0; t < f.M.size(); ++t) o << (t ? "," : "") << f.M[t].imag();
-                o << "]";
-            } else if (f.type == OP_DIAG) {
-                o << ",\"cst\":\"" << f.form.cst << "\",\"lin\":[";
-                bool c = false;
-                for (auto &kv : f.form.lin) { o << (c ? "," : "") << "[" << kv.first << ",\"" << kv.second << "\"]"; c = true; }
-                o << "],\"quad\":[";
-                c = false;
-                for (auto &kv : f.form.quad) {
-                    o << (c ? "," : "") << "[" << kv.first.first << "," << kv.first.second << ",\"" << kv.second << "\"]";
-                    c = true;
-                }
-                o << "]";
-            } else {
-                o << ",\"c\":" << f.c << ",\"t\":" << f.t;
-            }
-            o << "}";
-        }
-        o << "]}";
+        o << "],\"ops\":" << ops_json(ps.ops) << "}";
     }
     o << "],\"perm\":[";
     for (int q = 0; q < p.n; ++q) o << (q ? "," : "") << p.frame_out.perm[q];

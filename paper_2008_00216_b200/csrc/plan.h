@@ -77,6 +77,8 @@ struct FOp {
     QForm form;               // DIAG (actual-physical bits)
     int c = -1, t = -1;       // CNOT (actual-physical bits)
     uint64_t qmask = 0, dmask = 0;
+    uint64_t T = 0;           // GROUP: tile bits held in registers (<= 4, actual physical)
+    std::vector<FOp> subs;    // GROUP: sub-ops (DENSE k<=2, DIAG, CNOT) applied in registers
 };
 
 struct PPass {

@@ -55,6 +55,15 @@ def _bitswap(psi, n, a, b):
     return psi[src]
 
 
+def _flat(ops):
+    """Gate groups (type 4) are sequences of sub-ops applied in order."""
+    for op in ops:
+        if op["type"] == 4:
+            yield from _flat(op["subs"])
+        else:
+            yield op
+
+
 def run(plan, x0=0, psi=None):
     n = plan["n"]
     if psi is None:
@@ -66,7 +75,7 @@ def run(plan, x0=0, psi=None):
             for gb, lb in ps["swaps"]:
                 psi = _bitswap(psi, n, gb, lb)
             continue
-        for op in ps["ops"]:
+        for op in _flat(ps["ops"]):
             if op["type"] == 1:
                 D = 1 << len(op["tg"])
                 M = (np.array(op["re"]) + 1j * np.array(op["im"])).reshape(D, D)

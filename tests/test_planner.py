@@ -140,3 +140,44 @@ def test_remap_peers_schedule():
     assert stv.remap_peers(1, 1, 0b1, 1) == [0, 1]
     assert stv.remap_peers(3, 5, 0b110, 2) == [1, 3, 5, 7]
     assert stv.remap_peers(2, 2, 0b01, 1) == [2, 3]
+
+
+def _tile_of(ps):
+    return int(ps["S"])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_group_structure(seed):
+    # register-resident gate groups: in-tile qubits of every sub-op fit in the
+    # group's <= 4 register bits; non-diagonal targets are tile bits
+    circ = C.random_circuit(12, 200, 100 + seed)
+    plan = _check(circ, tile_bits=8, low_bits=3, budget=400)
+    ngroups = 0
+    for ps in plan["passes"]:
+        if ps["kind"] != 1:
+            continue
+        S = _tile_of(ps)
+        for op in ps["ops"]:
+            if op["type"] != 4:
+                continue
+            ngroups += 1
+            T = int(op["T"])
+            assert bin(T).count("1") <= 4 and (T & ~S) == 0
+            for so in op["subs"]:
+                if so["type"] == 1:
+                    assert all((T >> q) & 1 for q in so["tg"])
+                elif so["type"] == 3:
+                    assert (T >> so["t"]) & 1
+                else:
+                    qs = [b for b, _ in so["lin"]] + [q for p, r, _ in so["quad"] for q in (p, r)]
+                    assert all(((T >> q) & 1) or not ((S >> q) & 1) for q in qs)
+    assert ngroups > 0
+
+
+def test_groups_vs_flat_ops_same_state():
+    circ = C.config(1)
+    a = stv.plan_json(circ.n, circ.gates)
+    b = stv.plan_json(circ.n, circ.gates, flags=stv.OPT_NO_GROUPS)
+    pa = PI.logical(a, PI.run(a, x0=0))
+    pb = PI.logical(b, PI.run(b, x0=0))
+    assert np.max(np.abs(pa - pb)) < 1e-12

@@ -532,7 +532,7 @@ static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOpti
     const bool fold = !(opt.flags & SV_OPT_NO_DIAG_FOLD);
     const bool one_gate = opt.flags & SV_OPT_ONE_GATE;
     ev.rec = sizeof(StvPass);
-    if ((opt.flags & SV_OPT_NO_GROUPS) || one_gate) {
+    if ((opt.flags & SV_OPT_NO_GROUPS) || one_gate || opt.tile_bits < STV_GROUP_BITS) {
         for (const PGate &g : gs) merge_into(ev.ops, g, opt.kmax, fold, one_gate);
         for (auto &o : ev.ops) {
             ev.cost += op_cost(o);

@@ -179,6 +179,13 @@ sv_status sv_get_frame(const sv_state *s, int32_t *perm, uint64_t *xmask);
 sv_status sv_plan_json(int n, int n_global, sv_dtype dt, const sv_gate *gates, size_t ng,
                        const sv_options *opt, char *buf, size_t cap, size_t *needed);
 
+/* Host-only: the encoded device plan blob (pass_format.h) the kernels would
+ * read, for the CPU blob-emulator tests; pass_off[i] = byte offset of pass i
+ * (at most max_passes entries written; *npasses = total). */
+sv_status sv_plan_blob(int n, int n_global, sv_dtype dt, const sv_gate *gates, size_t ng,
+                       const sv_options *opt, uint8_t *buf, size_t cap, size_t *needed,
+                       uint32_t *pass_off, size_t max_passes, size_t *npasses);
+
 /* Host-only: the all-to-all schedule of one global<->local qubit swap
  * (SURVEY.md 8(e)): for rank `rank` of 2^g, swapping global bits `gbits`
  * (mask over [0,g)) with local physical bits `lbits` (ascending, same count

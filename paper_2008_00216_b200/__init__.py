@@ -32,7 +32,7 @@ PASS_KINDS = ["tile", "tile_low", "tile_high", "diag", "cnot", "remap", "init", 
 # every entry point declared in include/sv.h
 EXPORTS = ["sv_create", "sv_wrap", "sv_create_dist", "sv_create_virtual", "sv_set_basis",
            "sv_set_uniform", "sv_apply_circuit", "sv_get_amplitudes", "sv_read_state", "sv_norm",
-           "sv_last_run_stats", "sv_get_frame", "sv_plan_json", "sv_remap_peers", "sv_destroy",
+           "sv_last_run_stats", "sv_get_frame", "sv_plan_json", "sv_plan_blob", "sv_remap_peers", "sv_destroy",
            "sv_last_error", "sv_version"]
 
 
@@ -88,6 +88,9 @@ def lib():
         L.sv_get_frame.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(u64)]
         L.sv_plan_json.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Gate), sz,
                                    ctypes.POINTER(Options), ctypes.c_char_p, sz, ctypes.POINTER(sz)]
+        L.sv_plan_blob.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Gate), sz,
+                                   ctypes.POINTER(Options), ctypes.c_void_p, sz, ctypes.POINTER(sz),
+                                   ctypes.POINTER(ctypes.c_uint32), sz, ctypes.POINTER(sz)]
         L.sv_remap_peers.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint32, ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int32)]
         L.sv_destroy.argtypes = [vp]
@@ -157,6 +160,22 @@ def plan_json(n, gates, n_global=0, dtype="c64", **kw):
     _check(L.sv_plan_json(n, n_global, dt, arr, len(gates), ctypes.byref(o), buf, need.value,
                           ctypes.byref(need)))
     return json.loads(buf.value.decode())
+
+
+def plan_blob(n, gates, n_global=0, dtype="c64", **kw):
+    """Host-only: (blob bytes, pass offsets) of the encoded device plan."""
+    arr, keep = marshal(gates)
+    o = options(**kw)
+    need, npass = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    L = lib()
+    dt = C64 if dtype == "c64" else C128
+    L.sv_plan_blob(n, n_global, dt, arr, len(gates), ctypes.byref(o), None, 0, ctypes.byref(need), None, 0,
+                   ctypes.byref(npass))
+    buf = ctypes.create_string_buffer(max(1, need.value))
+    offs = (ctypes.c_uint32 * max(1, npass.value))()
+    _check(L.sv_plan_blob(n, n_global, dt, arr, len(gates), ctypes.byref(o), buf, need.value, ctypes.byref(need),
+                          offs, npass.value, ctypes.byref(npass)))
+    return bytes(buf.raw[:need.value]), list(offs)[:npass.value]
 
 
 def remap_peers(g, rank, gbits, m):

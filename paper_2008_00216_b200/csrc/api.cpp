@@ -536,6 +536,35 @@ sv_status sv_plan_json(int n, int n_global, sv_dtype dt, const sv_gate *gates, s
     return SV_OK;
 }
 
+sv_status sv_plan_blob(int n, int n_global, sv_dtype dt, const sv_gate *gates, size_t ng, const sv_options *opt,
+                       uint8_t *buf, size_t cap, size_t *needed, uint32_t *pass_off, size_t max_passes,
+                       size_t *npasses) {
+    if (n < 1 || n > 40 || n_global < 0 || n - n_global < 4) return fail(SV_ERR_INVALID_ARG, "bad n / n_global");
+    std::string err = validate(n, gates, ng);
+    if (!err.empty()) return fail(SV_ERR_INVALID_ARG, err);
+    Frame fr;
+    fr.identity(n);
+    const int esz = dt == SV_C128 ? 16 : 8;
+    std::vector<PGate> pg = to_physical(n, gates, ng, fr, opt ? opt->flags : 0);
+    PlanOptions po = resolve_options(opt, esz, n - n_global);
+    int sigma[64];
+    for (int v = 0; v < 64; ++v) sigma[v] = v;
+    Plan plan;
+    try {
+        plan = build_plan(n, n_global, esz, pg, po, sigma);
+    } catch (const std::exception &ex) {
+        return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
+    }
+    Encoded enc = encode(plan, n - n_global, dt == SV_C128);
+    if (needed) *needed = enc.blob.size();
+    if (npasses) *npasses = enc.pass_off.size();
+    if (pass_off)
+        for (size_t i = 0; i < enc.pass_off.size() && i < max_passes; ++i) pass_off[i] = enc.pass_off[i];
+    if (!buf || cap < enc.blob.size()) return fail(SV_ERR_INVALID_ARG, "buffer too small");
+    std::memcpy(buf, enc.blob.data(), enc.blob.size());
+    return SV_OK;
+}
+
 sv_status sv_remap_peers(int g, int rank, uint32_t gbits, int m, int32_t *peer) {
     if (g < 0 || g > 10 || rank < 0 || rank >= (1 << g) || !peer || m != __builtin_popcount(gbits) ||
         (gbits >> g))

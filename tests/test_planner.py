@@ -181,3 +181,31 @@ def test_groups_vs_flat_ops_same_state():
     pa = PI.logical(a, PI.run(a, x0=0))
     pb = PI.logical(b, PI.run(b, x0=0))
     assert np.max(np.abs(pa - pb)) < 1e-12
+
+
+from tests import blob_emu as BE
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("case", ["rand", "opts_tile8", "budget400", "qft_tail", "c1"])
+def test_encoded_blob_semantics(case, dtype):
+    """The exact device blob, emulated on CPU, reproduces the oracle."""
+    kw = {}
+    if case == "rand":
+        circ = C.random_circuit(11, 200, 7)
+    elif case == "opts_tile8":
+        circ = C.random_circuit(12, 300, 42)
+        kw = dict(tile_bits=8, low_bits=3)
+    elif case == "budget400":
+        circ = C.random_circuit(12, 300, 42)
+        kw = dict(budget=400)
+    elif case == "qft_tail":
+        circ = C.qft_circuit(11, tail=200, seed=3)
+    else:
+        circ = C.config(1)
+    blob, offs = stv.plan_blob(circ.n, circ.gates, dtype=dtype, **kw)
+    plan = stv.plan_json(circ.n, circ.gates, dtype=dtype, **kw)
+    psi = PI.logical(plan, BE.run(circ.n, blob, offs, x0=circ.x0, c128=dtype == "c128"))
+    ref = oracle.run(circ)
+    tol = 2e-6 if dtype == "c64" else 1e-11
+    assert np.max(np.abs(psi - ref)) < tol

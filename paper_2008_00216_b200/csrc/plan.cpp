@@ -871,7 +871,10 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                         } else if (so.type == OP_CNOT) {
                             sub.type = SUB_CNOT;
                             sub.b = lbit(so.t);
-                            if ((o.T >> so.c) & 1) sub.a = lbit(so.c);
+                            // a control on one of the group's 4 positions (a T bit or a padding
+                            // position) varies inside the register vector: in-register control
+                            if (loc[so.c] >= 0 && std::find(pos.begin(), pos.end(), loc[so.c]) != pos.end())
+                                sub.a = lbit(so.c);
                             else if (loc[so.c] >= 0) sub.c_tile = loc[so.c];
                             else sub.c_phys = so.c;
                         } else {

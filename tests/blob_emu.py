@@ -148,6 +148,9 @@ def run(n, blob, offs, x0=0, c128=False):
                             if sb.a >= 0:
                                 psi = PI._cnot(psi, n, G[sb.a], G[sb.b])
                             elif sb.c_tile >= 0:
+                                # the kernel reads this control from the vector base: it must not
+                                # be one of the group's positions (else it varies in the vector)
+                                assert sb.c_tile not in [op.tpos[i] for i in range(4)]
                                 psi = PI._cnot(psi, n, pos2phys[sb.c_tile], G[sb.b])
                             elif sb.c_phys >= 0:
                                 psi = PI._cnot(psi, n, sb.c_phys, G[sb.b])

@@ -187,7 +187,7 @@ from tests import blob_emu as BE
 
 
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
-@pytest.mark.parametrize("case", ["rand", "opts_tile8", "budget400", "qft_tail", "c1"])
+@pytest.mark.parametrize("case", ["rand", "opts_tile8", "budget400", "budget20_cnots", "qft_tail", "c1"])
 def test_encoded_blob_semantics(case, dtype):
     """The exact device blob, emulated on CPU, reproduces the oracle."""
     kw = {}
@@ -199,6 +199,9 @@ def test_encoded_blob_semantics(case, dtype):
     elif case == "budget400":
         circ = C.random_circuit(12, 300, 42)
         kw = dict(budget=400)
+    elif case == "budget20_cnots":
+        circ = C.random_circuit(11, 120, 5, kinds=["cnot", "h", "cphase"])
+        kw = dict(budget=20)
     elif case == "qft_tail":
         circ = C.qft_circuit(11, tail=200, seed=3)
     else:

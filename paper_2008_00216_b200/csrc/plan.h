@@ -93,7 +93,7 @@ struct PlanOptions {
     int kmax = 4;
     int tile_bits = 13;       // c64 default (c128: 12)
     int low_bits = 7;
-    int budget = 200;
+    int budget = 450;
     uint32_t flags = 0;
 };
 

@@ -195,3 +195,19 @@ def test_bitwise_reproducible(stv):
     a, _ = run_gpu(stv, circ)
     b, _ = run_gpu(stv, circ)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("budget", [20, 100, 450, 2000])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_grid_fsim_budgets(stv, budget, dtype):
+    circ = C.grid_circuit("g", 4, 5, 0, 20, "fsim", 2)
+    psi, _ = run_gpu(stv, circ, dtype, budget=budget)
+    assert_parity(psi, oracle.run(circ), dtype)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_c2_shape_reduced(stv, dtype):
+    # the c2 generator on a 4x6 grid (24 qubits), default options
+    circ = C.grid_circuit("c2s", 4, 6, 0, 20, "fsim", 2)
+    psi, _ = run_gpu(stv, circ, dtype)
+    assert_parity(psi, oracle.run(circ, nthreads=16), dtype)

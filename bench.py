@@ -129,6 +129,25 @@ def ncu_traffic():
         return None
 
 
+def roof(gbs, hbm, peak_kind, tflops, fp32_peak, tile_bytes, launches, tile_ms, flops_per_step):
+    """Roofline of the dominant kernel (k_tile_pass) against the resource that
+    binds it: HBM (algorithmic R+W bytes / time vs the measured copy peak) or
+    the FP32 FMA pipe (algorithmic flops / time vs 148 x 128 x 2 x clock)."""
+    if gbs is None:
+        return None
+    f_hbm = gbs / hbm
+    f_alu = tflops / fp32_peak if tflops else 0.0
+    common = {"kernel": "k_tile_pass (fused tile pass)", "bytes_per_launch": tile_bytes, "launches": launches,
+              "avg_launch_ms": tile_ms / max(1, launches), "traffic": ncu_traffic(),
+              "hbm": {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_hbm, "peak_kind": peak_kind},
+              "alu": {"achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s", "frac": f_alu,
+                      "flops_per_step": flops_per_step,
+                      "peak_kind": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"}}
+    if f_alu > f_hbm:
+        return dict(bound="alu", achieved=tflops, peak=fp32_peak, unit="TFLOP/s", frac=f_alu, **common)
+    return dict(bound="hbm", achieved=gbs, peak=hbm, unit="GB/s", frac=f_hbm, **common)
+
+
 # ---------------------------------------------------------------------------
 def oracle_sample(circ, ngates, threads):
     """Time the CPU oracle (as it stands) on the first `ngates` gates of circ."""
@@ -242,6 +261,7 @@ def main():
         one_step()
     barrier()
     tile_ms = 0.0
+    flops_total = 0.0
     tile_launches = 0
     launches = 0
     plan_ms = []
@@ -256,6 +276,7 @@ def main():
             tile_ms += s["pass_ms"]["tile_low"] + s["pass_ms"]["tile_high"]
             tile_launches += s["n_pass"]["tile_low"] + s["n_pass"]["tile_high"]
             launches += s["n_kernels"] + 1           # + the init kernel of set_basis
+            flops_total += s["alg_flops"]
             plan_ms.append(s["plan_ms"])
             kinds = s
         e1.record(stream)
@@ -273,6 +294,14 @@ def main():
     tile_bytes = 2 * esz * (1 << n_local)        # algorithmic R+W bytes per tile-pass launch
     hbm, peak_kind = peaks()
     achieved = tile_bytes / (tile_ms / max(1, tile_launches) / 1e3) / 1e9 if tile_launches else None
+    # FP32 CUDA-core peak: 148 SMs x 128 FMA lanes x 2 flop x max SM clock (B200_PROFILING.md
+    # unit counts; MEASURED_PEAKS.json sm_max_mhz), the ceiling of an FMA-bound tile pass
+    try:
+        smhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+    except Exception:
+        smhz = 1965.0
+    fp32_peak = 148 * 128 * 2 * smhz * 1e6 / 1e12 if args.dtype == "c64" else 148 * 64 * 2 * smhz * 1e6 / 1e12
+    flops_ach = (flops_total / (tile_ms / 1e3) / 1e12) if tile_ms > 0 else None
 
     # e2e: host gate list in, full state vector out (pinned host memory)
     e2e = None
@@ -325,11 +354,8 @@ def main():
         "plan_ms": statistics.median(plan_ms),
         "hbm_effective_gbs": kinds["alg_bytes"] / sec / 1e9,
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm if achieved else None, "traffic": ncu_traffic(),
-                     "kernel": "k_tile_pass (fused tile pass)", "peak_kind": peak_kind,
-                     "bytes_per_launch": tile_bytes, "launches": tile_launches,
-                     "avg_launch_ms": tile_ms / max(1, tile_launches)},
+        "roofline": roof(achieved, hbm, peak_kind, flops_ach, fp32_peak, tile_bytes, tile_launches, tile_ms,
+                         flops_total / max(1, args.steps)),
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,

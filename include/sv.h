@@ -165,6 +165,7 @@ typedef struct {
     int32_t n_ops[4];      /* ops inside fused passes: dense, diag, cnot, -        */
     int32_t n_kernels;     /* kernels launched by the last call                    */
     double h2d_bytes;      /* host->device bytes copied by the last call (plan)    */
+    double alg_flops;      /* algorithmic flops of the fused tile passes */
 } sv_stats;
 sv_status sv_last_run_stats(const sv_state *s, sv_stats *out);
 

@@ -335,6 +335,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
     std::memset(&s->stats, 0, sizeof(s->stats));
     s->stats.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     s->stats.alg_bytes = plan.alg_bytes;
+    s->stats.alg_flops = plan.alg_flops;
     s->stats.h2d_bytes = (double)enc.blob.size();
     if ((st = ensure(s, (void **)&s->hblob, &s->hblob_cap, enc.blob.size(), true))) return st;
     if ((st = ensure(s, (void **)&s->dblob, &s->dblob_cap, enc.blob.size(), false))) return st;

@@ -586,6 +586,19 @@ static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOpti
     return ev;
 }
 
+// Algorithmic floating-point work per amplitude: a k-qubit
+// dense op costs 8 * 2^k flops (2^k complex multiply-adds), a diagonal phase
+// one complex multiply (6), a CNOT none.
+static double pass_flops_per_amp(const std::vector<FOp> &ops) {
+    double f = 0;
+    for (const FOp &o : ops) {
+        if (o.type == OP_GROUP) f += pass_flops_per_amp(o.subs);
+        else if (o.type == OP_DENSE) f += 8.0 * (1 << o.tg.size());
+        else if (o.type == OP_DIAG) f += 6.0;
+    }
+    return f;
+}
+
 Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg_virtual,
                 const PlanOptions &opt, int *sigma) {
     Plan plan;
@@ -724,6 +737,7 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
             }
             pass.S = S;
             plan.alg_bytes += amp_pass_bytes;
+            plan.alg_flops += pass_flops_per_amp(pass.ops) * std::ldexp(1.0, nl);
         }
         plan.passes.push_back(pass);
     }

@@ -103,6 +103,7 @@ struct Plan {
     Frame frame_out;
     int sigma_out[64];        // virtual -> actual physical bit after the plan
     double alg_bytes = 0;     // algorithmic HBM bytes
+    double alg_flops = 0;     // algorithmic FP flops of the fused tile passes
 };
 
 // Validation (all-or-nothing).  Returns "" if ok, else the error message.

@@ -51,9 +51,10 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, uint32_t sleep_ns = 0) {
     const uint32_t a = smem_u32(bar);
     while (!mbar_try_wait(a, parity)) {
+        if (sleep_ns) __nanosleep(sleep_ns);   // back off: spinning steals issue slots from the consumers
     }
 }
 __device__ __forceinline__ void tma_load_1d(void *dst_smem, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -500,41 +501,38 @@ __device__ __forceinline__ void g_cnot_dispatch(C (&x)[16], int a, int b) {
     }
 }
 
-// per-tile phase tables of the pass's group DIAG sub-ops: tables[t*16 + l]
+// per-tile phase tables of the pass's group DIAG sub-ops: tables[t*16 + l];
+// the pass record lists the StvGDiag offset of every table (tab_off)
 template <typename C>
-__device__ void group_tables(const StvPass *__restrict__ P, const StvOp *__restrict__ ops, int nops, int ntab,
-                             uint64_t full_base, C *__restrict__ tables, int ctid) {
+__device__ void group_tables(const StvPass *__restrict__ P, int ntab, uint64_t full_base, C *__restrict__ tables,
+                             int ctid) {
+    const uint32_t *tab_off = (const uint32_t *)((const uint8_t *)P + P->tab_off);
     for (int idx = ctid; idx < ntab * 16; idx += STV_THREADS) {
-    const int t = idx >> 4, l = idx & 15;
-    for (int o = 0; o < nops; ++o) {
-        if (ops[o].type != OP_GROUP) continue;
-        const StvSub *subs = (const StvSub *)((const uint8_t *)P + ops[o].sub_off);
-        for (int k = 0; k < ops[o].nsub; ++k) {
-            if (subs[k].type != SUB_DIAG || subs[k].tbl != t) continue;
-            const uint8_t *rec = (const uint8_t *)P + subs[k].gdiag_off;
-            const StvGDiag *G = (const StvGDiag *)rec;
-            uint64_t ph = G->cst;
-            const StvTerm *ol = (const StvTerm *)(rec + G->olin_off);
-            for (int i = 0; i < G->n_olin; ++i)
-                if ((full_base >> ol[i].a) & 1) ph += ol[i].ang;
-            const StvTerm *oq = (const StvTerm *)(rec + G->oquad_off);
-            for (int i = 0; i < G->n_oquad; ++i)
-                if (((full_base >> oq[i].a) & 1) && ((full_base >> oq[i].b) & 1)) ph += oq[i].ang;
-            const StvTerm *cr = (const StvTerm *)(rec + G->cross_off);
-            for (int j = 0; j < 4; ++j) {
-                if (!((l >> j) & 1)) continue;
-                ph += G->w[j];
-                for (int i = 0; i < G->n_cross; ++i)
-                    if (cr[i].a == j && ((full_base >> cr[i].b) & 1)) ph += cr[i].ang;
-                for (int k2 = j + 1; k2 < 4; ++k2)
-                    if ((l >> k2) & 1) ph += G->A[j][k2];
-            }
-            C one;
-            one.x = 1;
-            one.y = 0;
-            tables[idx] = apply_phase(one, ph);
+        const int t = idx >> 4, l = idx & 15;
+        const uint8_t *rec = (const uint8_t *)P + tab_off[t];
+        const StvGDiag *G = (const StvGDiag *)rec;
+        uint64_t ph = G->cst;
+        const StvTerm *ol = (const StvTerm *)(rec + G->olin_off);
+        for (int i = 0; i < G->n_olin; ++i)
+            if ((full_base >> ol[i].a) & 1) ph += ol[i].ang;
+        const StvTerm *oq = (const StvTerm *)(rec + G->oquad_off);
+        for (int i = 0; i < G->n_oquad; ++i)
+            if (((full_base >> oq[i].a) & 1) && ((full_base >> oq[i].b) & 1)) ph += oq[i].ang;
+        const StvTerm *cr = (const StvTerm *)(rec + G->cross_off);
+        for (int i = 0; i < G->n_cross; ++i)
+            if (((l >> cr[i].a) & 1) && ((full_base >> cr[i].b) & 1)) ph += cr[i].ang;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!((l >> j) & 1)) continue;
+            ph += G->w[j];
+#pragma unroll
+            for (int k2 = j + 1; k2 < 4; ++k2)
+                if ((l >> k2) & 1) ph += G->A[j][k2];
         }
-    }
+        C one;
+        one.x = 1;
+        one.y = 0;
+        tables[idx] = apply_phase(one, ph);
     }
 }
 
@@ -720,7 +718,7 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
         int s = 0;
         uint32_t ph = 0;
         for (uint32_t j = 0; j < my_tiles; ++j) {
-            if (j >= (uint32_t)kStages) mbar_wait(&empty[s], ph ^ 1);
+            if (j >= (uint32_t)kStages) mbar_wait(&empty[s], ph ^ 1, 256);
             if (pt == 0) tbase[s] = tb;
             uint8_t *stile = (uint8_t *)(tiles + (size_t)s * tile_elems);
             if (use_tma) {
@@ -747,12 +745,12 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     int s = 0;
     uint32_t ph = 0;
     for (uint32_t j = 0; j < my_tiles; ++j) {
-        mbar_wait(&full[s], ph);
+        mbar_wait(&full[s], ph, 32);
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t base = tbase[s];
         const uint64_t full_base = base | rank_bits;
         if (ntab && nops) {
-            group_tables<C>(P, ops, nops, ntab, full_base, tables, tid);
+            group_tables<C>(P, ntab, full_base, tables, tid);
             consumer_sync();
         }
         for (int o = 0; o < nops; ++o) {

@@ -100,4 +100,6 @@ struct alignas(16) StvPass {
     uint32_t diag_off;         // PASS_DIAG: StvDiag offset (tile = low S bits)
     uint32_t rec_bytes;        // size of this pass record (multiple of 16)
     int32_t ntab;              // per-tile phase tables of group DIAG sub-ops
+    uint32_t tab_off;          // byte offset of uint32 StvGDiag offsets, one per table
+    int32_t pad2[3];
 };

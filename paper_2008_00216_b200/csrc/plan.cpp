@@ -959,6 +959,15 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                 put(b, subs[i].data(), subs[i].size() * sizeof(StvSub));
             }
             hd.ntab = ntab;
+            {   // table index -> StvGDiag offset
+                std::vector<uint32_t> toff(ntab, 0);
+                for (size_t i = 0; i < ps.ops.size(); ++i)
+                    for (auto &sub : subs[i])
+                        if (sub.type == SUB_DIAG) toff[sub.tbl] = sub.gdiag_off;
+                align(b, 16);
+                hd.tab_off = (uint32_t)(b.size() - at);
+                put(b, toff.data(), toff.size() * sizeof(uint32_t));
+            }
             std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
             (void)esz;
         } else if (ps.kind == PASS_DIAG) {

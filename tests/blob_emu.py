@@ -48,10 +48,10 @@ class Pass(ct.Structure):
                 ("hpos", ct.c_int32 * MAXT), ("out_mask", ct.c_uint64), ("rank_bits", ct.c_uint64),
                 ("n_local", ct.c_int32), ("nops", ct.c_int32), ("ops_off", ct.c_uint32), ("mat_off", ct.c_uint32),
                 ("mat_bytes", ct.c_uint32), ("cnot_c", ct.c_int32), ("cnot_t", ct.c_int32), ("diag_off", ct.c_uint32),
-                ("rec_bytes", ct.c_uint32), ("ntab", ct.c_int32)]
+                ("rec_bytes", ct.c_uint32), ("ntab", ct.c_int32), ("tab_off", ct.c_uint32), ("pad2", ct.c_int32 * 3)]
 
 
-assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 32 and ct.sizeof(Pass) == 128 and ct.sizeof(Term) == 16
+assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 32 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
 
 
 def _at(blob, cls, off):

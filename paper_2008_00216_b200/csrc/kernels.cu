@@ -503,11 +503,11 @@ __device__ __forceinline__ void g_cnot_dispatch(C (&x)[16], int a, int b) {
 
 // per-tile phase tables of the pass's group DIAG sub-ops: tables[t*16 + l];
 // the pass record lists the StvGDiag offset of every table (tab_off)
-template <typename C>
+template <typename C, int NT = STV_THREADS>
 __device__ void group_tables(const StvPass *__restrict__ P, int ntab, uint64_t full_base, C *__restrict__ tables,
                              int ctid) {
     const uint32_t *tab_off = (const uint32_t *)((const uint8_t *)P + P->tab_off);
-    for (int idx = ctid; idx < ntab * 16; idx += STV_THREADS) {
+    for (int idx = ctid; idx < ntab * 16; idx += NT) {
         const int t = idx >> 4, l = idx & 15;
         const uint8_t *rec = (const uint8_t *)P + tab_off[t];
         const StvGDiag *G = (const StvGDiag *)rec;
@@ -536,7 +536,7 @@ __device__ void group_tables(const StvPass *__restrict__ P, int ntab, uint64_t f
     }
 }
 
-template <typename C>
+template <typename C, int NT = STV_THREADS>
 __device__ void group_op(C *__restrict__ tile, int S, const StvOp &op, const StvPass *__restrict__ P,
                          const uint8_t *__restrict__ mat, const C *__restrict__ tables, uint64_t full_base, int ctid) {
     int tp[4];
@@ -549,7 +549,7 @@ __device__ void group_op(C *__restrict__ tile, int S, const StvOp &op, const Stv
     const int nsub = op.nsub;
     const uint32_t nvec = 1u << (S - 4);
     const bool pair16 = sizeof(C) == 8 && tp[0] == 0;
-    for (uint32_t v = ctid; v < nvec; v += STV_THREADS) {
+    for (uint32_t v = ctid; v < nvec; v += NT) {
         const uint32_t base = dense_base<4, C>(v, tp);
         C x[16];
         if (pair16) {
@@ -789,6 +789,81 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// warp-per-tile fused pass (tiles of <= 2^10 amplitudes, gate groups only):
+// every warp owns whole tiles -- it gathers the next tile with 16-B cp.async
+// into its own double buffer while it runs the current tile's gate groups in
+// registers, so groups need only __syncwarp (no CTA barriers, no producer
+// warps).  The GPU analog of the paper's "one core applies all clustered
+// gates to its resident cache lines".
+// ---------------------------------------------------------------------------
+constexpr int kWarpTileThreads = 256;
+constexpr int kWarpsPerCta = kWarpTileThreads / 32;
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <typename R>
+__global__ void __launch_bounds__(kWarpTileThreads, sizeof(R) == 4 ? 2 : 1)
+k_warp_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
+            uint32_t ntiles, int dbg_flags) {
+    using C = typename C2T<R>::T;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const StvPass *G = (const StvPass *)(blob + pass_off);
+    const uint32_t rec_bytes = G->rec_bytes;
+    const uint32_t rec_pad = (rec_bytes + 127u) & ~127u;
+    const StvPass *P = (const StvPass *)smem;
+    for (uint32_t k = threadIdx.x; k < rec_bytes / 16; k += blockDim.x) ((uint4 *)smem)[k] = ((const uint4 *)G)[k];
+    __syncthreads();
+    const int S = P->S, L = P->L, h = P->h;
+    const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
+    const int nops = (dbg_flags & 1) ? 0 : P->nops;
+    const StvOp *ops = (const StvOp *)((const uint8_t *)P + P->ops_off);
+    const uint8_t *mat = (const uint8_t *)P + P->mat_off;
+    const int ntab = P->ntab;
+    const uint32_t esz = sizeof(C);
+    const uint32_t tile_elems = 1u << S;
+    const uint32_t run_bytes = (1u << L) * esz;
+    const uint32_t nruns = 1u << h;
+    const uint32_t tab_bytes = ((uint32_t)ntab * 16 * esz + 127u) & ~127u;
+    const uint32_t warp_bytes = 2 * tile_elems * esz + tab_bytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t *wsm = smem + rec_pad + (size_t)warp * warp_bytes;
+    C *buf[2] = {(C *)wsm, (C *)(wsm + (size_t)tile_elems * esz)};
+    C *tables = (C *)(wsm + 2 * (size_t)tile_elems * esz);
+    uint64_t hmask = 0;
+    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
+    uint8_t *gstate = (uint8_t *)state;
+
+    const uint32_t gw = blockIdx.x * kWarpsPerCta + warp, nw = gridDim.x * kWarpsPerCta;
+    const uint32_t my_tiles = gw < ntiles ? (ntiles - gw + nw - 1) / nw : 0;
+    uint64_t tb = pdep64(gw, out_mask);
+    const uint64_t tstep = pdep64(nw, out_mask);
+    if (my_tiles) tile_copy16<true, 32>(gstate, (uint8_t *)buf[0], tb, hmask, run_bytes, nruns, esz, lane);
+    cp_async_commit();
+    for (uint32_t j = 0; j < my_tiles; ++j) {
+        const uint64_t base = tb;
+        tb = masked_add(tb, tstep, out_mask);
+        if (j + 1 < my_tiles)
+            tile_copy16<true, 32>(gstate, (uint8_t *)buf[(j + 1) & 1], tb, hmask, run_bytes, nruns, esz, lane);
+        cp_async_commit();
+        cp_async_wait1();
+        __syncwarp();
+        C *tile = buf[j & 1];
+        const uint64_t full_base = base | rank_bits;
+        if (ntab && nops) {
+            group_tables<C, 32>(P, ntab, full_base, tables, lane);
+            __syncwarp();
+        }
+        for (int o = 0; o < nops; ++o) {
+            group_op<C, 32>(tile, S, ops[o], P, mat, tables, full_base, lane);
+            __syncwarp();
+        }
+        tile_copy16<false, 32>(gstate, (uint8_t *)tile, base, hmask, run_bytes, nruns, esz, lane);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // standalone diagonal pass (streaming; skip-write)
 // ---------------------------------------------------------------------------
 template <typename R>
@@ -1001,6 +1076,45 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
     e = cudaGetLastError();
     ++*kernels;
     return e;
+}
+
+cudaError_t launch_warp_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
+                             uint32_t rec_bytes, int ntab, cudaStream_t st, int *kernels) {
+    const size_t esz = c128 ? 16 : 8;
+    const size_t tab = ((size_t)ntab * 16 * esz + 127) & ~(size_t)127;
+    const size_t per_warp = 2 * (esz << S) + tab;
+    const size_t smem = ((rec_bytes + 127u) & ~127u) + kWarpsPerCta * per_warp;
+    const uint64_t ntiles = 1ull << (n_local - S);
+    if (smem > 227 * 1024 || (ntiles >> 32)) return cudaErrorInvalidValue;
+    int occ = 0;
+    if (c128) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_warp_pass<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp_pass<double>, kWarpTileThreads, smem);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_warp_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp_pass<float>, kWarpTileThreads, smem);
+    }
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    uint64_t grid = (uint64_t)num_sms() * occ;
+    const uint64_t need = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+    if (grid > need) grid = need;
+    static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
+    if (c128)
+        k_warp_pass<double><<<(unsigned)grid, kWarpTileThreads, smem, st>>>((double2 *)state, dblob, pass_off,
+                                                                           (uint32_t)ntiles, dbg);
+    else
+        k_warp_pass<float><<<(unsigned)grid, kWarpTileThreads, smem, st>>>((float2 *)state, dblob, pass_off,
+                                                                          (uint32_t)ntiles, dbg);
+    ++*kernels;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,

@@ -364,7 +364,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
             kind = hp->h == 0 ? 1 : 2;
             bool all_group = true;
             for (auto &o : ps.ops) all_group &= (o.type == OP_GROUP);
-            if (all_group && hp->S <= 10 && !(flags & SV_OPT_CTA_TILES))
+            if (all_group && hp->S <= 10 && (flags & SV_OPT_WARP_TILES))
                 e = launch_warp_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->rec_bytes,
                                      hp->ntab, s->stream, &kernels);
             else

@@ -15,12 +15,13 @@ ap.add_argument("--low-bits", type=int, default=0)
 ap.add_argument("--budget", type=int, default=0)
 ap.add_argument("--kmax", type=int, default=0)
 ap.add_argument("--dtype", default="c64")
+ap.add_argument("--flags", type=int, default=0)
 a = ap.parse_args()
 circ = C.config(2) if a.n == 30 else C.grid_circuit("g", 5, a.n // 5, 0, 20, "fsim", 2)
 st = stv.State(circ.n, a.dtype)
 for r in range(a.reps):
     st.set_basis(0)
-    st.apply(circ.gates[:a.gates], tile_bits=a.tile_bits, low_bits=a.low_bits, budget=a.budget, kmax=a.kmax, profile=True)
+    st.apply(circ.gates[:a.gates], tile_bits=a.tile_bits, low_bits=a.low_bits, budget=a.budget, kmax=a.kmax, flags=a.flags, profile=True)
     s = st.stats()
     nt = s["n_pass"]["tile_low"] + s["n_pass"]["tile_high"]
     tms = s["pass_ms"]["tile_low"] + s["pass_ms"]["tile_high"]

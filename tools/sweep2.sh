@@ -1,6 +1,6 @@
 #!/bin/bash
 # tile shape sweep on full c2: "tile low budget [flags]"
-for cfg in "9 3 1000" "10 3 1000" "10 5 1000" "9 5 1000" "12 7 450" "12 3 1000" "10 3 1000 64"; do
+for cfg in ${CFGS:-"12 3 1000" "12 3 3000" "13 3 1000" "13 3 3000" "12 2 1000" "12 1 1000" "11 3 1000" "12 4 1000" "9 3 1000 64"}; do
 set -- $cfg
 EXTRA=""; [ -n "$4" ] && EXTRA="--flags $4"
 python tools/prof_pass.py --gates 723 --reps 2 --tile-bits $1 --low-bits $2 --budget $3 $EXTRA 2>&1 | tail -1 | python -c "

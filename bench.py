@@ -347,7 +347,7 @@ def main():
         "data": "synthetic (seeded BASELINE.json circuit; no dataset)",
         "config": {"workload": circ.name, "n": n, "gates": G, "state": args.dtype,
                    "state_bytes_per_gpu": esz << n_local, "l2": "state >> 126 MB L2 (no flush needed)",
-                   "kmax": args.kmax or 4, "budget": args.budget or 450, "tile_bits": args.tile_bits or None},
+                   "kmax": args.kmax or 4, "budget": args.budget or 1000, "tile_bits": args.tile_bits or None},
         "sec_per_circuit": sec,
         "passes": {k: v for k, v in kinds["n_pass"].items() if v},
         "ops": kinds["n_ops"],

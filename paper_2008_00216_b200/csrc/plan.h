@@ -92,8 +92,8 @@ struct PPass {
 struct PlanOptions {
     int kmax = 4;
     int tile_bits = 13;       // c64 default (c128: 12)
-    int low_bits = 7;
-    int budget = 450;
+    int low_bits = 4;
+    int budget = 1000;
     uint32_t flags = 0;
 };
 

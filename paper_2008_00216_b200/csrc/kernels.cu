@@ -606,7 +606,7 @@ constexpr int kStages = 3;
 constexpr int kHdrBytes = 1024;    // barriers, tile bases, DiagScratch
 constexpr int kProdWarps = 2;
 constexpr int kProd = 32 * kProdWarps;
-constexpr int kTileThreads = STV_THREADS + kProd;
+constexpr int kTileThreads = STV_THREADS;
 
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
@@ -614,6 +614,10 @@ __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // x + y in the "expanded" domain of mask (carries jump over the gaps):
 // pdep(a + b, m) == masked_add(pdep(a, m), pdep(b, m), m)
 __device__ __forceinline__ uint64_t masked_add(uint64_t x, uint64_t y, uint64_t m) {
@@ -670,35 +674,30 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
         uint4 *dst = (uint4 *)(smem + kHdrBytes);
         for (uint32_t k = threadIdx.x; k < rec_bytes / 16; k += blockDim.x) dst[k] = src[k];
     }
-    __syncthreads();
-    const int S = P->S, L = P->L, h = P->h;
-    const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
-    const int nops = (dbg_flags & 1) ? 0 : P->nops;   // bit 0: data movement only (microbenchmark)
-    const StvOp *ops = (const StvOp *)((const uint8_t *)P + P->ops_off);
+    const int S = G->S, L = G->L, h = G->h;
+    const uint64_t out_mask = G->out_mask, rank_bits = G->rank_bits;
+    const int nops = (dbg_flags & 1) ? 0 : G->nops;   // bit 0: data movement only (microbenchmark)
+    const StvOp *ops = (const StvOp *)((const uint8_t *)P + G->ops_off);
 
-    uint64_t *full = (uint64_t *)smem;                 // [3]
-    uint64_t *empty = (uint64_t *)(smem + 24);         // [3]
-    uint64_t *tbase = (uint64_t *)(smem + 48);         // [3]
+    uint64_t *full = (uint64_t *)smem;                 // [3] (TMA path only)
     DiagScratch *sc = (DiagScratch *)(smem + 128);
-    const uint8_t *mat = (const uint8_t *)P + P->mat_off;
-    const int ntab = P->ntab;
+    const uint8_t *mat = (const uint8_t *)P + G->mat_off;
+    const int ntab = G->ntab;
     C *tables = (C *)(smem + kHdrBytes + rec_pad);
     const uint32_t tab_pad = ((uint32_t)ntab * 16 * sizeof(C) + 127u) & ~127u;
     C *tiles = (C *)(smem + kHdrBytes + rec_pad + tab_pad);
     const uint32_t esz = sizeof(C);
     const uint32_t tile_elems = 1u << S;
-    const uint32_t run_elems = 1u << L;
+    const uint32_t run_bytes = (1u << L) * esz;
     const uint32_t nruns = 1u << h;
-    const uint32_t run_bytes = run_elems * esz;
     const uint32_t tile_bytes = tile_elems * esz;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool use_tma = run_bytes >= 8192;
+    const int tid = threadIdx.x;
+    // one contiguous run per tile: a single TMA bulk copy (1-D bulk copies cost
+    // ~160 SM cycles each, so strided tiles use 16-B cp.async instead)
+    const bool use_tma = (h == 0) && tile_bytes <= (1u << 20) - 1;
 
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], kProd);
-            mbar_init(&empty[s], STV_THREADS / 32);
-        }
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
@@ -707,51 +706,43 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     const uint32_t first = blockIdx.x, stride = gridDim.x;
     const uint32_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
     uint64_t hmask = 0;
-    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
+    for (int r = 0; r < h; ++r) hmask |= 1ull << G->hpos[r];
     uint8_t *gstate = (uint8_t *)state;
+    const uint64_t tstep = pdep64(stride, out_mask);
+    uint64_t load_tb = pdep64(first, out_mask);        // base of the next tile to load
+    uint32_t loaded = 0;
 
-    if (tid >= STV_THREADS) {
-        // ------------------------------ producers -------------------------
-        const int pt = tid - STV_THREADS;
-        uint64_t tb = pdep64(first, out_mask);
-        const uint64_t tstep = pdep64(stride, out_mask);
-        int s = 0;
-        uint32_t ph = 0;
-        for (uint32_t j = 0; j < my_tiles; ++j) {
-            if (j >= (uint32_t)kStages) mbar_wait(&empty[s], ph ^ 1, 256);
-            if (pt == 0) tbase[s] = tb;
-            uint8_t *stile = (uint8_t *)(tiles + (size_t)s * tile_elems);
+    auto issue = [&](int s) {                            // all threads: tile `loaded` -> stage s
+        uint8_t *stile = (uint8_t *)(tiles + (size_t)s * tile_elems);
+        if (loaded < my_tiles) {
             if (use_tma) {
-                if (pt == 0) mbar_arrive_expect_tx(&full[s], tile_bytes);
-                else mbar_arrive(&full[s]);
-                if (warp == STV_THREADS / 32) {
-                    uint64_t roff = pdep64(lane, hmask);
-                    const uint64_t d32 = pdep64(32, hmask);
-                    for (uint32_t r = lane; r < nruns; r += 32) {
-                        tma_load_1d(stile + (size_t)r * run_bytes, gstate + (tb | roff) * esz, run_bytes, &full[s]);
-                        roff = masked_add(roff, d32, hmask);
-                    }
+                if (tid == 0) {
+                    mbar_arrive_expect_tx(&full[s], tile_bytes);
+                    tma_load_1d(stile, gstate + load_tb * esz, tile_bytes, &full[s]);
                 }
             } else {
-                tile_copy16<true, kProd>(gstate, stile, tb, hmask, run_bytes, nruns, esz, pt);
-                cp_async_arrive_noinc(&full[s]);
+                tile_copy16<true, STV_THREADS>(gstate, stile, load_tb, hmask, run_bytes, nruns, esz, tid);
             }
-            tb = masked_add(tb, tstep, out_mask);
-            if (++s == kStages) { s = 0; ph ^= 1; }
         }
-        return;
-    }
-    // -------------------------------- consumers -----------------------------
-    int s = 0;
-    uint32_t ph = 0;
+        cp_async_commit();
+        load_tb = masked_add(load_tb, tstep, out_mask);
+        ++loaded;
+    };
+    issue(0);
+    issue(1);
+    uint64_t base = pdep64(first, out_mask);
+    uint32_t tphase = 0;                                 // TMA mbarrier parity per stage ring pass
     for (uint32_t j = 0; j < my_tiles; ++j) {
-        mbar_wait(&full[s], ph, 32);
+        const int s = (int)(j % kStages);
+        cp_async_wait1();                                // this thread's copies of tile j landed
+        if (use_tma) mbar_wait(&full[s], tphase);
+        __syncthreads();                                 // everyone's copies visible; stage (j+2)%3 free
+        issue((int)((j + 2) % kStages));
         C *tile = tiles + (size_t)s * tile_elems;
-        const uint64_t base = tbase[s];
         const uint64_t full_base = base | rank_bits;
         if (ntab && nops) {
             group_tables<C>(P, ntab, full_base, tables, tid);
-            consumer_sync();
+            __syncthreads();
         }
         for (int o = 0; o < nops; ++o) {
             const StvOp &op = ops[o];
@@ -775,17 +766,17 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
             } else {
                 const StvDiag *D = (const StvDiag *)((const uint8_t *)P + op.diag_off);
                 diag_prep<V>(D, S, full_base, sc);
-                consumer_sync();
+                __syncthreads();
                 diag_op_tile<V, C>(tile, S, D, sc);
             }
-            consumer_sync();
+            __syncthreads();
         }
         tile_copy16<false, STV_THREADS>(gstate, (uint8_t *)tile, base, hmask, run_bytes, nruns, esz, tid);
-        if (use_tma) fence_proxy_async();      // generic smem accesses before the next async-proxy (TMA) write
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == kStages) { s = 0; ph ^= 1; }
+        if (use_tma) fence_proxy_async();                // generic smem accesses before the next TMA write
+        base = masked_add(base, tstep, out_mask);
+        if (s == kStages - 1) tphase ^= 1;
     }
+    cp_async_wait0();
 }
 
 // ---------------------------------------------------------------------------
@@ -799,8 +790,6 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
 constexpr int kWarpTileThreads = 256;
 constexpr int kWarpsPerCta = kWarpTileThreads / 32;
 
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <typename R>
 __global__ void __launch_bounds__(kWarpTileThreads, sizeof(R) == 4 ? 2 : 1)

@@ -604,8 +604,6 @@ __device__ void group_op(C *__restrict__ tile, int S, const StvOp &op, const Stv
 // ---------------------------------------------------------------------------
 constexpr int kStages = 3;
 constexpr int kHdrBytes = 1024;    // barriers, tile bases, DiagScratch
-constexpr int kProdWarps = 2;
-constexpr int kProd = 32 * kProdWarps;
 constexpr int kTileThreads = STV_THREADS;
 
 __device__ __forceinline__ void cp_async16(void *dst_smem, const void *src) {

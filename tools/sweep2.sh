@@ -1,6 +1,7 @@
 #!/bin/bash
 # tile shape sweep on full c2: "tile low budget [flags]"
-for cfg in ${CFGS:-"12 3 1000" "12 3 3000" "13 3 1000" "13 3 3000" "12 2 1000" "12 1 1000" "11 3 1000" "12 4 1000" "9 3 1000 64"}; do
+IFS=, read -ra LIST <<< "${CFGS:-12 4 1000,12 2 1000,13 4 1000,12 4 300}"
+for cfg in "${LIST[@]}"; do
 set -- $cfg
 EXTRA=""; [ -n "$4" ] && EXTRA="--flags $4"
 python tools/prof_pass.py --gates 723 --reps 2 --tile-bits $1 --low-bits $2 --budget $3 $EXTRA 2>&1 | tail -1 | python -c "

@@ -520,57 +520,33 @@ static int sub_cost(const FOp &o) {
     }
 }
 
+struct GroupScan {              // final state of one group's scan (for incremental adds)
+    uint64_t T = 0, blockedAll = 0, blockedDense = 0;
+};
+
 struct OpsEval {
     std::vector<FOp> ops;
+    std::vector<GroupScan> scan;  // parallel to ops in group mode
+    bool grouped = false;
     int cost = 0;
     size_t rec = 0;
     int ntab = 0;
 };
 
-static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOptions &opt, int amp_bytes) {
-    OpsEval ev;
-    const bool fold = !(opt.flags & SV_OPT_NO_DIAG_FOLD);
-    const bool one_gate = opt.flags & SV_OPT_ONE_GATE;
+static void tally(OpsEval &ev, int amp_bytes) {
+    ev.cost = 0;
     ev.rec = sizeof(StvPass);
-    if ((opt.flags & SV_OPT_NO_GROUPS) || one_gate || opt.tile_bits < STV_GROUP_BITS) {
-        for (const PGate &g : gs) merge_into(ev.ops, g, opt.kmax, fold, one_gate);
-        for (auto &o : ev.ops) {
-            ev.cost += op_cost(o);
+    ev.ntab = 0;
+    for (auto &grp : ev.ops) {
+        if (grp.type != OP_GROUP) {
+            ev.cost += op_cost(grp);
             ev.rec += sizeof(StvOp);
-            if (o.type == OP_DENSE) ev.rec += (size_t)amp_bytes << (2 * o.tg.size());
-            if (o.type == OP_DIAG)
-                ev.rec += sizeof(StvDiag) + sizeof(StvTerm) * (o.form.lin.size() + o.form.quad.size());
+            if (grp.type == OP_DENSE) ev.rec += (size_t)amp_bytes << (2 * grp.tg.size());
+            if (grp.type == OP_DIAG)
+                ev.rec += sizeof(StvDiag) + sizeof(StvTerm) * (grp.form.lin.size() + grp.form.quad.size());
+            continue;
         }
-        return ev;
-    }
-    std::vector<char> taken(gs.size(), 0);
-    size_t first = 0;
-    while (true) {
-        while (first < gs.size() && taken[first]) ++first;
-        if (first >= gs.size()) break;
-        FOp grp;
-        grp.type = OP_GROUP;
-        uint64_t T = 0, blockedAll = 0, blockedDense = 0;
-        for (size_t i = first; i < gs.size(); ++i) {
-            if (taken[i]) continue;
-            const PGate &g = gs[i];
-            const uint64_t qm = g.qmask(), dm = g.dmask();
-            const uint64_t in_tile = (g.type == GType::DIAG ? qm : dm) & S;
-            bool ok = !(qm & blockedAll) && !(dm & blockedDense) &&
-                      __builtin_popcountll(T | in_tile) <= STV_GROUP_BITS;
-            if (!ok) {
-                blockedAll |= dm;
-                blockedDense |= qm & ~dm;
-                continue;
-            }
-            merge_into(grp.subs, g, 2, fold, false);
-            T |= in_tile;
-            taken[i] = 1;
-        }
-        grp.T = T;
         for (auto &o : grp.subs) {
-            grp.qmask |= o.qmask;
-            grp.dmask |= o.dmask;
             ev.cost += sub_cost(o);
             ev.rec += sizeof(StvSub);
             if (o.type == OP_DENSE) ev.rec += (size_t)amp_bytes << (2 * o.tg.size());
@@ -580,10 +556,102 @@ static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOpti
             }
         }
         ev.cost += 16;                           // the group's shared-memory round trip
-        ev.rec += sizeof(StvOp);
-        ev.ops.push_back(std::move(grp));
+        ev.rec += sizeof(StvOp) + 4;
     }
+}
+
+static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOptions &opt, int amp_bytes) {
+    OpsEval ev;
+    const bool fold = !(opt.flags & SV_OPT_NO_DIAG_FOLD);
+    const bool one_gate = opt.flags & SV_OPT_ONE_GATE;
+    if ((opt.flags & SV_OPT_NO_GROUPS) || one_gate || opt.tile_bits < STV_GROUP_BITS) {
+        for (const PGate &g : gs) merge_into(ev.ops, g, opt.kmax, fold, one_gate);
+        tally(ev, amp_bytes);
+        return ev;
+    }
+    ev.grouped = true;
+    std::vector<char> taken(gs.size(), 0);
+    size_t first = 0;
+    while (true) {
+        while (first < gs.size() && taken[first]) ++first;
+        if (first >= gs.size()) break;
+        FOp grp;
+        grp.type = OP_GROUP;
+        GroupScan sc;
+        for (size_t i = first; i < gs.size(); ++i) {
+            if (taken[i]) continue;
+            const PGate &g = gs[i];
+            const uint64_t qm = g.qmask(), dm = g.dmask();
+            const uint64_t in_tile = (g.type == GType::DIAG ? qm : dm) & S;
+            bool ok = !(qm & sc.blockedAll) && !(dm & sc.blockedDense) &&
+                      __builtin_popcountll(sc.T | in_tile) <= STV_GROUP_BITS;
+            if (!ok) {
+                sc.blockedAll |= dm;
+                sc.blockedDense |= qm & ~dm;
+                continue;
+            }
+            merge_into(grp.subs, g, 2, fold, false);
+            sc.T |= in_tile;
+            taken[i] = 1;
+        }
+        grp.T = sc.T;
+        for (auto &o : grp.subs) {
+            grp.qmask |= o.qmask;
+            grp.dmask |= o.dmask;
+        }
+        ev.ops.push_back(std::move(grp));
+        ev.scan.push_back(sc);
+    }
+    tally(ev, amp_bytes);
     return ev;
+}
+
+// Add gate g (last in scan order) to an existing group partition: exactly what
+// make_ops would decide, since earlier decisions never depend on later gates
+// (valid while the tile set S is unchanged).
+static void add_gate(OpsEval &ev, const PGate &g, uint64_t S, const PlanOptions &opt, int amp_bytes) {
+    const bool fold = !(opt.flags & SV_OPT_NO_DIAG_FOLD);
+    const uint64_t qm = g.qmask(), dm = g.dmask();
+    const uint64_t in_tile = (g.type == GType::DIAG ? qm : dm) & S;
+    bool placed = false;
+    for (size_t k = 0; k < ev.ops.size() && !placed; ++k) {
+        GroupScan &sc = ev.scan[k];
+        bool ok = !(qm & sc.blockedAll) && !(dm & sc.blockedDense) &&
+                  __builtin_popcountll(sc.T | in_tile) <= STV_GROUP_BITS;
+        if (!ok) {
+            sc.blockedAll |= dm;
+            sc.blockedDense |= qm & ~dm;
+            continue;
+        }
+        FOp &grp = ev.ops[k];
+        merge_into(grp.subs, g, 2, fold, false);
+        sc.T |= in_tile;
+        grp.T = sc.T;
+        grp.qmask |= qm;
+        grp.dmask |= dm;
+        placed = true;
+    }
+    if (!placed) {
+        FOp grp;
+        grp.type = OP_GROUP;
+        GroupScan sc;
+        merge_into(grp.subs, g, 2, fold, false);
+        sc.T = in_tile;
+        grp.T = sc.T;
+        grp.qmask = qm;
+        grp.dmask = dm;
+        ev.ops.push_back(std::move(grp));
+        ev.scan.push_back(sc);
+    }
+    // sub-op masks may have been merged: recompute the group masks exactly
+    for (auto &grp : ev.ops) {
+        grp.qmask = grp.dmask = 0;
+        for (auto &o : grp.subs) {
+            grp.qmask |= o.qmask;
+            grp.dmask |= o.dmask;
+        }
+    }
+    tally(ev, amp_bytes);
 }
 
 // Algorithmic floating-point work per amplitude: a k-qubit
@@ -634,14 +702,19 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
             uint64_t need = dm & ~S;
             if (ok && __builtin_popcountll(S | need) > opt.tile_bits) ok = false;
             if (ok && one_gate && !pgates.empty()) ok = false;
-            OpsEval trial;
             if (ok) {
                 pgates.push_back(g);
-                trial = make_ops(pgates, S | need, opt, amp_bytes);
+                const bool incremental = cur.grouped && need == 0;   // tile set unchanged
+                if (incremental) add_gate(cur, g, S, opt, amp_bytes);
+                else {
+                    OpsEval t = make_ops(pgates, S | need, opt, amp_bytes);
+                    std::swap(cur, t);
+                }
                 if (pgates.size() > 1 &&
-                    (trial.cost > opt.budget || trial.rec > kMaxRecBytes || trial.ntab > STV_MAX_TABLES)) {
+                    (cur.cost > opt.budget || cur.rec > kMaxRecBytes || cur.ntab > STV_MAX_TABLES)) {
                     ok = false;
                     pgates.pop_back();
+                    cur = make_ops(pgates, S, opt, amp_bytes);        // rare: rebuild without g
                 }
             }
             if (!ok) {
@@ -650,7 +723,6 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                 if (no_reorder) break;
                 continue;
             }
-            cur = std::move(trial);
             S |= need;
             done[i] = 1;
             pass.gates.push_back(g.src);

@@ -501,38 +501,65 @@ __device__ __forceinline__ void g_cnot_dispatch(C (&x)[16], int a, int b) {
     }
 }
 
-// per-tile phase tables of the pass's group DIAG sub-ops: tables[t*16 + l];
-// the pass record lists the StvGDiag offset of every table (tab_off)
+// per-tile phase tables of the pass's group DIAG sub-ops: tables[t*16 + l].
+// One warp per table: lanes reduce the per-tile constant (outside-tile linear
+// and pair terms) and the 4 per-tile linear coefficients (cross terms) over
+// strided term lists, then lanes 0..15 finish one entry each.  The pass record
+// lists the StvGDiag offset of every table (tab_off).
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
 template <typename C, int NT = STV_THREADS>
 __device__ void group_tables(const StvPass *__restrict__ P, int ntab, uint64_t full_base, C *__restrict__ tables,
                              int ctid) {
     const uint32_t *tab_off = (const uint32_t *)((const uint8_t *)P + P->tab_off);
-    for (int idx = ctid; idx < ntab * 16; idx += NT) {
-        const int t = idx >> 4, l = idx & 15;
+    const int lane = ctid & 31;
+    for (int t = ctid >> 5; t < ntab; t += NT / 32) {
         const uint8_t *rec = (const uint8_t *)P + tab_off[t];
         const StvGDiag *G = (const StvGDiag *)rec;
-        uint64_t ph = G->cst;
+        uint64_t c = 0, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
         const StvTerm *ol = (const StvTerm *)(rec + G->olin_off);
-        for (int i = 0; i < G->n_olin; ++i)
-            if ((full_base >> ol[i].a) & 1) ph += ol[i].ang;
+        for (int i = lane; i < G->n_olin; i += 32)
+            if ((full_base >> ol[i].a) & 1) c += ol[i].ang;
         const StvTerm *oq = (const StvTerm *)(rec + G->oquad_off);
-        for (int i = 0; i < G->n_oquad; ++i)
-            if (((full_base >> oq[i].a) & 1) && ((full_base >> oq[i].b) & 1)) ph += oq[i].ang;
+        for (int i = lane; i < G->n_oquad; i += 32)
+            if (((full_base >> oq[i].a) & 1) && ((full_base >> oq[i].b) & 1)) c += oq[i].ang;
         const StvTerm *cr = (const StvTerm *)(rec + G->cross_off);
-        for (int i = 0; i < G->n_cross; ++i)
-            if (((l >> cr[i].a) & 1) && ((full_base >> cr[i].b) & 1)) ph += cr[i].ang;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (!((l >> j) & 1)) continue;
-            ph += G->w[j];
-#pragma unroll
-            for (int k2 = j + 1; k2 < 4; ++k2)
-                if ((l >> k2) & 1) ph += G->A[j][k2];
+        for (int i = lane; i < G->n_cross; i += 32) {
+            if (!((full_base >> cr[i].b) & 1)) continue;
+            const uint64_t a = cr[i].ang;
+            switch (cr[i].a) {
+            case 0: w0 += a; break;
+            case 1: w1 += a; break;
+            case 2: w2 += a; break;
+            default: w3 += a; break;
+            }
         }
-        C one;
-        one.x = 1;
-        one.y = 0;
-        tables[idx] = apply_phase(one, ph);
+        c = warp_sum64(c) + G->cst;
+        w0 = warp_sum64(w0) + G->w[0];
+        w1 = warp_sum64(w1) + G->w[1];
+        w2 = warp_sum64(w2) + G->w[2];
+        w3 = warp_sum64(w3) + G->w[3];
+        if (lane < 16) {
+            const int l = lane;
+            uint64_t ph = c;
+            if (l & 1) ph += w0;
+            if (l & 2) ph += w1;
+            if (l & 4) ph += w2;
+            if (l & 8) ph += w3;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int k2 = j + 1; k2 < 4; ++k2)
+                    if (((l >> j) & 1) && ((l >> k2) & 1)) ph += G->A[j][k2];
+            C one;
+            one.x = 1;
+            one.y = 0;
+            tables[t * 16 + l] = apply_phase(one, ph);
+        }
     }
 }
 

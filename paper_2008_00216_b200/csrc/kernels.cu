@@ -596,8 +596,52 @@ __device__ void group_op(C *__restrict__ tile, int S, const StvOp &op, const Stv
             case SUB_U2: g_u2_dispatch(x, sb.a, sb.b, (const C *)(mat + sb.mat_off)); break;
             case SUB_DIAG: {
                 const C *tb = tables + sb.tbl * 16;
+                const uint8_t *rec = (const uint8_t *)P + sb.gdiag_off;
+                const StvGDiag *G = (const StvGDiag *)rec;
+                uint64_t dc = 0, dw0 = 0, dw1 = 0, dw2 = 0, dw3 = 0;
+                if (G->n_v) {
+                    // per-vector terms: V-bits are fixed bits of this vector's base
+                    const StvTerm *t = (const StvTerm *)(rec + G->vlin_off);
+                    for (int i = 0; i < G->n_vlin; ++i)
+                        if ((base >> t[i].a) & 1) dc += t[i].ang;
+                    t = (const StvTerm *)(rec + G->vquad_off);
+                    for (int i = 0; i < G->n_vquad; ++i)
+                        if (((base >> t[i].a) & 1) && ((base >> t[i].b) & 1)) dc += t[i].ang;
+                    t = (const StvTerm *)(rec + G->vout_off);
+                    for (int i = 0; i < G->n_vout; ++i)
+                        if (((base >> t[i].a) & 1) && ((full_base >> t[i].b) & 1)) dc += t[i].ang;
+                    t = (const StvTerm *)(rec + G->vcross_off);
+                    for (int i = 0; i < G->n_vcross; ++i) {
+                        if (!((base >> t[i].b) & 1)) continue;
+                        switch (t[i].a) {
+                        case 0: dw0 += t[i].ang; break;
+                        case 1: dw1 += t[i].ang; break;
+                        case 2: dw2 += t[i].ang; break;
+                        default: dw3 += t[i].ang; break;
+                        }
+                    }
+                }
+                if ((dc | dw0 | dw1 | dw2 | dw3) == 0) {
 #pragma unroll
-                for (int l = 0; l < 16; ++l) x[l] = cmul(x[l], tb[l]);
+                    for (int l = 0; l < 16; ++l) x[l] = cmul(x[l], tb[l]);
+                } else {
+                    C one;
+                    one.x = 1;
+                    one.y = 0;
+                    C f[16];
+                    f[0] = apply_phase(one, dc);
+                    const C e0 = apply_phase(one, dw0), e1 = apply_phase(one, dw1);
+                    const C e2 = apply_phase(one, dw2), e3 = apply_phase(one, dw3);
+                    f[1] = cmul(f[0], e0);
+#pragma unroll
+                    for (int l = 2; l < 4; ++l) f[l] = cmul(f[l - 2], e1);
+#pragma unroll
+                    for (int l = 4; l < 8; ++l) f[l] = cmul(f[l - 4], e2);
+#pragma unroll
+                    for (int l = 8; l < 16; ++l) f[l] = cmul(f[l - 8], e3);
+#pragma unroll
+                    for (int l = 0; l < 16; ++l) x[l] = cmul(x[l], cmul(tb[l], f[l]));
+                }
                 break;
             }
             default: {

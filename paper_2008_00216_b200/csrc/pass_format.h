@@ -82,8 +82,11 @@ struct alignas(16) StvGDiag {
     uint64_t cst;
     uint64_t w[STV_GROUP_BITS];
     uint64_t A[STV_GROUP_BITS][STV_GROUP_BITS];
-    int32_t n_cross, n_olin, n_oquad, pad;
+    int32_t n_cross, n_olin, n_oquad, n_v;            // n_v = total per-vector terms below
     uint32_t cross_off, olin_off, oquad_off, pad2;    // byte offsets from this record (StvTerm arrays)
+    // per-vector terms: in-tile bits outside the group ("V-bits", tile positions)
+    int32_t n_vlin, n_vquad, n_vcross, n_vout;        // (q) / (q1, q2) / (local j, q) / (q, outside phys p)
+    uint32_t vlin_off, vquad_off, vcross_off, vout_off;
 };
 
 struct alignas(16) StvPass {

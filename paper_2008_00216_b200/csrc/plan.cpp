@@ -533,7 +533,7 @@ struct OpsEval {
     int ntab = 0;
 };
 
-static void tally(OpsEval &ev, int amp_bytes) {
+static void tally(OpsEval &ev, int amp_bytes, uint64_t S = 0) {
     ev.cost = 0;
     ev.rec = sizeof(StvPass);
     ev.ntab = 0;
@@ -548,6 +548,7 @@ static void tally(OpsEval &ev, int amp_bytes) {
         }
         for (auto &o : grp.subs) {
             ev.cost += sub_cost(o);
+            if (o.type == OP_DIAG && (o.qmask & S & ~grp.T)) ev.cost += 14;   // per-vector V-bit factors
             ev.rec += sizeof(StvSub);
             if (o.type == OP_DENSE) ev.rec += (size_t)amp_bytes << (2 * o.tg.size());
             if (o.type == OP_DIAG) {
@@ -582,7 +583,9 @@ static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOpti
             if (taken[i]) continue;
             const PGate &g = gs[i];
             const uint64_t qm = g.qmask(), dm = g.dmask();
-            const uint64_t in_tile = (g.type == GType::DIAG ? qm : dm) & S;
+            // diagonal gates never claim register bits: their in-tile qubits outside
+            // the group become per-vector terms ("V-bits")
+            const uint64_t in_tile = (g.type == GType::DIAG ? 0 : dm) & S;
             bool ok = !(qm & sc.blockedAll) && !(dm & sc.blockedDense) &&
                       __builtin_popcountll(sc.T | in_tile) <= STV_GROUP_BITS;
             if (!ok) {
@@ -602,7 +605,7 @@ static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOpti
         ev.ops.push_back(std::move(grp));
         ev.scan.push_back(sc);
     }
-    tally(ev, amp_bytes);
+    tally(ev, amp_bytes, S);
     return ev;
 }
 
@@ -612,7 +615,7 @@ static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOpti
 static void add_gate(OpsEval &ev, const PGate &g, uint64_t S, const PlanOptions &opt, int amp_bytes) {
     const bool fold = !(opt.flags & SV_OPT_NO_DIAG_FOLD);
     const uint64_t qm = g.qmask(), dm = g.dmask();
-    const uint64_t in_tile = (g.type == GType::DIAG ? qm : dm) & S;
+    const uint64_t in_tile = (g.type == GType::DIAG ? 0 : dm) & S;
     bool placed = false;
     for (size_t k = 0; k < ev.ops.size() && !placed; ++k) {
         GroupScan &sc = ev.scan[k];
@@ -651,7 +654,7 @@ static void add_gate(OpsEval &ev, const PGate &g, uint64_t S, const PlanOptions 
             grp.dmask |= o.dmask;
         }
     }
-    tally(ev, amp_bytes);
+    tally(ev, amp_bytes, S);
 }
 
 // Algorithmic floating-point work per amplitude: a k-qubit
@@ -995,35 +998,52 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                     StvGDiag gd;
                     std::memset(&gd, 0, sizeof(gd));
                     gd.cst = so.form.cst;
-                    std::vector<StvTerm> cross, olin, oquad;
-                    auto lb = [&](int phys) -> int {   // local bit of a group qubit, or -1 if outside the tile
+                    std::vector<StvTerm> cross, olin, oquad, vlin, vquad, vcross, vout;
+                    // qubit class: local bit j (on a group position), outside the tile (-1),
+                    // or an in-tile V-bit (-2 - tile position)
+                    auto cls = [&](int phys) -> int {
                         if (loc[phys] < 0) return -1;
-                        return (int)(std::find(pos.begin(), pos.end(), loc[phys]) - pos.begin());
+                        auto it = std::find(pos.begin(), pos.end(), loc[phys]);
+                        if (it != pos.end()) return (int)(it - pos.begin());
+                        return -2 - loc[phys];
                     };
                     for (auto &kv : so.form.lin) {
-                        int j = lb(kv.first);
-                        if (j >= 0) gd.w[j] += kv.second;
-                        else olin.push_back({kv.first, -1, kv.second});
+                        int c = cls(kv.first);
+                        if (c >= 0) gd.w[c] += kv.second;
+                        else if (c == -1) olin.push_back({kv.first, -1, kv.second});
+                        else vlin.push_back({-2 - c, -1, kv.second});
                     }
                     for (auto &kv : so.form.quad) {
                         int x = kv.first.first, y = kv.first.second;
-                        int jx = lb(x), jy = lb(y);
-                        if (jx >= 0 && jy >= 0) { gd.A[jx][jy] += kv.second; gd.A[jy][jx] += kv.second; }
-                        else if (jx >= 0) cross.push_back({jx, y, kv.second});
-                        else if (jy >= 0) cross.push_back({jy, x, kv.second});
-                        else oquad.push_back({x, y, kv.second});
+                        int cx = cls(x), cy = cls(y);
+                        if (cx < 0 && cy >= 0) { std::swap(cx, cy); std::swap(x, y); }      // local first
+                        if (cx == -1 && cy <= -2) { std::swap(cx, cy); std::swap(x, y); }   // V before outside
+                        if (cx >= 0 && cy >= 0) { gd.A[cx][cy] += kv.second; gd.A[cy][cx] += kv.second; }
+                        else if (cx >= 0 && cy == -1) cross.push_back({cx, y, kv.second});
+                        else if (cx >= 0) vcross.push_back({cx, -2 - cy, kv.second});
+                        else if (cx == -1 && cy == -1) oquad.push_back({x, y, kv.second});
+                        else if (cy <= -2) vquad.push_back({-2 - cx, -2 - cy, kv.second});
+                        else vout.push_back({-2 - cx, y, kv.second});
                     }
                     gd.n_cross = (int)cross.size();
                     gd.n_olin = (int)olin.size();
                     gd.n_oquad = (int)oquad.size();
+                    gd.n_vlin = (int)vlin.size();
+                    gd.n_vquad = (int)vquad.size();
+                    gd.n_vcross = (int)vcross.size();
+                    gd.n_vout = (int)vout.size();
+                    gd.n_v = gd.n_vlin + gd.n_vquad + gd.n_vcross + gd.n_vout;
                     size_t off = sizeof(StvGDiag);
                     gd.cross_off = (uint32_t)off; off += cross.size() * sizeof(StvTerm);
                     gd.olin_off = (uint32_t)off; off += olin.size() * sizeof(StvTerm);
-                    gd.oquad_off = (uint32_t)off;
+                    gd.oquad_off = (uint32_t)off; off += oquad.size() * sizeof(StvTerm);
+                    gd.vlin_off = (uint32_t)off; off += vlin.size() * sizeof(StvTerm);
+                    gd.vquad_off = (uint32_t)off; off += vquad.size() * sizeof(StvTerm);
+                    gd.vcross_off = (uint32_t)off; off += vcross.size() * sizeof(StvTerm);
+                    gd.vout_off = (uint32_t)off;
                     put(b, &gd, sizeof(gd));
-                    put(b, cross.data(), cross.size() * sizeof(StvTerm));
-                    put(b, olin.data(), olin.size() * sizeof(StvTerm));
-                    put(b, oquad.data(), oquad.size() * sizeof(StvTerm));
+                    for (auto *v : {&cross, &olin, &oquad, &vlin, &vquad, &vcross, &vout})
+                        put(b, v->data(), v->size() * sizeof(StvTerm));
                 }
                 align(b, 16);
                 recs[i].nsub = (int)subs[i].size();

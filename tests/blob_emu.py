@@ -39,8 +39,10 @@ class Sub(ct.Structure):
 
 class GDiag(ct.Structure):
     _fields_ = [("cst", ct.c_uint64), ("w", ct.c_uint64 * 4), ("A", (ct.c_uint64 * 4) * 4),
-                ("n_cross", ct.c_int32), ("n_olin", ct.c_int32), ("n_oquad", ct.c_int32), ("pad", ct.c_int32),
-                ("cross_off", ct.c_uint32), ("olin_off", ct.c_uint32), ("oquad_off", ct.c_uint32), ("pad2", ct.c_uint32)]
+                ("n_cross", ct.c_int32), ("n_olin", ct.c_int32), ("n_oquad", ct.c_int32), ("n_v", ct.c_int32),
+                ("cross_off", ct.c_uint32), ("olin_off", ct.c_uint32), ("oquad_off", ct.c_uint32), ("pad2", ct.c_uint32),
+                ("n_vlin", ct.c_int32), ("n_vquad", ct.c_int32), ("n_vcross", ct.c_int32), ("n_vout", ct.c_int32),
+                ("vlin_off", ct.c_uint32), ("vquad_off", ct.c_uint32), ("vcross_off", ct.c_uint32), ("vout_off", ct.c_uint32)]
 
 
 class Pass(ct.Structure):
@@ -143,6 +145,17 @@ def run(n, blob, offs, x0=0, c128=False):
                                     ph += _bits(j, G[q]) * _bits(j, G[r]) * np.uint64(gd.A[q][r])
                             for t in _terms(blob, goff + gd.cross_off, gd.n_cross):
                                 ph += _bits(j, G[t.a]) * _bits(j, t.b) * np.uint64(t.ang)
+                            tpos = [op.tpos[i] for i in range(4)]
+                            for t in _terms(blob, goff + gd.vlin_off, gd.n_vlin):
+                                assert t.a not in tpos
+                                ph += _bits(j, pos2phys[t.a]) * np.uint64(t.ang)
+                            for t in _terms(blob, goff + gd.vquad_off, gd.n_vquad):
+                                ph += _bits(j, pos2phys[t.a]) * _bits(j, pos2phys[t.b]) * np.uint64(t.ang)
+                            for t in _terms(blob, goff + gd.vcross_off, gd.n_vcross):
+                                assert t.b not in tpos
+                                ph += _bits(j, G[t.a]) * _bits(j, pos2phys[t.b]) * np.uint64(t.ang)
+                            for t in _terms(blob, goff + gd.vout_off, gd.n_vout):
+                                ph += _bits(j, pos2phys[t.a]) * _bits(j, t.b) * np.uint64(t.ang)
                             psi = _phase_apply(psi, ph)
                         else:
                             if sb.a >= 0:

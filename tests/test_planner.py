@@ -148,8 +148,8 @@ def _tile_of(ps):
 
 @pytest.mark.parametrize("seed", range(4))
 def test_group_structure(seed):
-    # register-resident gate groups: in-tile qubits of every sub-op fit in the
-    # group's <= 4 register bits; non-diagonal targets are tile bits
+    # register-resident gate groups: non-diagonal targets of every sub-op are
+    # among the group's <= 4 register bits, which are tile bits
     circ = C.random_circuit(12, 200, 100 + seed)
     plan = _check(circ, tile_bits=8, low_bits=3, budget=400)
     ngroups = 0
@@ -168,9 +168,8 @@ def test_group_structure(seed):
                     assert all((T >> q) & 1 for q in so["tg"])
                 elif so["type"] == 3:
                     assert (T >> so["t"]) & 1
-                else:
-                    qs = [b for b, _ in so["lin"]] + [q for p, r, _ in so["quad"] for q in (p, r)]
-                    assert all(((T >> q) & 1) or not ((S >> q) & 1) for q in qs)
+                # diagonal sub-ops may also touch in-tile bits outside T ("V-bits",
+                # per-vector terms) and bits outside the tile (per-tile terms)
     assert ngroups > 0
 
 

@@ -392,278 +392,6 @@ __device__ void diag_op_tile(C *__restrict__ tile, int S, const StvDiag *__restr
 }
 
 // ---------------------------------------------------------------------------
-// register-resident gate groups (OP_GROUP): every consumer thread gathers the
-// 16 amplitudes of one 4-bit vector from the tile, runs the group's sub-op
-// program in registers (U1 / U2 matrices, CNOT register swaps, diagonal
-// phase tables) and scatters them back: one shared-memory round trip for the
-// whole group.  Sub-op bit indices are compile-time template arguments so
-// the vector never leaves registers.
-// ---------------------------------------------------------------------------
-template <typename C>
-__device__ __forceinline__ C cmul(C a, C b) {
-    C r;
-    r.x = a.x * b.x - a.y * b.y;
-    r.y = a.x * b.y + a.y * b.x;
-    return r;
-}
-
-template <int A, typename C>
-__device__ __forceinline__ void g_u1(C (&x)[16], const C *__restrict__ M) {
-    const C m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3];
-#pragma unroll
-    for (int l = 0; l < 16; ++l) {
-        if (l & (1 << A)) continue;
-        const C p = x[l], q = x[l | (1 << A)];
-        C u, w;
-        u.x = 0; u.y = 0; w.x = 0; w.y = 0;
-        u = cfma(m0, p, u); u = cfma(m1, q, u);
-        w = cfma(m2, p, w); w = cfma(m3, q, w);
-        x[l] = u;
-        x[l | (1 << A)] = w;
-    }
-}
-
-template <int A, int B, typename C>
-__device__ __forceinline__ void g_u2(C (&x)[16], const C *__restrict__ M) {
-#pragma unroll
-    for (int l = 0; l < 16; ++l) {
-        if (l & ((1 << A) | (1 << B))) continue;
-        C v[4] = {x[l], x[l | (1 << A)], x[l | (1 << B)], x[l | (1 << A) | (1 << B)]};
-        C o[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            C acc;
-            acc.x = 0; acc.y = 0;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc = cfma(M[r * 4 + c], v[c], acc);
-            o[r] = acc;
-        }
-        x[l] = o[0];
-        x[l | (1 << A)] = o[1];
-        x[l | (1 << B)] = o[2];
-        x[l | (1 << A) | (1 << B)] = o[3];
-    }
-}
-
-template <int CB, int TB, typename C>
-__device__ __forceinline__ void g_cnot(C (&x)[16]) {
-#pragma unroll
-    for (int l = 0; l < 16; ++l) {
-        if (l & (1 << TB)) continue;
-        if (CB >= 0 && !(l & (1 << (CB < 0 ? 0 : CB)))) continue;
-        const C t = x[l];
-        x[l] = x[l | (1 << TB)];
-        x[l | (1 << TB)] = t;
-    }
-}
-
-template <typename C>
-__device__ __forceinline__ void g_u1_dispatch(C (&x)[16], int a, const C *M) {
-    switch (a) {
-    case 0: g_u1<0>(x, M); break;
-    case 1: g_u1<1>(x, M); break;
-    case 2: g_u1<2>(x, M); break;
-    default: g_u1<3>(x, M); break;
-    }
-}
-
-template <typename C>
-__device__ __forceinline__ void g_u2_dispatch(C (&x)[16], int a, int b, const C *M) {
-    switch (a * 4 + b) {
-    case 1: g_u2<0, 1>(x, M); break;
-    case 2: g_u2<0, 2>(x, M); break;
-    case 3: g_u2<0, 3>(x, M); break;
-    case 6: g_u2<1, 2>(x, M); break;
-    case 7: g_u2<1, 3>(x, M); break;
-    default: g_u2<2, 3>(x, M); break;
-    }
-}
-
-template <typename C>
-__device__ __forceinline__ void g_cnot_dispatch(C (&x)[16], int a, int b) {
-    switch ((a + 1) * 4 + b) {
-    case 0: g_cnot<-1, 0>(x); break;
-    case 1: g_cnot<-1, 1>(x); break;
-    case 2: g_cnot<-1, 2>(x); break;
-    case 3: g_cnot<-1, 3>(x); break;
-    case 5: g_cnot<0, 1>(x); break;
-    case 6: g_cnot<0, 2>(x); break;
-    case 7: g_cnot<0, 3>(x); break;
-    case 8: g_cnot<1, 0>(x); break;
-    case 10: g_cnot<1, 2>(x); break;
-    case 11: g_cnot<1, 3>(x); break;
-    case 12: g_cnot<2, 0>(x); break;
-    case 13: g_cnot<2, 1>(x); break;
-    case 15: g_cnot<2, 3>(x); break;
-    case 16: g_cnot<3, 0>(x); break;
-    case 17: g_cnot<3, 1>(x); break;
-    default: g_cnot<3, 2>(x); break;
-    }
-}
-
-// per-tile phase tables of the pass's group DIAG sub-ops: tables[t*16 + l].
-// One warp per table: lanes reduce the per-tile constant (outside-tile linear
-// and pair terms) and the 4 per-tile linear coefficients (cross terms) over
-// strided term lists, then lanes 0..15 finish one entry each.  The pass record
-// lists the StvGDiag offset of every table (tab_off).
-__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-template <typename C, int NT = STV_THREADS>
-__device__ void group_tables(const StvPass *__restrict__ P, int ntab, uint64_t full_base, C *__restrict__ tables,
-                             int ctid) {
-    const uint32_t *tab_off = (const uint32_t *)((const uint8_t *)P + P->tab_off);
-    const int lane = ctid & 31;
-    for (int t = ctid >> 5; t < ntab; t += NT / 32) {
-        const uint8_t *rec = (const uint8_t *)P + tab_off[t];
-        const StvGDiag *G = (const StvGDiag *)rec;
-        uint64_t c = 0, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-        const StvTerm *ol = (const StvTerm *)(rec + G->olin_off);
-        for (int i = lane; i < G->n_olin; i += 32)
-            if ((full_base >> ol[i].a) & 1) c += ol[i].ang;
-        const StvTerm *oq = (const StvTerm *)(rec + G->oquad_off);
-        for (int i = lane; i < G->n_oquad; i += 32)
-            if (((full_base >> oq[i].a) & 1) && ((full_base >> oq[i].b) & 1)) c += oq[i].ang;
-        const StvTerm *cr = (const StvTerm *)(rec + G->cross_off);
-        for (int i = lane; i < G->n_cross; i += 32) {
-            if (!((full_base >> cr[i].b) & 1)) continue;
-            const uint64_t a = cr[i].ang;
-            switch (cr[i].a) {
-            case 0: w0 += a; break;
-            case 1: w1 += a; break;
-            case 2: w2 += a; break;
-            default: w3 += a; break;
-            }
-        }
-        c = warp_sum64(c) + G->cst;
-        w0 = warp_sum64(w0) + G->w[0];
-        w1 = warp_sum64(w1) + G->w[1];
-        w2 = warp_sum64(w2) + G->w[2];
-        w3 = warp_sum64(w3) + G->w[3];
-        if (lane < 16) {
-            const int l = lane;
-            uint64_t ph = c;
-            if (l & 1) ph += w0;
-            if (l & 2) ph += w1;
-            if (l & 4) ph += w2;
-            if (l & 8) ph += w3;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int k2 = j + 1; k2 < 4; ++k2)
-                    if (((l >> j) & 1) && ((l >> k2) & 1)) ph += G->A[j][k2];
-            C one;
-            one.x = 1;
-            one.y = 0;
-            tables[t * 16 + l] = apply_phase(one, ph);
-        }
-    }
-}
-
-template <typename C, int NT = STV_THREADS>
-__device__ void group_op(C *__restrict__ tile, int S, const StvOp &op, const StvPass *__restrict__ P,
-                         const uint8_t *__restrict__ mat, const C *__restrict__ tables, uint64_t full_base, int ctid) {
-    int tp[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) tp[b] = op.tpos[b];
-    uint32_t off[16];
-#pragma unroll
-    for (int l = 0; l < 16; ++l) off[l] = dense_off<4>(l, tp);
-    const StvSub *subs = (const StvSub *)((const uint8_t *)P + op.sub_off);
-    const int nsub = op.nsub;
-    const uint32_t nvec = 1u << (S - 4);
-    const bool pair16 = sizeof(C) == 8 && tp[0] == 0;
-    for (uint32_t v = ctid; v < nvec; v += NT) {
-        const uint32_t base = dense_base<4, C>(v, tp);
-        C x[16];
-        if (pair16) {
-#pragma unroll
-            for (int l = 0; l < 16; l += 2) {
-                const float4 q = *(const float4 *)&tile[base | off[l]];
-                x[l].x = q.x; x[l].y = q.y; x[l + 1].x = q.z; x[l + 1].y = q.w;
-            }
-        } else {
-#pragma unroll
-            for (int l = 0; l < 16; ++l) x[l] = tile[base | off[l]];
-        }
-        for (int k = 0; k < nsub; ++k) {
-            const StvSub &sb = subs[k];
-            switch (sb.type) {
-            case SUB_U1: g_u1_dispatch(x, sb.a, (const C *)(mat + sb.mat_off)); break;
-            case SUB_U2: g_u2_dispatch(x, sb.a, sb.b, (const C *)(mat + sb.mat_off)); break;
-            case SUB_DIAG: {
-                const C *tb = tables + sb.tbl * 16;
-                const uint8_t *rec = (const uint8_t *)P + sb.gdiag_off;
-                const StvGDiag *G = (const StvGDiag *)rec;
-                uint64_t dc = 0, dw0 = 0, dw1 = 0, dw2 = 0, dw3 = 0;
-                if (G->n_v) {
-                    // per-vector terms: V-bits are fixed bits of this vector's base
-                    const StvTerm *t = (const StvTerm *)(rec + G->vlin_off);
-                    for (int i = 0; i < G->n_vlin; ++i)
-                        if ((base >> t[i].a) & 1) dc += t[i].ang;
-                    t = (const StvTerm *)(rec + G->vquad_off);
-                    for (int i = 0; i < G->n_vquad; ++i)
-                        if (((base >> t[i].a) & 1) && ((base >> t[i].b) & 1)) dc += t[i].ang;
-                    t = (const StvTerm *)(rec + G->vout_off);
-                    for (int i = 0; i < G->n_vout; ++i)
-                        if (((base >> t[i].a) & 1) && ((full_base >> t[i].b) & 1)) dc += t[i].ang;
-                    t = (const StvTerm *)(rec + G->vcross_off);
-                    for (int i = 0; i < G->n_vcross; ++i) {
-                        if (!((base >> t[i].b) & 1)) continue;
-                        switch (t[i].a) {
-                        case 0: dw0 += t[i].ang; break;
-                        case 1: dw1 += t[i].ang; break;
-                        case 2: dw2 += t[i].ang; break;
-                        default: dw3 += t[i].ang; break;
-                        }
-                    }
-                }
-                if ((dc | dw0 | dw1 | dw2 | dw3) == 0) {
-#pragma unroll
-                    for (int l = 0; l < 16; ++l) x[l] = cmul(x[l], tb[l]);
-                } else {
-                    C one;
-                    one.x = 1;
-                    one.y = 0;
-                    C f[16];
-                    f[0] = apply_phase(one, dc);
-                    const C e0 = apply_phase(one, dw0), e1 = apply_phase(one, dw1);
-                    const C e2 = apply_phase(one, dw2), e3 = apply_phase(one, dw3);
-                    f[1] = cmul(f[0], e0);
-#pragma unroll
-                    for (int l = 2; l < 4; ++l) f[l] = cmul(f[l - 2], e1);
-#pragma unroll
-                    for (int l = 4; l < 8; ++l) f[l] = cmul(f[l - 4], e2);
-#pragma unroll
-                    for (int l = 8; l < 16; ++l) f[l] = cmul(f[l - 8], e3);
-#pragma unroll
-                    for (int l = 0; l < 16; ++l) x[l] = cmul(x[l], cmul(tb[l], f[l]));
-                }
-                break;
-            }
-            default: {
-                bool on = true;
-                if (sb.c_tile >= 0) on = (base >> sb.c_tile) & 1;
-                if (sb.c_phys >= 0) on = (full_base >> sb.c_phys) & 1;
-                if (on) g_cnot_dispatch(x, sb.a, sb.b);
-            }
-            }
-        }
-        if (pair16) {
-#pragma unroll
-            for (int l = 0; l < 16; l += 2)
-                *(float4 *)&tile[base | off[l]] = make_float4(x[l].x, x[l].y, x[l + 1].x, x[l + 1].y);
-        } else {
-#pragma unroll
-            for (int l = 0; l < 16; ++l) tile[base | off[l]] = x[l];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // the fused tile pass: warp-specialised.
 //   producer warps (kProdWarps): gather the tile's 2^h runs of 2^L amplitudes
 //     into a kStages shared-memory ring -- 16-B cp.async (LDGSTS) per thread
@@ -686,6 +414,8 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_n() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // x + y in the "expanded" domain of mask (carries jump over the gaps):
 // pdep(a + b, m) == masked_add(pdep(a, m), pdep(b, m), m)
@@ -809,16 +539,10 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
         issue((int)((j + 2) % kStages));
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t full_base = base | rank_bits;
-        if (ntab && nops) {
-            group_tables<C>(P, ntab, full_base, tables, tid);
-            __syncthreads();
-        }
         for (int o = 0; o < nops; ++o) {
             const StvOp &op = ops[o];
             const int type = op.type;
-            if (type == OP_GROUP) {
-                group_op<C>(tile, S, op, P, mat, tables, full_base, tid);
-            } else if (type == OP_DENSE) {
+            if (type == OP_DENSE) {
                 int tp[STV_MAX_K];
 #pragma unroll
                 for (int b = 0; b < STV_MAX_K; ++b) tp[b] = op.tpos[b];
@@ -849,21 +573,392 @@ k_tile_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// warp-per-tile fused pass (tiles of <= 2^10 amplitudes, gate groups only):
-// every warp owns whole tiles -- it gathers the next tile with 16-B cp.async
-// into its own double buffer while it runs the current tile's gate groups in
-// registers, so groups need only __syncwarp (no CTA barriers, no producer
-// warps).  The GPU analog of the paper's "one core applies all clustered
-// gates to its resident cache lines".
+// k_group_pass: the fused tile pass for gate-group plans (the default; SURVEY.md
+// 8(a) a5/a6 + NEXT #1).  Tiles are staged in a 3-stage shared-memory ring by
+// 16-B cp.async gathers into the swizzled layout of pass_format.h; per tile the
+// group diagonal tables are built, then every group is one shared-memory round
+// trip: each thread gathers one 16-amplitude vector (bank-conflict-free by the
+// encoder's vector-bit order), runs the sub-op program in registers (U1 / U2
+// matrices, CNOT register swaps, diagonal table factors) and scatters it back.
+// Paper analog: all clustered gates applied to a resident cache line, gates
+// kept in factored form.
 // ---------------------------------------------------------------------------
-constexpr int kWarpTileThreads = 256;
-constexpr int kWarpsPerCta = kWarpTileThreads / 32;
+__device__ __forceinline__ uint32_t swz_hash_d(uint32_t x) {
+    return (uint32_t)(__popc(x & kSwzM0) & 1) | ((uint32_t)(__popc(x & kSwzM1) & 1) << 1) |
+           ((uint32_t)(__popc(x & kSwzM2) & 1) << 2);
+}
 
+// Move one tile between global memory and its swizzled shared-memory stage:
+// thread t moves chunks c = t + NT*k (16 B each) to / from slot
+// c ^ H(c >> 3) = c ^ H(t >> 3) ^ H(NT*k >> 3)  (NT = 256: disjoint bits).
+template <bool kLoad, int NT>
+__device__ __forceinline__ void tile_copy_swz(uint8_t *gstate, uint8_t *stile, uint64_t base, uint64_t hmask,
+                                              uint32_t run_bytes, uint32_t nruns, uint32_t esz, int t,
+                                              uint32_t hash_t) {
+    static_assert(NT >= 8 && (NT & (NT - 1)) == 0, "chunk split assumes a power-of-two thread count");
+    const uint32_t cpr = run_bytes >> 4;             // 16-B chunks per run (power of two)
+    if (cpr >= (uint32_t)NT) {
+        const uint64_t d1 = hmask & (0 - hmask);
+        uint64_t roff = 0;
+        for (uint32_t r = 0; r < nruns; ++r) {
+            uint8_t *g = gstate + (base | roff) * esz;
+            for (uint32_t w = t; w < cpr; w += NT) {
+                const uint32_t c = r * cpr + w;
+                const uint32_t slot = c ^ hash_t ^ swz_hash_d((c - (uint32_t)t) >> 3);
+                uint8_t *sm = stile + (size_t)slot * 16;
+                if (kLoad) cp_async16(sm, g + (size_t)w * 16);
+                else *(uint4 *)(g + (size_t)w * 16) = *(const uint4 *)sm;
+            }
+            roff = masked_add(roff, d1, hmask);
+        }
+    } else {
+        const uint32_t lc = 31 - __clz(cpr);
+        const uint32_t total = nruns * cpr;
+        const uint64_t dstep = pdep64((uint32_t)NT >> lc, hmask);
+        uint64_t roff = pdep64((uint32_t)t >> lc, hmask);
+        const uint32_t within = ((uint32_t)t & (cpr - 1)) * 16;
+        for (uint32_t c = t; c < total; c += NT) {
+            uint8_t *g = gstate + (base | roff) * esz + within;
+            const uint32_t slot = c ^ hash_t ^ swz_hash_d((c - (uint32_t)t) >> 3);
+            uint8_t *sm = stile + (size_t)slot * 16;
+            if (kLoad) cp_async16(sm, g);
+            else *(uint4 *)g = *(const uint4 *)sm;
+            roff = masked_add(roff, dstep, hmask);
+        }
+    }
+}
 
-template <typename R>
-__global__ void __launch_bounds__(kWarpTileThreads, sizeof(R) == 4 ? 2 : 1)
-k_warp_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
-            uint32_t ntiles, int dbg_flags) {
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) {
+    C r;
+    r.x = a.x * b.x - a.y * b.y;
+    r.y = a.x * b.y + a.y * b.x;
+    return r;
+}
+
+// exp(2 pi i ph / 2^64) in double precision, rounded once to the state's type
+template <typename C>
+__device__ __forceinline__ C unit_phase(uint64_t ph) {
+    double s, c;
+    sincospi((double)(int64_t)ph * 1.0842021724855044340074528008699e-19, &s, &c);   // 2^-63
+    C r;
+    r.x = (decltype(r.x))c;
+    r.y = (decltype(r.y))s;
+    return r;
+}
+
+template <int A, typename C>
+__device__ __forceinline__ void g_u1(C (&x)[16], const C *__restrict__ M) {
+    const C m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & (1 << A)) continue;
+        const C p = x[l], q = x[l | (1 << A)];
+        C u, w;
+        u.x = 0; u.y = 0; w.x = 0; w.y = 0;
+        u = cfma(m0, p, u); u = cfma(m1, q, u);
+        w = cfma(m2, p, w); w = cfma(m3, q, w);
+        x[l] = u;
+        x[l | (1 << A)] = w;
+    }
+}
+
+template <int A, int B, typename C>
+__device__ __forceinline__ void g_u2(C (&x)[16], const C *__restrict__ M) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & ((1 << A) | (1 << B))) continue;
+        C v[4] = {x[l], x[l | (1 << A)], x[l | (1 << B)], x[l | (1 << A) | (1 << B)]};
+        C o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            C acc;
+            acc.x = 0; acc.y = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc = cfma(M[r * 4 + c], v[c], acc);
+            o[r] = acc;
+        }
+        x[l] = o[0];
+        x[l | (1 << A)] = o[1];
+        x[l | (1 << B)] = o[2];
+        x[l | (1 << A) | (1 << B)] = o[3];
+    }
+}
+
+// CNOT as predicated register swaps: target TB, in-register control CB (or -1)
+template <int CB, int TB, typename C>
+__device__ __forceinline__ void g_cnot(C (&x)[16], bool on) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & (1 << TB)) continue;
+        if (CB >= 0 && !(l & (1 << (CB < 0 ? 0 : CB)))) continue;
+        const C a = x[l], b = x[l | (1 << TB)];
+        x[l] = on ? b : a;
+        x[l | (1 << TB)] = on ? a : b;
+    }
+}
+
+// ---- complex64 with packed FP32 (FFMA2, sm_100): a complex multiply-add
+// acc += m x is two FFMA2: acc += m_re * (x_re, x_im) (broadcast operand), then
+// acc += (-m_im, m_im) * (x_im, x_re) (swapped operand).  Matrices are encoded
+// as m_re[D*D] scalars followed by (-m_im, m_im)[D*D] pairs (plan.cpp).
+__device__ __forceinline__ float2 cmac2(float mr, float2 mp, float2 x, float2 acc) {
+    acc = __ffma2_rn(make_float2(mr, mr), x, acc);
+    return __ffma2_rn(mp, make_float2(x.y, x.x), acc);
+}
+__device__ __forceinline__ float2 cmul1(float mr, float2 mp, float2 x) {
+    return __ffma2_rn(mp, make_float2(x.y, x.x), __fmul2_rn(make_float2(mr, mr), x));
+}
+
+template <int A>
+__device__ __forceinline__ void g_u1p(float2 (&x)[16], const float *__restrict__ MR, const float2 *__restrict__ MP) {
+    float mr[4];
+    float2 mp[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { mr[e] = MR[e]; mp[e] = MP[e]; }
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & (1 << A)) continue;
+        const float2 p = x[l], q = x[l | (1 << A)];
+        x[l] = cmac2(mr[1], mp[1], q, cmul1(mr[0], mp[0], p));
+        x[l | (1 << A)] = cmac2(mr[3], mp[3], q, cmul1(mr[2], mp[2], p));
+    }
+}
+
+template <int A, int B>
+__device__ __forceinline__ void g_u2p(float2 (&x)[16], const float (&mr)[16], const float2 (&mp)[16]) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & ((1 << A) | (1 << B))) continue;
+        const float2 v[4] = {x[l], x[l | (1 << A)], x[l | (1 << B)], x[l | (1 << A) | (1 << B)]};
+        float2 o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            float2 acc = cmul1(mr[r * 4], mp[r * 4], v[0]);
+#pragma unroll
+            for (int c = 1; c < 4; ++c) acc = cmac2(mr[r * 4 + c], mp[r * 4 + c], v[c], acc);
+            o[r] = acc;
+        }
+        x[l] = o[0];
+        x[l | (1 << A)] = o[1];
+        x[l | (1 << B)] = o[2];
+        x[l | (1 << A) | (1 << B)] = o[3];
+    }
+}
+
+// table entry of a unit phase: complex64 (re, 0, -im, im) for cmul1, complex128 (re, im)
+template <typename C> struct TabEnt;
+template <> struct TabEnt<float2> { using T = float4; };
+template <> struct TabEnt<double2> { using T = double2; };
+
+template <typename C, int NT>
+__device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, uint64_t fb,
+                                             typename TabEnt<C>::T *__restrict__ tables,
+                                             int ctid) {
+    const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
+    const int ntab = P->ntab;
+    const int lane = ctid & 31;
+    for (int t = ctid >> 5; t < ntab; t += NT / 32) {
+        const StvDTab &d = tabs[t];
+        const uint64_t *stat = (const uint64_t *)((const uint8_t *)P + d.stat_off);
+        const StvTerm *tm = (const StvTerm *)((const uint8_t *)P + d.term_off);
+        const int ne = 16 << d.m, nterm = d.nterm;
+        // per-tile coefficients: lane b < 4 + m sums the terms on index bit b, lane 31 the constant
+        uint64_t lam = 0;
+        for (int i = 0; i < nterm; ++i) {
+            const StvTerm q = tm[i];
+            const int who = q.a >= 0 ? q.a : 31;
+            if (who != lane || !((fb >> q.b) & 1)) continue;
+            if (q.a <= -2 && !((fb >> (-2 - q.a)) & 1)) continue;
+            lam += q.ang;
+        }
+        const uint64_t cst = __shfl_sync(0xffffffffu, lam, 31);
+        uint64_t lb[7];
+#pragma unroll
+        for (int b = 0; b < 7; ++b) lb[b] = __shfl_sync(0xffffffffu, lam, b);
+        for (int e = lane; e < ne; e += 32) {
+            uint64_t ph = stat[e] + cst;
+#pragma unroll
+            for (int b = 0; b < 7; ++b)
+                if ((e >> b) & 1) ph += lb[b];
+            const C u = unit_phase<C>(ph);
+            typename TabEnt<C>::T t;
+            if constexpr (sizeof(C) == 8) t = make_float4(u.x, 0.f, -u.y, u.y);
+            else t = u;
+            tables[d.ent_off + (uint32_t)(e >> 4) * STV_TAB_STRIDE + (e & 15)] = t;
+        }
+    }
+}
+
+// Run a group's sub-op program on NV register vectors (same program, the
+// matrices are loaded once per sub-op and shared by the vectors).
+template <typename C, int NV>
+__device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[NV], const StvSub *__restrict__ subs,
+                                         int nsub, const uint8_t *__restrict__ mat, const StvDTab *__restrict__ tabs,
+                                         const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base) {
+    constexpr bool kPacked = sizeof(C) == 8;
+    for (int k = 0; k < nsub; ++k) {
+        const StvSub sb = subs[k];
+        const C *M = (const C *)(mat + ((uint32_t)sb.arg << 4));
+        const float *MR = (const float *)M;
+        switch (sb.code) {
+#define STV_U1(a)                                                                           \
+    case SUBC_U1 + (a): {                                                                   \
+        if constexpr (kPacked) {                                                            \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
+                g_u1p<(a)>(*(float2(*)[16]) & x[i], MR, (const float2 *)(MR + 4));         \
+        } else {                                                                            \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u1<(a)>(x[i], M);               \
+        }                                                                                   \
+        break;                                                                              \
+    }
+            STV_U1(0) STV_U1(1) STV_U1(2) STV_U1(3)
+#undef STV_U1
+#define STV_U2(p, a, b)                                                                     \
+    case SUBC_U2 + (p): {                                                                   \
+        if constexpr (kPacked) {                                                            \
+            float mr[16];                                                                   \
+            float2 mp[16];                                                                  \
+            const float2 *MP = (const float2 *)(MR + 16);                                   \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) { mr[e] = MR[e]; mp[e] = MP[e]; } \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
+                g_u2p<(a), (b)>(*(float2(*)[16]) & x[i], mr, mp);                          \
+        } else {                                                                            \
+            C m[16];                                                                        \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = M[e];                     \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u2<(a), (b)>(x[i], m);         \
+        }                                                                                   \
+        break;                                                                              \
+    }
+            STV_U2(0, 0, 1) STV_U2(1, 0, 2) STV_U2(2, 0, 3) STV_U2(3, 1, 2) STV_U2(4, 1, 3) STV_U2(5, 2, 3)
+#undef STV_U2
+#define STV_CX(c, t)                                                                             \
+    case SUBC_CNOT + 4 * ((c) + 1) + (t): {                                                      \
+        const uint32_t raw = sb.ctl & 0xffffu, ph = sb.ctl >> 16;                                \
+        const bool pon = ph == 0 || ((full_base >> (ph - 1)) & 1);                               \
+        _Pragma("unroll") for (int i = 0; i < NV; ++i)                                           \
+            g_cnot<(c), (t)>(x[i], pon && (raw == 0 || (braw[i] & raw) != 0));                   \
+        break;                                                                                   \
+    }
+            STV_CX(-1, 0) STV_CX(-1, 1) STV_CX(-1, 2) STV_CX(-1, 3)
+            STV_CX(0, 1) STV_CX(0, 2) STV_CX(0, 3)
+            STV_CX(1, 0) STV_CX(1, 2) STV_CX(1, 3)
+            STV_CX(2, 0) STV_CX(2, 1) STV_CX(2, 3)
+            STV_CX(3, 0) STV_CX(3, 1) STV_CX(3, 2)
+#undef STV_CX
+        case SUBC_DIAG: {   // per-tile table row of each vector's V-bits
+            const StvDTab &d = tabs[sb.arg];
+            const uint32_t v0 = d.vraw[0], v1 = d.vraw[1], v2 = d.vraw[2];
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const uint32_t r = ((braw[i] & v0) ? 1u : 0u) | ((braw[i] & v1) ? 2u : 0u) | ((braw[i] & v2) ? 4u : 0u);
+                const typename TabEnt<C>::T *row = tables + d.ent_off + r * STV_TAB_STRIDE;
+                if constexpr (kPacked) {
+                    float2(&xv)[16] = *(float2(*)[16]) & x[i];
+#pragma unroll
+                    for (int l = 0; l < 16; ++l) {
+                        const float4 q = row[l];
+                        xv[l] = cmul1(q.x, make_float2(q.z, q.w), xv[l]);
+                    }
+                } else {
+#pragma unroll
+                    for (int l = 0; l < 16; ++l) x[i][l] = cmul(x[i][l], row[l]);
+                }
+            }
+            break;
+        }
+        default: break;
+        }
+    }
+}
+
+// One group on the resident tile: thread ctid owns vectors v = ctid + NT*(i + NV*k).
+template <typename C, int NT, int NV>
+__device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
+                                             const uint8_t *__restrict__ mat,
+                                             const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base,
+                                             int ctid) {
+    constexpr int TB = NT == 128 ? 7 : 8;   // log2(NT)
+    static_assert((1 << TB) == NT, "NT must be 128 or 256");
+    const int nvb = g.nvb;
+    uint32_t braw0 = 0, bsw0 = 0;
+#pragma unroll
+    for (int b = 0; b < TB; ++b)
+        if (b < nvb && ((ctid >> b) & 1)) {
+            braw0 |= g.vraw[b];
+            bsw0 ^= g.vsw[b];
+        }
+    uint32_t so[16];
+    {
+        const uint4 s0 = *(const uint4 *)&g.sw_off[0], s1 = *(const uint4 *)&g.sw_off[8];
+        const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            so[2 * k] = w[k] & 0xffffu;
+            so[2 * k + 1] = w[k] >> 16;
+        }
+    }
+    const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off);
+    const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
+    const int nsub = g.nsub;
+    const bool pair16 = sizeof(C) == 8 && g.pair16;
+    const uint32_t nvec = 1u << nvb;
+    for (uint32_t v0 = ctid; v0 < nvec; v0 += NT * NV) {
+        uint32_t braw[NV], bsw[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const uint32_t v = v0 + NT * i;
+            braw[i] = braw0;
+            bsw[i] = bsw0;
+            for (int b = TB; b < nvb; ++b)
+                if ((v >> b) & 1) {
+                    braw[i] |= g.vraw[b];
+                    bsw[i] ^= g.vsw[b];
+                }
+        }
+        C x[NV][16];
+        const bool live1 = NV == 1 || v0 + NT < nvec;   // tiny tiles: second vector may not exist
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            if (i > 0 && !live1) {
+#pragma unroll
+                for (int l = 0; l < 16; ++l) { x[i][l].x = 0; x[i][l].y = 0; }
+                continue;
+            }
+            if (pair16) {
+#pragma unroll
+                for (int l = 0; l < 16; l += 2) {
+                    const float4 q = *(const float4 *)&tile[bsw[i] ^ so[l]];
+                    x[i][l].x = q.x; x[i][l].y = q.y; x[i][l + 1].x = q.z; x[i][l + 1].y = q.w;
+                }
+            } else {
+#pragma unroll
+                for (int l = 0; l < 16; ++l) x[i][l] = tile[bsw[i] ^ so[l]];
+            }
+        }
+        run_subs<C, NV>(x, braw, subs, nsub, mat, tabs, tables, full_base);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            if (i > 0 && !live1) continue;
+            if (pair16) {
+#pragma unroll
+                for (int l = 0; l < 16; l += 2)
+                    *(float4 *)&tile[bsw[i] ^ so[l]] = make_float4(x[i][l].x, x[i][l].y, x[i][l + 1].x, x[i][l + 1].y);
+            } else {
+#pragma unroll
+                for (int l = 0; l < 16; ++l) tile[bsw[i] ^ so[l]] = x[i][l];
+            }
+        }
+    }
+}
+
+constexpr int kGThreads = 128;     // group pass CTA: 4 warps, 2 vectors per thread (complex64)
+constexpr int kGStages = 2;        // double-buffered tiles (prefetch distance 1)
+
+template <typename R, int NV>
+__global__ void __launch_bounds__(kGThreads, sizeof(R) == 4 ? 3 : 2)
+k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
+             uint32_t ntiles, int dbg_flags) {
     using C = typename C2T<R>::T;
     extern __shared__ __align__(1024) uint8_t smem[];
     const StvPass *G = (const StvPass *)(blob + pass_off);
@@ -871,54 +966,60 @@ k_warp_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ 
     const uint32_t rec_pad = (rec_bytes + 127u) & ~127u;
     const StvPass *P = (const StvPass *)smem;
     for (uint32_t k = threadIdx.x; k < rec_bytes / 16; k += blockDim.x) ((uint4 *)smem)[k] = ((const uint4 *)G)[k];
-    __syncthreads();
-    const int S = P->S, L = P->L, h = P->h;
-    const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
-    const int nops = (dbg_flags & 1) ? 0 : P->nops;
-    const StvOp *ops = (const StvOp *)((const uint8_t *)P + P->ops_off);
-    const uint8_t *mat = (const uint8_t *)P + P->mat_off;
-    const int ntab = P->ntab;
+    const int S = G->S, L = G->L, h = G->h;
+    const uint64_t out_mask = G->out_mask, rank_bits = G->rank_bits;
+    const int nops = (dbg_flags & 1) ? 0 : G->nops;   // bit 0: data movement only (microbenchmark)
+    const int ntab = G->ntab;
+    const StvGroup *groups = (const StvGroup *)((const uint8_t *)P + G->ops_off);
+    const uint8_t *mat = (const uint8_t *)P + G->mat_off;
     const uint32_t esz = sizeof(C);
+    const uint32_t tab_pad = (G->tab_entries * 16u + 127u) & ~127u;       // 16-B table entries
+    typename TabEnt<C>::T *tables = (typename TabEnt<C>::T *)(smem + rec_pad);
+    C *tiles = (C *)(smem + rec_pad + tab_pad);
     const uint32_t tile_elems = 1u << S;
     const uint32_t run_bytes = (1u << L) * esz;
     const uint32_t nruns = 1u << h;
-    const uint32_t tab_bytes = ((uint32_t)ntab * 16 * esz + 127u) & ~127u;
-    const uint32_t warp_bytes = 2 * tile_elems * esz + tab_bytes;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint8_t *wsm = smem + rec_pad + (size_t)warp * warp_bytes;
-    C *buf[2] = {(C *)wsm, (C *)(wsm + (size_t)tile_elems * esz)};
-    C *tables = (C *)(wsm + 2 * (size_t)tile_elems * esz);
-    uint64_t hmask = 0;
-    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
-    uint8_t *gstate = (uint8_t *)state;
+    const int tid = threadIdx.x;
+    const uint32_t hash_t = swz_hash_d((uint32_t)tid >> 3);
+    __syncthreads();
 
-    const uint32_t gw = blockIdx.x * kWarpsPerCta + warp, nw = gridDim.x * kWarpsPerCta;
-    const uint32_t my_tiles = gw < ntiles ? (ntiles - gw + nw - 1) / nw : 0;
-    uint64_t tb = pdep64(gw, out_mask);
-    const uint64_t tstep = pdep64(nw, out_mask);
-    if (my_tiles) tile_copy16<true, 32>(gstate, (uint8_t *)buf[0], tb, hmask, run_bytes, nruns, esz, lane);
-    cp_async_commit();
-    for (uint32_t j = 0; j < my_tiles; ++j) {
-        const uint64_t base = tb;
-        tb = masked_add(tb, tstep, out_mask);
-        if (j + 1 < my_tiles)
-            tile_copy16<true, 32>(gstate, (uint8_t *)buf[(j + 1) & 1], tb, hmask, run_bytes, nruns, esz, lane);
+    const uint32_t first = blockIdx.x, stride = gridDim.x;
+    const uint32_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+    uint64_t hmask = 0;
+    for (int r = 0; r < h; ++r) hmask |= 1ull << G->hpos[r];
+    uint8_t *gstate = (uint8_t *)state;
+    const uint64_t tstep = pdep64(stride, out_mask);
+    uint64_t load_tb = pdep64(first, out_mask);
+    uint32_t loaded = 0;
+    auto issue = [&](int s) {
+        uint8_t *stile = (uint8_t *)(tiles + (size_t)s * tile_elems);
+        if (loaded < my_tiles)
+            tile_copy_swz<true, kGThreads>(gstate, stile, load_tb, hmask, run_bytes, nruns, esz, tid, hash_t);
         cp_async_commit();
-        cp_async_wait1();
-        __syncwarp();
-        C *tile = buf[j & 1];
+        load_tb = masked_add(load_tb, tstep, out_mask);
+        ++loaded;
+    };
+    for (int s = 0; s < kGStages - 1; ++s) issue(s);
+    uint64_t base = pdep64(first, out_mask);
+    for (uint32_t j = 0; j < my_tiles; ++j) {
+        const int s = (int)(j % kGStages);
+        cp_async_wait_n<kGStages - 2>();
+        __syncthreads();                                 // tile j visible; stage (j-1)%kGStages free
+        issue((int)((j + kGStages - 1) % kGStages));
+        C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t full_base = base | rank_bits;
         if (ntab && nops) {
-            group_tables<C, 32>(P, ntab, full_base, tables, lane);
-            __syncwarp();
+            build_tables<C, kGThreads>(P, full_base, tables, tid);
+            __syncthreads();
         }
         for (int o = 0; o < nops; ++o) {
-            group_op<C, 32>(tile, S, ops[o], P, mat, tables, full_base, lane);
-            __syncwarp();
+            group_vec_op<C, kGThreads, NV>(tile, groups[o], P, mat, tables, full_base, tid);
+            __syncthreads();
         }
-        tile_copy16<false, 32>(gstate, (uint8_t *)tile, base, hmask, run_bytes, nruns, esz, lane);
-        __syncwarp();
+        tile_copy_swz<false, kGThreads>(gstate, (uint8_t *)tile, base, hmask, run_bytes, nruns, esz, tid, hash_t);
+        base = masked_add(base, tstep, out_mask);
     }
+    cp_async_wait0();
 }
 
 // ---------------------------------------------------------------------------
@@ -1136,41 +1237,39 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
     return e;
 }
 
-cudaError_t launch_warp_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
-                             uint32_t rec_bytes, int ntab, cudaStream_t st, int *kernels) {
+cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
+                              uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st, int *kernels) {
     const size_t esz = c128 ? 16 : 8;
-    const size_t tab = ((size_t)ntab * 16 * esz + 127) & ~(size_t)127;
-    const size_t per_warp = 2 * (esz << S) + tab;
-    const size_t smem = ((rec_bytes + 127u) & ~127u) + kWarpsPerCta * per_warp;
+    const size_t smem = ((rec_bytes + 127u) & ~127u) + (((size_t)tab_entries * 16 + 127u) & ~(size_t)127) +
+                        (size_t)kGStages * (esz << S);
     const uint64_t ntiles = 1ull << (n_local - S);
     if (smem > 227 * 1024 || (ntiles >> 32)) return cudaErrorInvalidValue;
-    int occ = 0;
-    if (c128) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_warp_pass<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            attr = true;
+    static const int nv_env = getenv("STV_NV") ? atoi(getenv("STV_NV")) : 2;
+    auto kf = c128 ? (const void *)k_group_pass<double, 1>
+                   : (nv_env == 1 ? (const void *)k_group_pass<float, 1> : (const void *)k_group_pass<float, 2>);
+    static const void *attr_done[3] = {nullptr, nullptr, nullptr};
+    {
+        int slot = c128 ? 0 : (nv_env == 1 ? 1 : 2);
+        if (attr_done[slot] != kf) {
+            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr_done[slot] = kf;
         }
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp_pass<double>, kWarpTileThreads, smem);
-    } else {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_warp_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            attr = true;
-        }
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_warp_pass<float>, kWarpTileThreads, smem);
     }
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kGThreads, smem);
     if (occ < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)num_sms() * occ;
-    const uint64_t need = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
-    if (grid > need) grid = need;
+    if (grid > ntiles) grid = ntiles;
     static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
     if (c128)
-        k_warp_pass<double><<<(unsigned)grid, kWarpTileThreads, smem, st>>>((double2 *)state, dblob, pass_off,
+        k_group_pass<double, 1><<<(unsigned)grid, kGThreads, smem, st>>>((double2 *)state, dblob, pass_off,
+                                                                            (uint32_t)ntiles, dbg);
+    else if (nv_env == 1)
+        k_group_pass<float, 1><<<(unsigned)grid, kGThreads, smem, st>>>((float2 *)state, dblob, pass_off,
                                                                            (uint32_t)ntiles, dbg);
     else
-        k_warp_pass<float><<<(unsigned)grid, kWarpTileThreads, smem, st>>>((float2 *)state, dblob, pass_off,
-                                                                          (uint32_t)ntiles, dbg);
+        k_group_pass<float, 2><<<(unsigned)grid, kGThreads, smem, st>>>((float2 *)state, dblob, pass_off,
+                                                                           (uint32_t)ntiles, dbg);
     ++*kernels;
     return cudaGetLastError();
 }

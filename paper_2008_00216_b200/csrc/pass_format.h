@@ -19,13 +19,9 @@
 #define OP_CNOT 3
 #define OP_GROUP 4
 
-// sub-ops of a register-resident gate group (OP_GROUP)
-#define SUB_U1 1
-#define SUB_U2 2
-#define SUB_DIAG 3
-#define SUB_CNOT 4
 #define STV_GROUP_BITS 4
 #define STV_MAX_TABLES 32
+#define STV_MAX_VBITS 3          // in-tile bits outside the group a diag table may index
 
 #define STV_MAX_TILE_BITS 14
 #define STV_MAX_K 4
@@ -64,31 +60,6 @@ struct alignas(16) StvOp {
     int32_t pad;
 };
 
-// One sub-op of a gate group; local bits index the group's tpos[0..3].
-struct alignas(16) StvSub {
-    int32_t type;              // SUB_*
-    int32_t a, b;              // U1: a; U2: a < b (matrix local index bit0 = a, bit1 = b);
-                               // CNOT: a = local control or -1, b = local target
-    int32_t c_tile;            // CNOT: tile-local control position outside the group, or -1
-    int32_t c_phys;            // CNOT: physical control bit outside the tile, or -1
-    uint32_t mat_off;          // U1/U2: byte offset in the pass matrix area
-    uint32_t gdiag_off;        // DIAG: byte offset of StvGDiag from the PassDesc
-    int32_t tbl;               // DIAG: index of its per-tile phase table
-};
-
-// Diagonal sub-op over the group's 4 local bits + bits outside the tile:
-//   phase = cst + sum_{olin} + sum_{oquad} + sum_j b_j (w[j] + sum_{cross(j,p)}) + sum_{j<k} A[j][k] b_j b_k
-struct alignas(16) StvGDiag {
-    uint64_t cst;
-    uint64_t w[STV_GROUP_BITS];
-    uint64_t A[STV_GROUP_BITS][STV_GROUP_BITS];
-    int32_t n_cross, n_olin, n_oquad, n_v;            // n_v = total per-vector terms below
-    uint32_t cross_off, olin_off, oquad_off, pad2;    // byte offsets from this record (StvTerm arrays)
-    // per-vector terms: in-tile bits outside the group ("V-bits", tile positions)
-    int32_t n_vlin, n_vquad, n_vcross, n_vout;        // (q) / (q1, q2) / (local j, q) / (q, outside phys p)
-    uint32_t vlin_off, vquad_off, vcross_off, vout_off;
-};
-
 struct alignas(16) StvPass {
     int32_t kind;
     int32_t S, L, h;
@@ -103,6 +74,78 @@ struct alignas(16) StvPass {
     uint32_t diag_off;         // PASS_DIAG: StvDiag offset (tile = low S bits)
     uint32_t rec_bytes;        // size of this pass record (multiple of 16)
     int32_t ntab;              // per-tile phase tables of group DIAG sub-ops
-    uint32_t tab_off;          // byte offset of uint32 StvGDiag offsets, one per table
-    int32_t pad2[3];
+    uint32_t tab_off;          // byte offset of StvDTab[ntab]
+    int32_t grouped;           // 1: every op is a gate group (StvGroup[nops] at ops_off), k_group_pass
+    uint32_t tab_entries;      // total table entries (amplitudes) in shared memory
+    int32_t pad2;
 };
+
+// ---------------------------------------------------------------------------
+// Gate-group passes (k_group_pass).  A group owns 4 tile positions tpos[0..3]
+// (local index bit j <-> tile position tpos[j]); every thread gathers the 16
+// amplitudes of one vector (fixed values of the other S-4 "vector" bits) into
+// registers, runs the sub-op program and scatters them back.
+//
+// Shared-memory tile layout (bank-conflict-free gathers): the tile is stored
+// in 16-B chunks (2 complex64 / 1 complex128 amplitudes); chunk c lives in slot
+//     swz(c) = c ^ H(c >> 3),   H(x) = XOR_j x_j * kSwzH[j]  (3-bit values)
+// which is linear over GF(2).  A warp phase of 8 lanes (LDS.128) is
+// conflict-free iff its 3 varying chunk bits have independent bank vectors
+// (chunk bits 0..2: 1, 2, 4; bit 3+j: kSwzH[j]); the encoder orders every
+// group's vector bits so that lane bits 0..2 (0..3 for 8-B accesses) meet that.
+// ---------------------------------------------------------------------------
+#define STV_SWZ_NH 11
+#ifdef __cplusplus
+static constexpr uint32_t kSwzH[STV_SWZ_NH] = {3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7};
+static constexpr uint32_t swz_mask(int bit) {
+    uint32_t m = 0;
+    for (int j = 0; j < STV_SWZ_NH; ++j)
+        if ((kSwzH[j] >> bit) & 1) m |= 1u << j;
+    return m;
+}
+static constexpr uint32_t kSwzM0 = swz_mask(0), kSwzM1 = swz_mask(1), kSwzM2 = swz_mask(2);
+#endif
+
+// sub-op dispatch codes (dense, so the device switch is one jump table)
+#define SUBC_U1 0                // + a (0..3)
+#define SUBC_U2 4                // + pair index of (a<b): 01 02 03 12 13 23 -> 0..5
+#define SUBC_CNOT 10             // + 4 * (c + 1) + t, c = in-register control or -1
+#define SUBC_DIAG 30
+#define SUBC_N 31
+
+// one sub-op (8 B, one shared-memory load)
+struct alignas(8) StvSub {
+    uint16_t code;             // SUBC_*
+    uint16_t arg;              // U1/U2: matrix byte offset / 16 in the pass matrix area; DIAG: table index
+    uint32_t ctl;              // CNOT: bits 0..15 raw tile offset of a control on a vector bit (0 = none);
+                               //       bits 16..23 physical control bit + 1 outside the tile (0 = none)
+};
+
+struct alignas(16) StvGroup {
+    int32_t nsub;
+    uint32_t sub_off;          // byte offset of StvSub[nsub] from the pass record
+    int32_t nvb;               // number of vector bits (S - 4)
+    int32_t pair16;            // complex64 with tpos[0] == 0: amplitudes l, l|1 share a 16-B chunk
+    int32_t tpos[4];
+    uint16_t sw_off[16];       // swizzled tile offset (amplitudes) of local index l
+    uint16_t vsw[STV_MAX_TILE_BITS - 4];    // swizzled offset of vector bit b
+    uint16_t vraw[STV_MAX_TILE_BITS - 4];   // raw tile offset (1 << position) of vector bit b
+};
+
+// Per-tile phase table of one group DIAG sub-op, over index e = l | (r << 4):
+// l = the group's local bits, r = its m V-bits (in-tile bits outside the group).
+//   phase(e) = stat[e] + sum of the per-tile terms active for this tile
+// Per-tile term {a, b, ang}: a >= 0: index bit a of e times bit b of the
+// tile's full base; a == -1: bit b of the base; a <= -2: bits (-2 - a) and b.
+// Entries live in shared memory at ent_off + r * STV_TAB_STRIDE + l (rows padded against
+// bank conflicts between lanes with different r; rows are read as 16-B pairs).
+struct alignas(16) StvDTab {
+    uint32_t stat_off;         // byte offset (pass record) of uint64 stat[16 << m]
+    uint32_t term_off;         // byte offset of StvTerm[nterm]
+    int32_t nterm;
+    int32_t m;
+    uint32_t ent_off;          // first entry in the shared-memory table area
+    uint16_t vraw[STV_MAX_VBITS];   // raw tile offsets of the V-bits (0 for unused)
+    uint16_t pad;
+};
+#define STV_TAB_STRIDE 18        // entries per table row: 16 + 2 pad (16-B aligned rows, no bank conflicts)

@@ -533,6 +533,30 @@ struct OpsEval {
     int ntab = 0;
 };
 
+// Shared-memory bytes (pass record + table area) of a group diagonal sub-op:
+// the greedy split of its terms into tables of <= STV_MAX_VBITS V-bits
+// (vmask = in-tile qubits outside the group; mirrors split_group_diag).
+static size_t diag_table_bytes(const QForm &f, uint64_t vmask, int amp_bytes, int *ntab) {
+    std::vector<uint64_t> sets;
+    auto place = [&](uint64_t need) {
+        for (uint64_t &u : sets)
+            if (__builtin_popcountll(u | need) <= STV_MAX_VBITS) { u |= need; return; }
+        sets.push_back(need);
+    };
+    size_t terms = 0;
+    for (auto &kv : f.lin) place(vmask & (1ull << kv.first));
+    for (auto &kv : f.quad) place(vmask & ((1ull << kv.first.first) | (1ull << kv.first.second)));
+    terms = f.lin.size() + f.quad.size();
+    if (sets.empty()) sets.push_back(0);
+    size_t bytes = sizeof(StvTerm) * terms;
+    for (uint64_t u : sets) {
+        const int m = __builtin_popcountll(u);
+        bytes += sizeof(StvDTab) + sizeof(StvSub) + ((size_t)128 << m) + ((size_t)(STV_TAB_STRIDE * 16) << m) + 32;
+    }
+    *ntab = (int)sets.size();
+    return bytes;
+}
+
 static void tally(OpsEval &ev, int amp_bytes, uint64_t S = 0) {
     ev.cost = 0;
     ev.rec = sizeof(StvPass);
@@ -548,16 +572,17 @@ static void tally(OpsEval &ev, int amp_bytes, uint64_t S = 0) {
         }
         for (auto &o : grp.subs) {
             ev.cost += sub_cost(o);
-            if (o.type == OP_DIAG && (o.qmask & S & ~grp.T)) ev.cost += 14;   // per-vector V-bit factors
             ev.rec += sizeof(StvSub);
             if (o.type == OP_DENSE) ev.rec += (size_t)amp_bytes << (2 * o.tg.size());
             if (o.type == OP_DIAG) {
-                ev.rec += sizeof(StvGDiag) + sizeof(StvTerm) * (o.form.lin.size() + o.form.quad.size());
-                ++ev.ntab;
+                // per-tile tables over the group bits + V-bits, split as the encoder does
+                int ntb = 0;
+                ev.rec += diag_table_bytes(o.form, S & ~grp.T, amp_bytes, &ntb);
+                ev.ntab += ntb;
             }
         }
         ev.cost += 16;                           // the group's shared-memory round trip
-        ev.rec += sizeof(StvOp) + 4;
+        ev.rec += sizeof(StvGroup);
     }
 }
 
@@ -686,6 +711,12 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
     std::vector<char> done(G, 0);
     size_t first = 0;
     const double amp_pass_bytes = 2.0 * amp_bytes * std::ldexp(1.0, nl);   // R+W per rank
+    // pass record + diag tables share the CTA's shared memory with 3 tile stages:
+    // keep two 256-thread CTAs per SM when the tiles allow it
+    const size_t tile_b = (size_t)amp_bytes << opt.tile_bits;
+    size_t rec_limit = kMaxRecBytes;
+    if (3 * tile_b <= 96 * 1024) rec_limit = std::min(rec_limit, (size_t)112 * 1024 - 3 * tile_b);
+    else if (3 * tile_b < 224 * 1024) rec_limit = std::min(rec_limit, (size_t)224 * 1024 - 3 * tile_b);
 
     while (true) {
         while (first < G && done[first]) ++first;
@@ -714,7 +745,7 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                     std::swap(cur, t);
                 }
                 if (pgates.size() > 1 &&
-                    (cur.cost > opt.budget || cur.rec > kMaxRecBytes || cur.ntab > STV_MAX_TABLES)) {
+                    (cur.cost > opt.budget || cur.rec > rec_limit || cur.ntab > STV_MAX_TABLES)) {
                     ok = false;
                     pgates.pop_back();
                     cur = make_ops(pgates, S, opt, amp_bytes);        // rare: rebuild without g
@@ -807,7 +838,7 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
             for (int b = 0; b < nl && __builtin_popcountll(S) < opt.tile_bits; ++b) S |= 1ull << b;
             if (S != S0) {
                 OpsEval fin = make_ops(pgates, S, opt, amp_bytes);
-                if (fin.rec <= kMaxRecBytes && fin.ntab <= STV_MAX_TABLES) pass.ops = fin.ops;
+                if (fin.rec <= rec_limit && fin.ntab <= STV_MAX_TABLES) pass.ops = fin.ops;
                 else S = S0;
             }
             pass.S = S;
@@ -873,6 +904,117 @@ static void encode_diag(std::vector<uint8_t> &b, size_t rec_at, const QForm &f, 
     put(b, oquad.data(), oquad.size() * sizeof(StvTerm));
 }
 
+// Shared-memory slot of tile amplitude i under the chunk swizzle of
+// pass_format.h (linear over GF(2)).
+static uint32_t swz_hash(uint32_t x) {
+    return (uint32_t)(__builtin_popcount(x & kSwzM0) & 1) | ((uint32_t)(__builtin_popcount(x & kSwzM1) & 1) << 1) |
+           ((uint32_t)(__builtin_popcount(x & kSwzM2) & 1) << 2);
+}
+static uint32_t swz_amp(uint32_t i, bool c128) {
+    if (c128) return i ^ swz_hash(i >> 3);
+    const uint32_t c = i >> 1;
+    return (((c ^ swz_hash(c >> 3))) << 1) | (i & 1);
+}
+
+// bank vector (3 bits) of tile position p: which 16-B bank group a chunk bit selects
+static uint32_t bank_vec(int p, bool c128) {
+    const int j = c128 ? p : p - 1;          // chunk bit
+    if (j < 0) return 0;
+    return j < 3 ? (1u << j) : kSwzH[j - 3];
+}
+
+// Order of a group's vector bits: lane bits 0..2 (LDS.128 phases of 8 lanes)
+// get positions with linearly independent bank vectors; a complex64 group
+// without position 0 uses 8-B accesses (16-lane phases), so position 0 leads.
+static std::vector<int> vector_bit_order(const std::vector<int> &pos, int S, bool c128) {
+    std::vector<int> R, head, order;
+    for (int q = 0; q < S; ++q)
+        if (std::find(pos.begin(), pos.end(), q) == pos.end()) R.push_back(q);
+    if (!c128 && pos[0] != 0) head.push_back(0);
+    std::vector<uint32_t> basis;
+    auto reduce = [&](uint32_t v) {
+        for (uint32_t b : basis) v = std::min(v, v ^ b);
+        return v;
+    };
+    for (int q : R) {
+        if (basis.size() >= 3) break;
+        if (!c128 && q == 0) continue;
+        const uint32_t v = reduce(bank_vec(q, c128));
+        if (v) { basis.push_back(v); head.push_back(q); }
+    }
+    order = head;
+    for (int q : R)
+        if (std::find(head.begin(), head.end(), q) == head.end()) order.push_back(q);
+    return order;
+}
+
+// One per-tile phase table of a group diagonal sub-op (pass_format.h StvDTab).
+struct GroupTable {
+    std::vector<int> vpos;           // tile positions of its V-bits (<= STV_MAX_VBITS)
+    std::vector<uint64_t> stat;      // static phases, index l | r << 4
+    std::vector<StvTerm> terms;      // per-tile terms
+};
+
+// Split a group's diagonal form into tables of <= STV_MAX_VBITS V-bits each
+// (diagonal terms commute and add, so the split is exact).
+static std::vector<GroupTable> split_group_diag(const QForm &f, const std::vector<int> &pos, const int *loc) {
+    struct Item { int x, y; uint64_t ang; };   // y = -1: linear term on x
+    std::vector<Item> items;
+    for (auto &kv : f.lin) items.push_back({kv.first, -1, kv.second});
+    for (auto &kv : f.quad) items.push_back({kv.first.first, kv.first.second, kv.second});
+    auto is_v = [&](int phys) {
+        return loc[phys] >= 0 && std::find(pos.begin(), pos.end(), loc[phys]) == pos.end();
+    };
+    std::vector<std::vector<int>> vsets;       // per table: V tile positions
+    std::vector<std::vector<Item>> members;
+    for (const Item &it : items) {
+        std::vector<int> need;
+        for (int q : {it.x, it.y})
+            if (q >= 0 && is_v(q)) need.push_back(loc[q]);
+        size_t t = 0;
+        for (; t < vsets.size(); ++t) {
+            std::vector<int> u = vsets[t];
+            for (int v : need)
+                if (std::find(u.begin(), u.end(), v) == u.end()) u.push_back(v);
+            if ((int)u.size() <= STV_MAX_VBITS) { vsets[t] = u; break; }
+        }
+        if (t == vsets.size()) { vsets.push_back(need); members.emplace_back(); }
+        members[t].push_back(it);
+    }
+    if (vsets.empty()) { vsets.emplace_back(); members.emplace_back(); }   // constant-only form
+    std::vector<GroupTable> out;
+    for (size_t t = 0; t < vsets.size(); ++t) {
+        GroupTable gt;
+        gt.vpos = vsets[t];
+        std::sort(gt.vpos.begin(), gt.vpos.end());
+        const int m = (int)gt.vpos.size();
+        // index bit of a physical qubit in this table (-1: outside the tile)
+        auto ibit = [&](int phys) -> int {
+            if (loc[phys] < 0) return -1;
+            auto it = std::find(pos.begin(), pos.end(), loc[phys]);
+            if (it != pos.end()) return (int)(it - pos.begin());
+            return 4 + (int)(std::find(gt.vpos.begin(), gt.vpos.end(), loc[phys]) - gt.vpos.begin());
+        };
+        gt.stat.assign((size_t)16 << m, t == 0 ? f.cst : 0);
+        for (const Item &it : members[t]) {
+            const int bx = ibit(it.x), by = it.y >= 0 ? ibit(it.y) : -1;
+            if (it.y < 0) {
+                if (bx >= 0) {
+                    for (size_t e = 0; e < gt.stat.size(); ++e)
+                        if ((e >> bx) & 1) gt.stat[e] += it.ang;
+                } else gt.terms.push_back({-1, it.x, it.ang});
+            } else if (bx >= 0 && by >= 0) {
+                for (size_t e = 0; e < gt.stat.size(); ++e)
+                    if (((e >> bx) & 1) && ((e >> by) & 1)) gt.stat[e] += it.ang;
+            } else if (bx >= 0) gt.terms.push_back({bx, it.y, it.ang});
+            else if (by >= 0) gt.terms.push_back({by, it.x, it.ang});
+            else gt.terms.push_back({-2 - it.x, it.y, it.ang});
+        }
+        out.push_back(gt);
+    }
+    return out;
+}
+
 Encoded encode(const Plan &p, int n_local, bool c128) {
     Encoded e;
     std::vector<uint8_t> &b = e.blob;
@@ -903,7 +1045,9 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
             align(b, 16);
             hd.ops_off = (uint32_t)(b.size() - at);
             const size_t ops_at = b.size();
-            b.resize(ops_at + ps.ops.size() * sizeof(StvOp));
+            bool grouped = !ps.ops.empty();
+            for (auto &o : ps.ops) grouped &= (o.type == OP_GROUP);
+            b.resize(ops_at + ps.ops.size() * (grouped ? sizeof(StvGroup) : sizeof(StvOp)));
             std::vector<StvOp> recs(ps.ops.size());
             std::vector<std::vector<StvSub>> subs(ps.ops.size());
             std::vector<std::vector<int>> gpos(ps.ops.size());   // group tile positions (sorted)
@@ -913,6 +1057,17 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                     if (c128) { double v[2] = {z.real(), z.imag()}; put(b, v, 16); }
                     else { float v[2] = {(float)z.real(), (float)z.imag()}; put(b, v, 8); }
                 }
+                align(b, 16);
+                return off;
+            };
+            // group sub-op matrices, complex64: re parts (scalars, broadcast operands of
+            // FFMA2), then (-im, im) pairs, so a complex multiply-add is two FFMA2
+            auto put_matrix_packed = [&](const std::vector<cd> &M) -> uint32_t {
+                if (c128) return put_matrix(M);
+                const uint32_t off = (uint32_t)(b.size() - at - hd.mat_off);
+                for (const cd &z : M) { float v = (float)z.real(); put(b, &v, 4); }
+                align(b, 8);
+                for (const cd &z : M) { float v[2] = {-(float)z.imag(), (float)z.imag()}; put(b, v, 8); }
                 align(b, 16);
                 return off;
             };
@@ -941,8 +1096,6 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                         if (std::find(pos.begin(), pos.end(), q) == pos.end()) pos.push_back(q);
                     std::sort(pos.begin(), pos.end());
                     gpos[i] = pos;
-                    r.k = (int)pos.size();
-                    for (int j = 0; j < r.k; ++j) r.tpos[j] = pos[j];
                     auto lbit = [&](int phys) {
                         const int tp = loc[phys];
                         return (int)(std::find(pos.begin(), pos.end(), tp) - pos.begin());
@@ -950,24 +1103,27 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                     for (const FOp &so : o.subs) {
                         StvSub sub;
                         std::memset(&sub, 0, sizeof(sub));
-                        sub.c_tile = sub.c_phys = -1;
-                        sub.a = sub.b = -1;
                         if (so.type == OP_DENSE) {
-                            sub.type = so.tg.size() == 1 ? SUB_U1 : SUB_U2;
-                            sub.a = lbit(so.tg[0]);
-                            if (so.tg.size() == 2) sub.b = lbit(so.tg[1]);
-                            sub.mat_off = put_matrix(so.M);
+                            const int x = lbit(so.tg[0]);
+                            if (so.tg.size() == 1) sub.code = SUBC_U1 + x;
+                            else {
+                                static const int pidx[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
+                                sub.code = (uint16_t)(SUBC_U2 + pidx[x][lbit(so.tg[1])]);
+                            }
+                            const uint32_t mo = put_matrix_packed(so.M);
+                            if (mo % 16 || mo / 16 > 0xffff) throw std::runtime_error("matrix offset");
+                            sub.arg = (uint16_t)(mo / 16);
                         } else if (so.type == OP_CNOT) {
-                            sub.type = SUB_CNOT;
-                            sub.b = lbit(so.t);
+                            int c = -1;
                             // a control on one of the group's 4 positions (a T bit or a padding
                             // position) varies inside the register vector: in-register control
                             if (loc[so.c] >= 0 && std::find(pos.begin(), pos.end(), loc[so.c]) != pos.end())
-                                sub.a = lbit(so.c);
-                            else if (loc[so.c] >= 0) sub.c_tile = loc[so.c];
-                            else sub.c_phys = so.c;
+                                c = lbit(so.c);
+                            else if (loc[so.c] >= 0) sub.ctl = 1u << loc[so.c];
+                            else sub.ctl = (uint32_t)(so.c + 1) << 16;
+                            sub.code = (uint16_t)(SUBC_CNOT + 4 * (c + 1) + lbit(so.t));
                         } else {
-                            sub.type = SUB_DIAG;
+                            sub.code = SUBC_DIAG;
                         }
                         subs[i].push_back(sub);
                     }
@@ -983,84 +1139,74 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                 b.resize(rec_at + sizeof(StvDiag));
                 encode_diag(b, rec_at, ps.ops[i].form, loc, hd.S);
             }
-            // group records: diag sub-op forms, then the sub-op arrays
-            int ntab = 0;
+            // group records: diag tables (static phases + per-tile terms), sub-op arrays
+            std::vector<StvDTab> tabs;
+            std::vector<StvGroup> grecs(ps.ops.size());
+            uint32_t ent = 0;
             for (size_t i = 0; i < ps.ops.size(); ++i) {
                 const FOp &o = ps.ops[i];
                 if (o.type != OP_GROUP) continue;
                 const std::vector<int> &pos = gpos[i];
+                std::vector<StvSub> out;
+                size_t di = 0;
                 for (size_t k = 0; k < o.subs.size(); ++k) {
                     const FOp &so = o.subs[k];
-                    if (so.type != OP_DIAG) continue;
-                    align(b, 16);
-                    subs[i][k].gdiag_off = (uint32_t)(b.size() - at);
-                    subs[i][k].tbl = ntab++;
-                    StvGDiag gd;
-                    std::memset(&gd, 0, sizeof(gd));
-                    gd.cst = so.form.cst;
-                    std::vector<StvTerm> cross, olin, oquad, vlin, vquad, vcross, vout;
-                    // qubit class: local bit j (on a group position), outside the tile (-1),
-                    // or an in-tile V-bit (-2 - tile position)
-                    auto cls = [&](int phys) -> int {
-                        if (loc[phys] < 0) return -1;
-                        auto it = std::find(pos.begin(), pos.end(), loc[phys]);
-                        if (it != pos.end()) return (int)(it - pos.begin());
-                        return -2 - loc[phys];
-                    };
-                    for (auto &kv : so.form.lin) {
-                        int c = cls(kv.first);
-                        if (c >= 0) gd.w[c] += kv.second;
-                        else if (c == -1) olin.push_back({kv.first, -1, kv.second});
-                        else vlin.push_back({-2 - c, -1, kv.second});
+                    if (so.type != OP_DIAG) { out.push_back(subs[i][k]); continue; }
+                    (void)di;
+                    for (const GroupTable &gt : split_group_diag(so.form, pos, loc)) {
+                        StvDTab d;
+                        std::memset(&d, 0, sizeof(d));
+                        d.m = (int)gt.vpos.size();
+                        for (int v = 0; v < d.m; ++v) d.vraw[v] = (uint16_t)(1u << gt.vpos[v]);
+                        d.nterm = (int)gt.terms.size();
+                        align(b, 16);
+                        d.stat_off = (uint32_t)(b.size() - at);
+                        put(b, gt.stat.data(), gt.stat.size() * sizeof(uint64_t));
+                        align(b, 16);
+                        d.term_off = (uint32_t)(b.size() - at);
+                        put(b, gt.terms.data(), gt.terms.size() * sizeof(StvTerm));
+                        d.ent_off = ent;
+                        ent += (uint32_t)(STV_TAB_STRIDE << d.m);
+                        StvSub sub;
+                        std::memset(&sub, 0, sizeof(sub));
+                        sub.code = SUBC_DIAG;
+                        sub.arg = (uint16_t)tabs.size();
+                        tabs.push_back(d);
+                        out.push_back(sub);
                     }
-                    for (auto &kv : so.form.quad) {
-                        int x = kv.first.first, y = kv.first.second;
-                        int cx = cls(x), cy = cls(y);
-                        if (cx < 0 && cy >= 0) { std::swap(cx, cy); std::swap(x, y); }      // local first
-                        if (cx == -1 && cy <= -2) { std::swap(cx, cy); std::swap(x, y); }   // V before outside
-                        if (cx >= 0 && cy >= 0) { gd.A[cx][cy] += kv.second; gd.A[cy][cx] += kv.second; }
-                        else if (cx >= 0 && cy == -1) cross.push_back({cx, y, kv.second});
-                        else if (cx >= 0) vcross.push_back({cx, -2 - cy, kv.second});
-                        else if (cx == -1 && cy == -1) oquad.push_back({x, y, kv.second});
-                        else if (cy <= -2) vquad.push_back({-2 - cx, -2 - cy, kv.second});
-                        else vout.push_back({-2 - cx, y, kv.second});
-                    }
-                    gd.n_cross = (int)cross.size();
-                    gd.n_olin = (int)olin.size();
-                    gd.n_oquad = (int)oquad.size();
-                    gd.n_vlin = (int)vlin.size();
-                    gd.n_vquad = (int)vquad.size();
-                    gd.n_vcross = (int)vcross.size();
-                    gd.n_vout = (int)vout.size();
-                    gd.n_v = gd.n_vlin + gd.n_vquad + gd.n_vcross + gd.n_vout;
-                    size_t off = sizeof(StvGDiag);
-                    gd.cross_off = (uint32_t)off; off += cross.size() * sizeof(StvTerm);
-                    gd.olin_off = (uint32_t)off; off += olin.size() * sizeof(StvTerm);
-                    gd.oquad_off = (uint32_t)off; off += oquad.size() * sizeof(StvTerm);
-                    gd.vlin_off = (uint32_t)off; off += vlin.size() * sizeof(StvTerm);
-                    gd.vquad_off = (uint32_t)off; off += vquad.size() * sizeof(StvTerm);
-                    gd.vcross_off = (uint32_t)off; off += vcross.size() * sizeof(StvTerm);
-                    gd.vout_off = (uint32_t)off;
-                    put(b, &gd, sizeof(gd));
-                    for (auto *v : {&cross, &olin, &oquad, &vlin, &vquad, &vcross, &vout})
-                        put(b, v->data(), v->size() * sizeof(StvTerm));
+                }
+                subs[i] = out;
+                StvGroup &g = grecs[i];
+                std::memset(&g, 0, sizeof(g));
+                for (int j = 0; j < 4; ++j) g.tpos[j] = pos[j];
+                g.nvb = hd.S - STV_GROUP_BITS;
+                g.pair16 = (!c128 && pos[0] == 0) ? 1 : 0;
+                const std::vector<int> vp = vector_bit_order(pos, hd.S, c128);
+                for (int v = 0; v < g.nvb; ++v) {
+                    g.vraw[v] = (uint16_t)(1u << vp[v]);
+                    g.vsw[v] = (uint16_t)swz_amp(1u << vp[v], c128);
+                }
+                for (int l = 0; l < 16; ++l) {
+                    uint32_t off = 0;
+                    for (int j = 0; j < 4; ++j)
+                        if ((l >> j) & 1) off |= 1u << pos[j];
+                    g.sw_off[l] = (uint16_t)swz_amp(off, c128);
                 }
                 align(b, 16);
-                recs[i].nsub = (int)subs[i].size();
-                recs[i].sub_off = (uint32_t)(b.size() - at);
+                g.nsub = (int)subs[i].size();
+                g.sub_off = (uint32_t)(b.size() - at);
+                recs[i].nsub = g.nsub;
+                recs[i].sub_off = g.sub_off;
                 put(b, subs[i].data(), subs[i].size() * sizeof(StvSub));
             }
-            hd.ntab = ntab;
-            {   // table index -> StvGDiag offset
-                std::vector<uint32_t> toff(ntab, 0);
-                for (size_t i = 0; i < ps.ops.size(); ++i)
-                    for (auto &sub : subs[i])
-                        if (sub.type == SUB_DIAG) toff[sub.tbl] = sub.gdiag_off;
-                align(b, 16);
-                hd.tab_off = (uint32_t)(b.size() - at);
-                put(b, toff.data(), toff.size() * sizeof(uint32_t));
-            }
-            std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
+            hd.ntab = (int)tabs.size();
+            hd.tab_entries = ent;
+            align(b, 16);
+            hd.tab_off = (uint32_t)(b.size() - at);
+            put(b, tabs.data(), tabs.size() * sizeof(StvDTab));
+            hd.grouped = grouped ? 1 : 0;
+            if (grouped) std::memcpy(&b[ops_at], grecs.data(), grecs.size() * sizeof(StvGroup));
+            else std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
             (void)esz;
         } else if (ps.kind == PASS_DIAG) {
             int S = std::min(n_local, 12);

@@ -33,16 +33,18 @@ class Op(ct.Structure):
 
 
 class Sub(ct.Structure):
-    _fields_ = [("type", ct.c_int32), ("a", ct.c_int32), ("b", ct.c_int32), ("c_tile", ct.c_int32),
-                ("c_phys", ct.c_int32), ("mat_off", ct.c_uint32), ("gdiag_off", ct.c_uint32), ("tbl", ct.c_int32)]
+    _fields_ = [("code", ct.c_uint16), ("arg", ct.c_uint16), ("ctl", ct.c_uint32)]
 
 
-class GDiag(ct.Structure):
-    _fields_ = [("cst", ct.c_uint64), ("w", ct.c_uint64 * 4), ("A", (ct.c_uint64 * 4) * 4),
-                ("n_cross", ct.c_int32), ("n_olin", ct.c_int32), ("n_oquad", ct.c_int32), ("n_v", ct.c_int32),
-                ("cross_off", ct.c_uint32), ("olin_off", ct.c_uint32), ("oquad_off", ct.c_uint32), ("pad2", ct.c_uint32),
-                ("n_vlin", ct.c_int32), ("n_vquad", ct.c_int32), ("n_vcross", ct.c_int32), ("n_vout", ct.c_int32),
-                ("vlin_off", ct.c_uint32), ("vquad_off", ct.c_uint32), ("vcross_off", ct.c_uint32), ("vout_off", ct.c_uint32)]
+class Group(ct.Structure):
+    _fields_ = [("nsub", ct.c_int32), ("sub_off", ct.c_uint32), ("nvb", ct.c_int32), ("pair16", ct.c_int32),
+                ("tpos", ct.c_int32 * 4), ("sw_off", ct.c_uint16 * 16), ("vsw", ct.c_uint16 * (MAXT - 4)),
+                ("vraw", ct.c_uint16 * (MAXT - 4)), ("pad", ct.c_uint8 * 8)]
+
+
+class DTab(ct.Structure):
+    _fields_ = [("stat_off", ct.c_uint32), ("term_off", ct.c_uint32), ("nterm", ct.c_int32), ("m", ct.c_int32),
+                ("ent_off", ct.c_uint32), ("vraw", ct.c_uint16 * 3), ("pad", ct.c_uint16), ("pad2", ct.c_uint32)]
 
 
 class Pass(ct.Structure):
@@ -50,10 +52,14 @@ class Pass(ct.Structure):
                 ("hpos", ct.c_int32 * MAXT), ("out_mask", ct.c_uint64), ("rank_bits", ct.c_uint64),
                 ("n_local", ct.c_int32), ("nops", ct.c_int32), ("ops_off", ct.c_uint32), ("mat_off", ct.c_uint32),
                 ("mat_bytes", ct.c_uint32), ("cnot_c", ct.c_int32), ("cnot_t", ct.c_int32), ("diag_off", ct.c_uint32),
-                ("rec_bytes", ct.c_uint32), ("ntab", ct.c_int32), ("tab_off", ct.c_uint32), ("pad2", ct.c_int32 * 3)]
+                ("rec_bytes", ct.c_uint32), ("ntab", ct.c_int32), ("tab_off", ct.c_uint32), ("grouped", ct.c_int32),
+                ("tab_entries", ct.c_uint32), ("pad2", ct.c_int32)]
 
 
-assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 32 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
+assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 8 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
+assert ct.sizeof(Group) == 112 and ct.sizeof(DTab) == 32
+
+U2_PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
 
 
 def _at(blob, cls, off):
@@ -82,6 +88,16 @@ def _matrix(blob, off, D, c128):
     return (a[0::2] + 1j * a[1::2]).reshape(D, D)
 
 
+def _matrix_packed(blob, off, D, c128):
+    """Group sub-op matrix: complex128 interleaved; complex64 re[D*D] then (-im, im) pairs."""
+    if c128:
+        return _matrix(blob, off, D, True)
+    re = np.frombuffer(blob, dtype=np.float32, count=D * D, offset=off).astype(np.float64)
+    pr = np.frombuffer(blob, dtype=np.float32, count=2 * D * D, offset=off + 4 * D * D).astype(np.float64)
+    assert np.all(pr[0::2] == -pr[1::2])
+    return (re + 1j * pr[1::2]).reshape(D, D)
+
+
 def run(n, blob, offs, x0=0, c128=False):
     psi = np.zeros(1 << n, dtype=np.complex128)
     psi[x0] = 1
@@ -96,11 +112,15 @@ def run(n, blob, offs, x0=0, c128=False):
         pos2phys = [i for i in range(P.L)] + [P.hpos[r] for r in range(P.h)]
         if P.kind == 2:
             ops = [("diag", P.diag_off)]
+        elif P.grouped:
+            ops = [("group", _at(blob, Group, po + P.ops_off + ct.sizeof(Group) * i)) for i in range(P.nops)]
         else:
             ops = [("op", _at(blob, Op, po + P.ops_off + 64 * i)) for i in range(P.nops)]
         with np.errstate(over="ignore"):
             for kind, op in ops:
-                if kind == "diag" or op.type == 2:
+                if kind == "group":
+                    psi = _run_group(psi, n, blob, po, P, op, pos2phys, c128, j)
+                elif kind == "diag" or op.type == 2:
                     doff = po + (op if kind == "diag" else op.diag_off)
                     D = _at(blob, Diag, doff)
                     ph = np.full(1 << n, np.uint64(D.cst), dtype=np.uint64)
@@ -122,52 +142,57 @@ def run(n, blob, offs, x0=0, c128=False):
                 elif op.type == 3:
                     c = pos2phys[op.c_loc] if op.c_loc >= 0 else op.c_phys
                     psi = PI._cnot(psi, n, c, pos2phys[op.t_loc])
-                elif op.type == 4:
-                    G = [pos2phys[op.tpos[i]] for i in range(4)]
-                    for k in range(op.nsub):
-                        sb = _at(blob, Sub, po + op.sub_off + 32 * k)
-                        if sb.type == 1:
-                            psi = PI._apply_dense(psi, n, [G[sb.a]], _matrix(blob, po + P.mat_off + sb.mat_off, 2, c128))
-                        elif sb.type == 2:
-                            psi = PI._apply_dense(psi, n, [G[sb.a], G[sb.b]],
-                                                  _matrix(blob, po + P.mat_off + sb.mat_off, 4, c128))
-                        elif sb.type == 3:
-                            goff = po + sb.gdiag_off
-                            gd = _at(blob, GDiag, goff)
-                            ph = np.full(1 << n, np.uint64(gd.cst), dtype=np.uint64)
-                            for t in _terms(blob, goff + gd.olin_off, gd.n_olin):
-                                ph += _bits(j, t.a) * np.uint64(t.ang)
-                            for t in _terms(blob, goff + gd.oquad_off, gd.n_oquad):
-                                ph += _bits(j, t.a) * _bits(j, t.b) * np.uint64(t.ang)
-                            for q in range(4):
-                                ph += _bits(j, G[q]) * np.uint64(gd.w[q])
-                                for r in range(q + 1, 4):
-                                    ph += _bits(j, G[q]) * _bits(j, G[r]) * np.uint64(gd.A[q][r])
-                            for t in _terms(blob, goff + gd.cross_off, gd.n_cross):
-                                ph += _bits(j, G[t.a]) * _bits(j, t.b) * np.uint64(t.ang)
-                            tpos = [op.tpos[i] for i in range(4)]
-                            for t in _terms(blob, goff + gd.vlin_off, gd.n_vlin):
-                                assert t.a not in tpos
-                                ph += _bits(j, pos2phys[t.a]) * np.uint64(t.ang)
-                            for t in _terms(blob, goff + gd.vquad_off, gd.n_vquad):
-                                ph += _bits(j, pos2phys[t.a]) * _bits(j, pos2phys[t.b]) * np.uint64(t.ang)
-                            for t in _terms(blob, goff + gd.vcross_off, gd.n_vcross):
-                                assert t.b not in tpos
-                                ph += _bits(j, G[t.a]) * _bits(j, pos2phys[t.b]) * np.uint64(t.ang)
-                            for t in _terms(blob, goff + gd.vout_off, gd.n_vout):
-                                ph += _bits(j, pos2phys[t.a]) * _bits(j, t.b) * np.uint64(t.ang)
-                            psi = _phase_apply(psi, ph)
-                        else:
-                            if sb.a >= 0:
-                                psi = PI._cnot(psi, n, G[sb.a], G[sb.b])
-                            elif sb.c_tile >= 0:
-                                # the kernel reads this control from the vector base: it must not
-                                # be one of the group's positions (else it varies in the vector)
-                                assert sb.c_tile not in [op.tpos[i] for i in range(4)]
-                                psi = PI._cnot(psi, n, pos2phys[sb.c_tile], G[sb.b])
-                            elif sb.c_phys >= 0:
-                                psi = PI._cnot(psi, n, sb.c_phys, G[sb.b])
-                            else:
-                                t = G[sb.b]
-                                psi = psi[np.arange(1 << n) ^ (1 << t)]
+    return psi
+
+
+def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
+    """Apply one encoded gate group: local bit k <-> tile position tpos[k]."""
+    G = [pos2phys[g.tpos[i]] for i in range(4)]
+    assert len(set(g.sw_off[l] for l in range(16))) == 16
+    for k in range(g.nsub):
+        sb = _at(blob, Sub, po + g.sub_off + 8 * k)
+        c = sb.code
+        ctl_raw, ctl_phys = sb.ctl & 0xFFFF, (sb.ctl >> 16) - 1
+        if c < 4:
+            psi = PI._apply_dense(psi, n, [G[c]], _matrix_packed(blob, po + P.mat_off + 16 * sb.arg, 2, c128))
+        elif c < 10:
+            a, b = U2_PAIRS[c - 4]
+            psi = PI._apply_dense(psi, n, [G[a], G[b]], _matrix_packed(blob, po + P.mat_off + 16 * sb.arg, 4, c128))
+        elif 10 <= c < 30:
+            cl, t = (c - 10) // 4 - 1, (c - 10) % 4
+            ctl = []
+            if cl >= 0:
+                ctl.append(G[cl])
+            if ctl_raw:
+                q = ctl_raw.bit_length() - 1
+                assert q not in [g.tpos[i] for i in range(4)]   # must be fixed within the vector
+                ctl.append(pos2phys[q])
+            if ctl_phys >= 0:
+                ctl.append(ctl_phys)
+            assert len(ctl) <= 1
+            if ctl:
+                psi = PI._cnot(psi, n, ctl[0], G[t])
+            else:
+                psi = psi[np.arange(1 << n) ^ (1 << G[t])]
+        else:
+            assert c == 30
+            d = _at(blob, DTab, po + P.tab_off + ct.sizeof(DTab) * sb.arg)
+            vq = [d.vraw[i].bit_length() - 1 for i in range(d.m)]
+            assert all(q not in [g.tpos[i] for i in range(4)] for q in vq)
+            assert all(d.vraw[i] == 0 for i in range(d.m, 3))
+            stat = np.frombuffer(blob, dtype=np.uint64, count=16 << d.m, offset=po + d.stat_off)
+            e = np.zeros(1 << n, dtype=np.uint64)
+            for k2 in range(4):
+                e |= _bits(j, G[k2]) << np.uint64(k2)
+            for i, q in enumerate(vq):
+                e |= _bits(j, pos2phys[q]) << np.uint64(4 + i)
+            ph = stat[e.astype(np.int64)].copy()
+            for t in _terms(blob, po + d.term_off, d.nterm):
+                on = _bits(j, t.b)
+                if t.a >= 0:
+                    on = on * ((e >> np.uint64(t.a)) & np.uint64(1))
+                elif t.a <= -2:
+                    on = on * _bits(j, -2 - t.a)
+                ph += on * np.uint64(t.ang)
+            psi = _phase_apply(psi, ph)
     return psi

@@ -211,3 +211,85 @@ def test_encoded_blob_semantics(case, dtype):
     ref = oracle.run(circ)
     tol = 2e-6 if dtype == "c64" else 1e-11
     assert np.max(np.abs(psi - ref)) < tol
+
+
+def _swz_slot(chunk):
+    """Shared-memory slot of a 16-B tile chunk (pass_format.h, restated)."""
+    H = [3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7]
+    h, x, j = 0, chunk >> 3, 0
+    while x:
+        if x & 1:
+            h ^= H[j]
+        x >>= 1
+        j += 1
+    return chunk ^ h
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("case", ["c2", "qft", "tile9"])
+def test_group_layout_bijective_and_conflict_free(case, dtype):
+    """Every group's (vector, local index) -> shared-memory address map is the
+    swizzle of the raw tile index, a bijection of the tile; every warp phase of
+    the group gathers (8 lanes x 16 B, or 16 lanes x 8 B) hits distinct banks."""
+    if case == "c2":
+        circ, kw = C.config(2), {}
+    elif case == "qft":
+        circ, kw = C.qft_circuit(20, tail=100, seed=9), {}
+    else:
+        circ, kw = C.random_circuit(14, 200, 3), dict(tile_bits=9, low_bits=3)
+    blob, offs = stv.plan_blob(circ.n, circ.gates, dtype=dtype, **kw)
+    c128 = dtype == "c128"
+    esz = 16 if c128 else 8
+    ngroups = 0
+    for po in offs:
+        P = BE._at(blob, BE.Pass, po)
+        if P.kind != 1 or not P.grouped:
+            continue
+        for gi in range(P.nops):
+            g = BE._at(blob, BE.Group, po + P.ops_off + 112 * gi)
+            ngroups += 1
+            assert g.nvb == P.S - 4
+            assert bool(g.pair16) == (not c128 and g.tpos[0] == 0)
+
+            def raw_index(v, l):
+                i = 0
+                for b in range(g.nvb):
+                    if (v >> b) & 1:
+                        i |= g.vraw[b]
+                for k in range(4):
+                    if (l >> k) & 1:
+                        i |= 1 << g.tpos[k]
+                return i
+
+            def addr(v, l):
+                s = 0
+                for b in range(g.nvb):
+                    if (v >> b) & 1:
+                        s ^= g.vsw[b]
+                return s ^ g.sw_off[l]
+
+            seen = set()
+            for v in range(1 << g.nvb):
+                for l in range(16):
+                    i, a = raw_index(v, l), addr(v, l)
+                    ci = i >> (0 if c128 else 1)
+                    exp = _swz_slot(ci) if c128 else (_swz_slot(ci) << 1) | (i & 1)
+                    assert a == exp
+                    seen.add(a)
+            assert len(seen) == 1 << P.S
+            # bank-conflict freedom of one access instruction (fixed l, lanes vary v)
+            vec16 = c128 or g.pair16
+            lanes = 8 if vec16 else 16
+            # banks reachable at all by the vector bits (small tiles may not span)
+            reach = {((addr(v, 0) * esz) // (16 if vec16 else 8)) % (8 if vec16 else 16)
+                     for v in range(1 << g.nvb)}
+            want = min(lanes, len(reach))
+            for l in (range(0, 16, 2) if (g.pair16 and not c128) else range(16)):
+                for v0 in range(0, min(1 << g.nvb, 256), lanes):
+                    banks = set()
+                    for v in range(v0, min(v0 + lanes, 1 << g.nvb)):
+                        byte = addr(v, l) * esz
+                        banks.add((byte // (16 if vec16 else 8)) % (8 if vec16 else 16))
+                    assert len(banks) == min(want, v0 + lanes if v0 + lanes <= (1 << g.nvb) else (1 << g.nvb) - v0), \
+                        (case, gi, l, v0)
+    assert ngroups > 0

@@ -26,8 +26,9 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
                              uint32_t rec_bytes, int ntab, cudaStream_t st, int *kernels);
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
                              cudaStream_t st, int *kernels);
-cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
-                              uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st, int *kernels);
+cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off,
+                              int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st,
+                              int *kernels);
 cudaError_t launch_cnot(bool c128, void *state, int c, int t, int n_local, cudaStream_t st, int *kernels);
 cudaError_t launch_bitswap(bool c128, void *state, int a, int b, int n_bits, cudaStream_t st, int *kernels);
 cudaError_t launch_norm(bool c128, const void *state, uint64_t N, double *part, int np, double *out, cudaStream_t st,
@@ -363,8 +364,8 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
         if (ps.kind == PASS_TILE) {
             kind = hp->h == 0 ? 1 : 2;
             if (hp->grouped)
-                e = launch_group_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->rec_bytes,
-                                      hp->tab_entries, s->stream, &kernels);
+                e = launch_group_pass(s->c128(), s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
+                                      enc_local, hp->rec_bytes, hp->tab_entries, s->stream, &kernels);
             else
                 e = launch_tile_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->rec_bytes,
                                      hp->ntab, s->stream, &kernels);

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <cstring>
 
 #include "pass_format.h"
 
@@ -751,16 +752,24 @@ template <typename C> struct TabEnt;
 template <> struct TabEnt<float2> { using T = float4; };
 template <> struct TabEnt<double2> { using T = double2; };
 
+// The pass record of a group pass travels as a __grid_constant__ kernel
+// parameter: every field, sub-op and matrix is read with uniform constant-bank
+// loads (LDCU) into uniform registers, FFMA2 takes the matrix entries straight
+// from them, and sub-op dispatch is a uniform branch.  Only the per-lane static
+// phase tables are read from the device copy of the blob (global, L1-cached).
+struct __align__(16) RecParam {
+    uint8_t b[STV_REC_PARAM_BYTES];
+};
+
 template <typename C, int NT>
-__device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, uint64_t fb,
-                                             typename TabEnt<C>::T *__restrict__ tables,
-                                             int ctid) {
+__device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, const uint8_t *__restrict__ grec,
+                                             uint64_t fb, typename TabEnt<C>::T *__restrict__ tables, int ctid) {
     const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
     const int ntab = P->ntab;
     const int lane = ctid & 31;
     for (int t = ctid >> 5; t < ntab; t += NT / 32) {
         const StvDTab &d = tabs[t];
-        const uint64_t *stat = (const uint64_t *)((const uint8_t *)P + d.stat_off);
+        const uint64_t *stat = (const uint64_t *)(grec + d.stat_off);
         const StvTerm *tm = (const StvTerm *)((const uint8_t *)P + d.term_off);
         const int ne = 16 << d.m, nterm = d.nterm;
         // per-tile coefficients: lane b < 4 + m sums the terms on index bit b, lane 31 the constant
@@ -777,7 +786,7 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, uint
 #pragma unroll
         for (int b = 0; b < 7; ++b) lb[b] = __shfl_sync(0xffffffffu, lam, b);
         for (int e = lane; e < ne; e += 32) {
-            uint64_t ph = stat[e] + cst;
+            uint64_t ph = __ldg(stat + e) + cst;
 #pragma unroll
             for (int b = 0; b < 7; ++b)
                 if ((e >> b) & 1) ph += lb[b];
@@ -790,8 +799,8 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, uint
     }
 }
 
-// Run a group's sub-op program on NV register vectors (same program, the
-// matrices are loaded once per sub-op and shared by the vectors).
+// Run a group's sub-op program on NV register vectors (same program; matrix
+// entries come from uniform registers).
 template <typename C, int NV>
 __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[NV], const StvSub *__restrict__ subs,
                                          int nsub, const uint8_t *__restrict__ mat, const StvDTab *__restrict__ tabs,
@@ -801,19 +810,9 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
         const StvSub sb = subs[k];
         const C *M = (const C *)(mat + ((uint32_t)sb.arg << 4));
         const float *MR = (const float *)M;
-        switch (sb.code) {
-#define STV_U1(a)                                                                           \
-    case SUBC_U1 + (a): {                                                                   \
-        if constexpr (kPacked) {                                                            \
-            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
-                g_u1p<(a)>(*(float2(*)[16]) & x[i], MR, (const float2 *)(MR + 4));         \
-        } else {                                                                            \
-            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u1<(a)>(x[i], M);               \
-        }                                                                                   \
-        break;                                                                              \
-    }
-            STV_U1(0) STV_U1(1) STV_U1(2) STV_U1(3)
-#undef STV_U1
+        const int code = sb.code;
+        if (code >= SUBC_U2 && code < SUBC_U2 + 6) {        // the common case first
+            switch (code) {
 #define STV_U2(p, a, b)                                                                     \
     case SUBC_U2 + (p): {                                                                   \
         if constexpr (kPacked) {                                                            \
@@ -830,29 +829,17 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
         }                                                                                   \
         break;                                                                              \
     }
-            STV_U2(0, 0, 1) STV_U2(1, 0, 2) STV_U2(2, 0, 3) STV_U2(3, 1, 2) STV_U2(4, 1, 3) STV_U2(5, 2, 3)
+                STV_U2(0, 0, 1) STV_U2(1, 0, 2) STV_U2(2, 0, 3) STV_U2(3, 1, 2) STV_U2(4, 1, 3) STV_U2(5, 2, 3)
 #undef STV_U2
-#define STV_CX(c, t)                                                                             \
-    case SUBC_CNOT + 4 * ((c) + 1) + (t): {                                                      \
-        const uint32_t raw = sb.ctl & 0xffffu, ph = sb.ctl >> 16;                                \
-        const bool pon = ph == 0 || ((full_base >> (ph - 1)) & 1);                               \
-        _Pragma("unroll") for (int i = 0; i < NV; ++i)                                           \
-            g_cnot<(c), (t)>(x[i], pon && (raw == 0 || (braw[i] & raw) != 0));                   \
-        break;                                                                                   \
-    }
-            STV_CX(-1, 0) STV_CX(-1, 1) STV_CX(-1, 2) STV_CX(-1, 3)
-            STV_CX(0, 1) STV_CX(0, 2) STV_CX(0, 3)
-            STV_CX(1, 0) STV_CX(1, 2) STV_CX(1, 3)
-            STV_CX(2, 0) STV_CX(2, 1) STV_CX(2, 3)
-            STV_CX(3, 0) STV_CX(3, 1) STV_CX(3, 2)
-#undef STV_CX
-        case SUBC_DIAG: {   // per-tile table row of each vector's V-bits
+            }
+        } else if (code == SUBC_DIAG) {   // per-tile table row of each vector's V-bits
             const StvDTab &d = tabs[sb.arg];
             const uint32_t v0 = d.vraw[0], v1 = d.vraw[1], v2 = d.vraw[2];
+            const uint32_t eo = d.ent_off;
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
                 const uint32_t r = ((braw[i] & v0) ? 1u : 0u) | ((braw[i] & v1) ? 2u : 0u) | ((braw[i] & v2) ? 4u : 0u);
-                const typename TabEnt<C>::T *row = tables + d.ent_off + r * STV_TAB_STRIDE;
+                const typename TabEnt<C>::T *row = tables + eo + r * STV_TAB_STRIDE;
                 if constexpr (kPacked) {
                     float2(&xv)[16] = *(float2(*)[16]) & x[i];
 #pragma unroll
@@ -865,9 +852,36 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
                     for (int l = 0; l < 16; ++l) x[i][l] = cmul(x[i][l], row[l]);
                 }
             }
-            break;
-        }
-        default: break;
+        } else {
+            switch (code) {
+#define STV_U1(a)                                                                           \
+    case SUBC_U1 + (a): {                                                                   \
+        if constexpr (kPacked) {                                                            \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
+                g_u1p<(a)>(*(float2(*)[16]) & x[i], MR, (const float2 *)(MR + 4));         \
+        } else {                                                                            \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u1<(a)>(x[i], M);               \
+        }                                                                                   \
+        break;                                                                              \
+    }
+                STV_U1(0) STV_U1(1) STV_U1(2) STV_U1(3)
+#undef STV_U1
+#define STV_CX(c, t)                                                                             \
+    case SUBC_CNOT + 4 * ((c) + 1) + (t): {                                                      \
+        const uint32_t raw = sb.ctl & 0xffffu, ph = sb.ctl >> 16;                                \
+        const bool pon = ph == 0 || ((full_base >> (ph - 1)) & 1);                               \
+        _Pragma("unroll") for (int i = 0; i < NV; ++i)                                           \
+            g_cnot<(c), (t)>(x[i], pon && (raw == 0 || (braw[i] & raw) != 0));                   \
+        break;                                                                                   \
+    }
+                STV_CX(-1, 0) STV_CX(-1, 1) STV_CX(-1, 2) STV_CX(-1, 3)
+                STV_CX(0, 1) STV_CX(0, 2) STV_CX(0, 3)
+                STV_CX(1, 0) STV_CX(1, 2) STV_CX(1, 3)
+                STV_CX(2, 0) STV_CX(2, 1) STV_CX(2, 3)
+                STV_CX(3, 0) STV_CX(3, 1) STV_CX(3, 2)
+#undef STV_CX
+            default: break;
+            }
         }
     }
 }
@@ -889,15 +903,8 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
             bsw0 ^= g.vsw[b];
         }
     uint32_t so[16];
-    {
-        const uint4 s0 = *(const uint4 *)&g.sw_off[0], s1 = *(const uint4 *)&g.sw_off[8];
-        const uint32_t w[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            so[2 * k] = w[k] & 0xffffu;
-            so[2 * k + 1] = w[k] >> 16;
-        }
-    }
+    for (int l = 0; l < 16; ++l) so[l] = g.sw_off[l];
     const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off);
     const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
     const int nsub = g.nsub;
@@ -917,7 +924,7 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
                 }
         }
         C x[NV][16];
-        const bool live1 = NV == 1 || v0 + NT < nvec;   // tiny tiles: second vector may not exist
+        const bool live1 = NV == 1 || v0 + NT < nvec;   // tiny tiles: the second vector may not exist
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             if (i > 0 && !live1) {
@@ -952,41 +959,94 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
     }
 }
 
-constexpr int kGThreads = 128;     // group pass CTA: 4 warps, 2 vectors per thread (complex64)
 constexpr int kGStages = 2;        // double-buffered tiles (prefetch distance 1)
 
-template <typename R, int NV>
-__global__ void __launch_bounds__(kGThreads, sizeof(R) == 4 ? 3 : 2)
+// Tile copy state that does not change from tile to tile (computed once per CTA).
+struct CopyPlan {
+    uint64_t roff0, dstep, d1;
+    uint32_t cpr, total, within;
+    bool long_runs;
+};
+
+template <int NT>
+__device__ __forceinline__ CopyPlan make_copy_plan(uint64_t hmask, uint32_t run_bytes, uint32_t nruns, int t) {
+    CopyPlan c;
+    c.cpr = run_bytes >> 4;
+    c.long_runs = c.cpr >= (uint32_t)NT;
+    c.d1 = hmask & (0 - hmask);
+    c.total = nruns * c.cpr;
+    const uint32_t lc = 31 - __clz(c.cpr);
+    c.dstep = c.long_runs ? 0 : pdep64((uint32_t)NT >> lc, hmask);
+    c.roff0 = c.long_runs ? 0 : pdep64((uint32_t)t >> lc, hmask);
+    c.within = c.long_runs ? 0 : ((uint32_t)t & (c.cpr - 1)) * 16;
+    return c;
+}
+
+// Swizzled tile copy (see tile_copy_swz) with per-CTA precomputed addressing;
+// hk[k] = H((NT * k) >> 3) for the k-th chunk of this thread.
+template <bool kLoad, int NT>
+__device__ __forceinline__ void tile_copy_fast(uint8_t *gstate, uint8_t *stile, uint64_t base, uint64_t hmask,
+                                               const CopyPlan &cp, uint32_t nruns, uint32_t esz, int t,
+                                               uint32_t hash_t, const uint8_t *hk) {
+    if (cp.long_runs) {
+        uint64_t roff = 0;
+        for (uint32_t r = 0; r < nruns; ++r) {
+            uint8_t *g = gstate + (base | roff) * esz;
+            for (uint32_t w = t; w < cp.cpr; w += NT) {
+                const uint32_t c = r * cp.cpr + w;
+                const uint32_t slot = c ^ hash_t ^ hk[(c - (uint32_t)t) / NT];
+                uint8_t *sm = stile + (size_t)slot * 16;
+                if (kLoad) cp_async16(sm, g + (size_t)w * 16);
+                else *(uint4 *)(g + (size_t)w * 16) = *(const uint4 *)sm;
+            }
+            roff = masked_add(roff, cp.d1, hmask);
+        }
+    } else {
+        uint64_t roff = cp.roff0;
+        uint32_t k = 0;
+        for (uint32_t c = t; c < cp.total; c += NT, ++k) {
+            uint8_t *g = gstate + (base | roff) * esz + cp.within;
+            const uint32_t slot = c ^ hash_t ^ hk[k];
+            uint8_t *sm = stile + (size_t)slot * 16;
+            if (kLoad) cp_async16(sm, g);
+            else *(uint4 *)g = *(const uint4 *)sm;
+            roff = masked_add(roff, cp.dstep, hmask);
+        }
+    }
+}
+
+template <typename R, int NT, int NV>
+__global__ void __launch_bounds__(NT, sizeof(R) == 4 ? 3 : 2)
 k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
-             uint32_t ntiles, int dbg_flags) {
+             uint32_t ntiles, int dbg_flags, const __grid_constant__ RecParam rec) {
     using C = typename C2T<R>::T;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const StvPass *G = (const StvPass *)(blob + pass_off);
-    const uint32_t rec_bytes = G->rec_bytes;
-    const uint32_t rec_pad = (rec_bytes + 127u) & ~127u;
-    const StvPass *P = (const StvPass *)smem;
-    for (uint32_t k = threadIdx.x; k < rec_bytes / 16; k += blockDim.x) ((uint4 *)smem)[k] = ((const uint4 *)G)[k];
-    const int S = G->S, L = G->L, h = G->h;
-    const uint64_t out_mask = G->out_mask, rank_bits = G->rank_bits;
-    const int nops = (dbg_flags & 1) ? 0 : G->nops;   // bit 0: data movement only (microbenchmark)
-    const int ntab = G->ntab;
-    const StvGroup *groups = (const StvGroup *)((const uint8_t *)P + G->ops_off);
-    const uint8_t *mat = (const uint8_t *)P + G->mat_off;
+    const StvPass *P = (const StvPass *)rec.b;
+    const uint8_t *grec = blob + pass_off;
+    const int S = P->S, L = P->L, h = P->h;
+    const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
+    const int nops = (dbg_flags & 1) ? 0 : P->nops;   // bit 0: data movement only (microbenchmark)
+    const int ntab = P->ntab;
+    const StvGroup *groups = (const StvGroup *)(rec.b + P->ops_off);
+    const uint8_t *mat = rec.b + P->mat_off;
     const uint32_t esz = sizeof(C);
-    const uint32_t tab_pad = (G->tab_entries * 16u + 127u) & ~127u;       // 16-B table entries
-    typename TabEnt<C>::T *tables = (typename TabEnt<C>::T *)(smem + rec_pad);
-    C *tiles = (C *)(smem + rec_pad + tab_pad);
+    const uint32_t tab_pad = (P->tab_entries * 16u + 127u) & ~127u;       // 16-B table entries
+    uint8_t *hk = smem;                                                    // 1024 B: chunk hashes
+    typename TabEnt<C>::T *tables = (typename TabEnt<C>::T *)(smem + 1024);
+    C *tiles = (C *)(smem + 1024 + tab_pad);
     const uint32_t tile_elems = 1u << S;
     const uint32_t run_bytes = (1u << L) * esz;
     const uint32_t nruns = 1u << h;
     const int tid = threadIdx.x;
     const uint32_t hash_t = swz_hash_d((uint32_t)tid >> 3);
+    for (int k = tid; k < 1024; k += NT) hk[k] = (uint8_t)swz_hash_d(((uint32_t)NT * (uint32_t)k) >> 3);
+    uint64_t hmask = 0;
+    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
+    const CopyPlan cp = make_copy_plan<NT>(hmask, run_bytes, nruns, tid);
     __syncthreads();
 
     const uint32_t first = blockIdx.x, stride = gridDim.x;
     const uint32_t my_tiles = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
-    uint64_t hmask = 0;
-    for (int r = 0; r < h; ++r) hmask |= 1ull << G->hpos[r];
     uint8_t *gstate = (uint8_t *)state;
     const uint64_t tstep = pdep64(stride, out_mask);
     uint64_t load_tb = pdep64(first, out_mask);
@@ -994,7 +1054,7 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
     auto issue = [&](int s) {
         uint8_t *stile = (uint8_t *)(tiles + (size_t)s * tile_elems);
         if (loaded < my_tiles)
-            tile_copy_swz<true, kGThreads>(gstate, stile, load_tb, hmask, run_bytes, nruns, esz, tid, hash_t);
+            tile_copy_fast<true, NT>(gstate, stile, load_tb, hmask, cp, nruns, esz, tid, hash_t, hk);
         cp_async_commit();
         load_tb = masked_add(load_tb, tstep, out_mask);
         ++loaded;
@@ -1009,14 +1069,14 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t full_base = base | rank_bits;
         if (ntab && nops) {
-            build_tables<C, kGThreads>(P, full_base, tables, tid);
+            build_tables<C, NT>(P, grec, full_base, tables, tid);
             __syncthreads();
         }
         for (int o = 0; o < nops; ++o) {
-            group_vec_op<C, kGThreads, NV>(tile, groups[o], P, mat, tables, full_base, tid);
+            group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, tid);
             __syncthreads();
         }
-        tile_copy_swz<false, kGThreads>(gstate, (uint8_t *)tile, base, hmask, run_bytes, nruns, esz, tid, hash_t);
+        tile_copy_fast<false, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
         base = masked_add(base, tstep, out_mask);
     }
     cp_async_wait0();
@@ -1237,41 +1297,41 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
     return e;
 }
 
-cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
-                              uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st, int *kernels) {
-    const size_t esz = c128 ? 16 : 8;
-    const size_t smem = ((rec_bytes + 127u) & ~127u) + (((size_t)tab_entries * 16 + 127u) & ~(size_t)127) +
-                        (size_t)kGStages * (esz << S);
-    const uint64_t ntiles = 1ull << (n_local - S);
-    if (smem > 227 * 1024 || (ntiles >> 32)) return cudaErrorInvalidValue;
-    static const int nv_env = getenv("STV_NV") ? atoi(getenv("STV_NV")) : 2;
-    auto kf = c128 ? (const void *)k_group_pass<double, 1>
-                   : (nv_env == 1 ? (const void *)k_group_pass<float, 1> : (const void *)k_group_pass<float, 2>);
-    static const void *attr_done[3] = {nullptr, nullptr, nullptr};
-    {
-        int slot = c128 ? 0 : (nv_env == 1 ? 1 : 2);
-        if (attr_done[slot] != kf) {
-            cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            attr_done[slot] = kf;
-        }
+template <typename R, int NT, int NV>
+static cudaError_t group_launch(void *state, const uint8_t *dblob, uint32_t pass_off, uint32_t ntiles, size_t smem,
+                                const RecParam &rp, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_group_pass<R, NT, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
     }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, kGThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_pass<R, NT, NV>, NT, smem);
     if (occ < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)num_sms() * occ;
     if (grid > ntiles) grid = ntiles;
     static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
-    if (c128)
-        k_group_pass<double, 1><<<(unsigned)grid, kGThreads, smem, st>>>((double2 *)state, dblob, pass_off,
-                                                                            (uint32_t)ntiles, dbg);
-    else if (nv_env == 1)
-        k_group_pass<float, 1><<<(unsigned)grid, kGThreads, smem, st>>>((float2 *)state, dblob, pass_off,
-                                                                           (uint32_t)ntiles, dbg);
-    else
-        k_group_pass<float, 2><<<(unsigned)grid, kGThreads, smem, st>>>((float2 *)state, dblob, pass_off,
-                                                                           (uint32_t)ntiles, dbg);
-    ++*kernels;
+    k_group_pass<R, NT, NV><<<(unsigned)grid, NT, smem, st>>>((typename C2T<R>::T *)state, dblob, pass_off, ntiles,
+                                                               dbg, rp);
     return cudaGetLastError();
+}
+
+cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off,
+                              int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st,
+                              int *kernels) {
+    const size_t esz = c128 ? 16 : 8;
+    const size_t smem = 1024 + (((size_t)tab_entries * 16 + 127u) & ~(size_t)127) + (size_t)kGStages * (esz << S);
+    const uint64_t ntiles = 1ull << (n_local - S);
+    if (smem > 227 * 1024 || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
+    static thread_local RecParam rp;
+    std::memcpy(rp.b, hrec, rec_bytes);
+    static const int cfg = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
+    cudaError_t e;
+    if (c128) e = group_launch<double, 128, 1>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    else if (cfg == 1) e = group_launch<float, 128, 2>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    else e = group_launch<float, 256, 1>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    ++*kernels;
+    return e;
 }
 
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,

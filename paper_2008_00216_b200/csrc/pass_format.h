@@ -26,6 +26,7 @@
 #define STV_MAX_TILE_BITS 14
 #define STV_MAX_K 4
 #define STV_THREADS 256
+#define STV_REC_PARAM_BYTES 24576   // group-pass record = __grid_constant__ kernel parameter
 #define STV_THREADS_LOG 8
 
 struct alignas(16) StvTerm {

@@ -530,13 +530,14 @@ struct OpsEval {
     bool grouped = false;
     int cost = 0;
     size_t rec = 0;
+    size_t tab = 0;           // shared-memory bytes of the group diag tables
     int ntab = 0;
 };
 
 // Shared-memory bytes (pass record + table area) of a group diagonal sub-op:
 // the greedy split of its terms into tables of <= STV_MAX_VBITS V-bits
 // (vmask = in-tile qubits outside the group; mirrors split_group_diag).
-static size_t diag_table_bytes(const QForm &f, uint64_t vmask, int amp_bytes, int *ntab) {
+static size_t diag_table_bytes(const QForm &f, uint64_t vmask, int amp_bytes, int *ntab, size_t *tab_smem) {
     std::vector<uint64_t> sets;
     auto place = [&](uint64_t need) {
         for (uint64_t &u : sets)
@@ -551,8 +552,10 @@ static size_t diag_table_bytes(const QForm &f, uint64_t vmask, int amp_bytes, in
     size_t bytes = sizeof(StvTerm) * terms;
     for (uint64_t u : sets) {
         const int m = __builtin_popcountll(u);
-        bytes += sizeof(StvDTab) + sizeof(StvSub) + ((size_t)128 << m) + ((size_t)(STV_TAB_STRIDE * 16) << m) + 32;
+        bytes += sizeof(StvDTab) + sizeof(StvSub) + ((size_t)128 << m) + 32;
+        *tab_smem += (size_t)(STV_TAB_STRIDE * 16) << m;
     }
+    (void)amp_bytes;
     *ntab = (int)sets.size();
     return bytes;
 }
@@ -560,6 +563,7 @@ static size_t diag_table_bytes(const QForm &f, uint64_t vmask, int amp_bytes, in
 static void tally(OpsEval &ev, int amp_bytes, uint64_t S = 0) {
     ev.cost = 0;
     ev.rec = sizeof(StvPass);
+    ev.tab = 0;
     ev.ntab = 0;
     for (auto &grp : ev.ops) {
         if (grp.type != OP_GROUP) {
@@ -577,7 +581,7 @@ static void tally(OpsEval &ev, int amp_bytes, uint64_t S = 0) {
             if (o.type == OP_DIAG) {
                 // per-tile tables over the group bits + V-bits, split as the encoder does
                 int ntb = 0;
-                ev.rec += diag_table_bytes(o.form, S & ~grp.T, amp_bytes, &ntb);
+                ev.rec += diag_table_bytes(o.form, S & ~grp.T, amp_bytes, &ntb, &ev.tab);
                 ev.ntab += ntb;
             }
         }
@@ -711,12 +715,13 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
     std::vector<char> done(G, 0);
     size_t first = 0;
     const double amp_pass_bytes = 2.0 * amp_bytes * std::ldexp(1.0, nl);   // R+W per rank
-    // pass record + diag tables share the CTA's shared memory with 3 tile stages:
-    // keep two 256-thread CTAs per SM when the tiles allow it
+    // the group pass record is a kernel parameter (<= STV_REC_PARAM_BYTES); its
+    // diag tables share the CTA's shared memory with 2 tile stages: keep three
+    // CTAs per SM when the tiles allow it
     const size_t tile_b = (size_t)amp_bytes << opt.tile_bits;
-    size_t rec_limit = kMaxRecBytes;
-    if (3 * tile_b <= 96 * 1024) rec_limit = std::min(rec_limit, (size_t)112 * 1024 - 3 * tile_b);
-    else if (3 * tile_b < 224 * 1024) rec_limit = std::min(rec_limit, (size_t)224 * 1024 - 3 * tile_b);
+    const size_t rec_limit = std::min(kMaxRecBytes, (size_t)STV_REC_PARAM_BYTES);
+    size_t tab_limit = 16 * 1024;
+    if (2 * tile_b + 2048 < 74 * 1024) tab_limit = std::max((size_t)4096, 74 * 1024 - 2 * tile_b - 2048);
 
     while (true) {
         while (first < G && done[first]) ++first;
@@ -745,7 +750,8 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                     std::swap(cur, t);
                 }
                 if (pgates.size() > 1 &&
-                    (cur.cost > opt.budget || cur.rec > rec_limit || cur.ntab > STV_MAX_TABLES)) {
+                    (cur.cost > opt.budget || cur.rec > rec_limit || cur.tab > tab_limit ||
+                     cur.ntab > STV_MAX_TABLES)) {
                     ok = false;
                     pgates.pop_back();
                     cur = make_ops(pgates, S, opt, amp_bytes);        // rare: rebuild without g
@@ -838,7 +844,7 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
             for (int b = 0; b < nl && __builtin_popcountll(S) < opt.tile_bits; ++b) S |= 1ull << b;
             if (S != S0) {
                 OpsEval fin = make_ops(pgates, S, opt, amp_bytes);
-                if (fin.rec <= rec_limit && fin.ntab <= STV_MAX_TABLES) pass.ops = fin.ops;
+                if (fin.rec <= rec_limit && fin.tab <= tab_limit && fin.ntab <= STV_MAX_TABLES) pass.ops = fin.ops;
                 else S = S0;
             }
             pass.S = S;

@@ -61,6 +61,65 @@ __global__ void u2_smem(float2 *out, const Mat4 *g, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__device__ __forceinline__ float2 cmac2(float mr, float2 mp, float2 x, float2 acc) {
+    acc = __ffma2_rn(make_float2(mr, mr), x, acc);
+    return __ffma2_rn(mp, make_float2(x.y, x.x), acc);
+}
+__device__ __forceinline__ float2 cmul1(float mr, float2 mp, float2 x) {
+    return __ffma2_rn(mp, make_float2(x.y, x.x), __fmul2_rn(make_float2(mr, mr), x));
+}
+template <int A, int B>
+__device__ __forceinline__ void g_u2p(float2 (&x)[16], const float (&mr)[16], const float2 (&mp)[16]) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & ((1 << A) | (1 << B))) continue;
+        const float2 v[4] = {x[l], x[l | (1 << A)], x[l | (1 << B)], x[l | (1 << A) | (1 << B)]};
+        float2 o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            float2 acc = cmul1(mr[r * 4], mp[r * 4], v[0]);
+#pragma unroll
+            for (int c = 1; c < 4; ++c) acc = cmac2(mr[r * 4 + c], mp[r * 4 + c], v[c], acc);
+            o[r] = acc;
+        }
+        x[l] = o[0];
+        x[l | (1 << A)] = o[1];
+        x[l | (1 << B)] = o[2];
+        x[l | (1 << A) | (1 << B)] = o[3];
+    }
+}
+// packed FFMA2 U2 on NV register vectors, matrices from shared memory
+template <int NV>
+__global__ void u2p_smem(float2 *out, const float *g, int iters) {
+    __shared__ float sm[8 * 48];
+    for (int i = threadIdx.x; i < 8 * 48; i += blockDim.x) sm[i] = g[i % 64] * 0.1f;
+    __syncthreads();
+    float2 x[NV][16];
+    for (int i = 0; i < NV; ++i)
+        for (int l = 0; l < 16; ++l) x[i][l] = make_float2(threadIdx.x * 1e-3f + l + i, l * 0.5f);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const float *M = sm + ((it + s) & 7) * 48;
+            float mr[16];
+            float2 mp[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) { mr[e] = M[e]; mp[e] = ((const float2 *)(M + 16))[e]; }
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                if (s == 0) g_u2p<0, 1>(x[i], mr, mp);
+                if (s == 1) g_u2p<2, 3>(x[i], mr, mp);
+                if (s == 2) g_u2p<0, 2>(x[i], mr, mp);
+                if (s == 3) g_u2p<1, 3>(x[i], mr, mp);
+            }
+        }
+    }
+    float2 s = make_float2(0, 0);
+    for (int i = 0; i < NV; ++i)
+        for (int l = 0; l < 16; ++l) { s.x += x[i][l].x; s.y += x[i][l].y; }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void u2_const(float2 *out, int iters) {
     float2 x[16];
     for (int l = 0; l < 16; ++l) x[l] = make_float2(threadIdx.x * 1e-3f + l, l * 0.5f);
@@ -135,14 +194,14 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int threads : {256, 512}) {
-        for (int ctas_per_sm : {1, 2, 4}) {
+    for (int threads : {128, 256}) {
+        for (int ctas_per_sm : {1, 2, 3, 4}) {
             const int grid = sms * ctas_per_sm;
             if (threads * ctas_per_sm > 2048) continue;
             // U2: 4 sub-ops x 4 quads x 16 cfma x 4 FFMA = 1024 FFMA per iteration per thread
             const double u2_flops = 2.0 * 1024 * iters * (double)grid * threads;
             const double ffma_flops = 2.0 * 8 * 64 * iters * (double)grid * threads;
-            for (int k = 0; k < 5; ++k) {
+            for (int k = 0; k < 7; ++k) {
                 float ms = 0;
                 for (int rep = 0; rep < 2; ++rep) {
                     cudaEventRecord(e0);
@@ -151,12 +210,14 @@ int main() {
                     if (k == 2) u2_param<<<grid, threads>>>(out, P, iters);
                     if (k == 3) ffma_reg<<<grid, threads>>>((float *)out, 1.0001f, 1e-4f, iters);
                     if (k == 4) ffma_imm<<<grid, threads>>>((float *)out, iters);
+                    if (k == 5) u2p_smem<1><<<grid, threads>>>(out, (const float *)dg, iters);
+                    if (k == 6) u2p_smem<2><<<grid, threads>>>(out, (const float *)dg, iters);
                     cudaEventRecord(e1);
                     cudaEventSynchronize(e1);
                     cudaEventElapsedTime(&ms, e0, e1);
                 }
-                const char *nm[] = {"u2_smem", "u2_const", "u2_param", "ffma_reg", "ffma_imm"};
-                const double fl = k < 3 ? u2_flops : ffma_flops;
+                const char *nm[] = {"u2_smem", "u2_const", "u2_param", "ffma_reg", "ffma_imm", "u2p_nv1", "u2p_nv2"};
+                const double fl = k < 3 ? u2_flops : k == 5 ? u2_flops : k == 6 ? 2 * u2_flops : ffma_flops;
                 printf("%-9s threads=%d ctas/sm=%d  %.3f ms  %.1f TFLOP/s  (peak@%d MHz = %.1f)\n", nm[k], threads,
                        ctas_per_sm, ms, fl / ms / 1e9, clk / 1000, sms * 128 * 2.0 * clk * 1e3 / 1e12);
             }

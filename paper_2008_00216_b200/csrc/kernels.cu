@@ -699,35 +699,34 @@ __device__ __forceinline__ void g_cnot(C (&x)[16], bool on) {
     }
 }
 
-// ---- complex64 with packed FP32 (FFMA2, sm_100): a complex multiply-add
-// acc += m x is two FFMA2: acc += m_re * (x_re, x_im) (broadcast operand), then
-// acc += (-m_im, m_im) * (x_im, x_re) (swapped operand).  Matrices are encoded
-// as m_re[D*D] scalars followed by (-m_im, m_im)[D*D] pairs (plan.cpp).
-__device__ __forceinline__ float2 cmac2(float mr, float2 mp, float2 x, float2 acc) {
-    acc = __ffma2_rn(make_float2(mr, mr), x, acc);
-    return __ffma2_rn(mp, make_float2(x.y, x.x), acc);
+// ---- complex64 with packed FP32 (FFMA2, sm_100): with m = (m_re, m_im),
+//   acc += m x  is  acc = FFMA2(x, m_re.bcast, acc); acc = FFMA2(-x.swapped.lo, m_im.bcast, acc)
+// i.e. (x_re, x_im) m_re + (-x_im, x_re) m_im: two instructions, the swap and
+// the one-lane negation are operand modifiers (.LO_HI.NP).
+__device__ __forceinline__ float2 cmac2(float2 m, float2 x, float2 acc) {
+    acc = __ffma2_rn(x, make_float2(m.x, m.x), acc);
+    return __ffma2_rn(make_float2(-x.y, x.x), make_float2(m.y, m.y), acc);
 }
-__device__ __forceinline__ float2 cmul1(float mr, float2 mp, float2 x) {
-    return __ffma2_rn(mp, make_float2(x.y, x.x), __fmul2_rn(make_float2(mr, mr), x));
+__device__ __forceinline__ float2 cmul1(float2 m, float2 x) {
+    return __ffma2_rn(make_float2(-x.y, x.x), make_float2(m.y, m.y), __fmul2_rn(x, make_float2(m.x, m.x)));
 }
 
 template <int A>
-__device__ __forceinline__ void g_u1p(float2 (&x)[16], const float *__restrict__ MR, const float2 *__restrict__ MP) {
-    float mr[4];
-    float2 mp[4];
+__device__ __forceinline__ void g_u1p(float2 (&x)[16], const float2 *__restrict__ M) {
+    float2 m[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) { mr[e] = MR[e]; mp[e] = MP[e]; }
+    for (int e = 0; e < 4; ++e) m[e] = M[e];
 #pragma unroll
     for (int l = 0; l < 16; ++l) {
         if (l & (1 << A)) continue;
         const float2 p = x[l], q = x[l | (1 << A)];
-        x[l] = cmac2(mr[1], mp[1], q, cmul1(mr[0], mp[0], p));
-        x[l | (1 << A)] = cmac2(mr[3], mp[3], q, cmul1(mr[2], mp[2], p));
+        x[l] = cmac2(m[1], q, cmul1(m[0], p));
+        x[l | (1 << A)] = cmac2(m[3], q, cmul1(m[2], p));
     }
 }
 
 template <int A, int B>
-__device__ __forceinline__ void g_u2p(float2 (&x)[16], const float (&mr)[16], const float2 (&mp)[16]) {
+__device__ __forceinline__ void g_u2p(float2 (&x)[16], const float2 (&m)[16]) {
 #pragma unroll
     for (int l = 0; l < 16; ++l) {
         if (l & ((1 << A) | (1 << B))) continue;
@@ -735,9 +734,9 @@ __device__ __forceinline__ void g_u2p(float2 (&x)[16], const float (&mr)[16], co
         float2 o[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            float2 acc = cmul1(mr[r * 4], mp[r * 4], v[0]);
+            float2 acc = cmul1(m[r * 4], v[0]);
 #pragma unroll
-            for (int c = 1; c < 4; ++c) acc = cmac2(mr[r * 4 + c], mp[r * 4 + c], v[c], acc);
+            for (int c = 1; c < 4; ++c) acc = cmac2(m[r * 4 + c], v[c], acc);
             o[r] = acc;
         }
         x[l] = o[0];
@@ -747,10 +746,8 @@ __device__ __forceinline__ void g_u2p(float2 (&x)[16], const float (&mr)[16], co
     }
 }
 
-// table entry of a unit phase: complex64 (re, 0, -im, im) for cmul1, complex128 (re, im)
-template <typename C> struct TabEnt;
-template <> struct TabEnt<float2> { using T = float4; };
-template <> struct TabEnt<double2> { using T = double2; };
+// table entry of a unit phase: (re, im) in the state's precision
+template <typename C> struct TabEnt { using T = C; };
 
 // The pass record of a group pass travels as a __grid_constant__ kernel
 // parameter: every field, sub-op and matrix is read with uniform constant-bank
@@ -790,11 +787,7 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
 #pragma unroll
             for (int b = 0; b < 7; ++b)
                 if ((e >> b) & 1) ph += lb[b];
-            const C u = unit_phase<C>(ph);
-            typename TabEnt<C>::T t;
-            if constexpr (sizeof(C) == 8) t = make_float4(u.x, 0.f, -u.y, u.y);
-            else t = u;
-            tables[d.ent_off + (uint32_t)(e >> 4) * STV_TAB_STRIDE + (e & 15)] = t;
+            tables[d.ent_off + (uint32_t)(e >> 4) * STV_TAB_STRIDE + (e & 15)] = unit_phase<C>(ph);
         }
     }
 }
@@ -809,22 +802,17 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
     for (int k = 0; k < nsub; ++k) {
         const StvSub sb = subs[k];
         const C *M = (const C *)(mat + ((uint32_t)sb.arg << 4));
-        const float *MR = (const float *)M;
         const int code = sb.code;
         if (code >= SUBC_U2 && code < SUBC_U2 + 6) {        // the common case first
             switch (code) {
 #define STV_U2(p, a, b)                                                                     \
     case SUBC_U2 + (p): {                                                                   \
+        C m[16];                                                                            \
+        _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = M[e];                         \
         if constexpr (kPacked) {                                                            \
-            float mr[16];                                                                   \
-            float2 mp[16];                                                                  \
-            const float2 *MP = (const float2 *)(MR + 16);                                   \
-            _Pragma("unroll") for (int e = 0; e < 16; ++e) { mr[e] = MR[e]; mp[e] = MP[e]; } \
             _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
-                g_u2p<(a), (b)>(*(float2(*)[16]) & x[i], mr, mp);                          \
+                g_u2p<(a), (b)>(*(float2(*)[16]) & x[i], *(const float2(*)[16]) & m);      \
         } else {                                                                            \
-            C m[16];                                                                        \
-            _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = M[e];                     \
             _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u2<(a), (b)>(x[i], m);         \
         }                                                                                   \
         break;                                                                              \
@@ -843,10 +831,7 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
                 if constexpr (kPacked) {
                     float2(&xv)[16] = *(float2(*)[16]) & x[i];
 #pragma unroll
-                    for (int l = 0; l < 16; ++l) {
-                        const float4 q = row[l];
-                        xv[l] = cmul1(q.x, make_float2(q.z, q.w), xv[l]);
-                    }
+                    for (int l = 0; l < 16; ++l) xv[l] = cmul1(row[l], xv[l]);
                 } else {
 #pragma unroll
                     for (int l = 0; l < 16; ++l) x[i][l] = cmul(x[i][l], row[l]);
@@ -858,7 +843,7 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
     case SUBC_U1 + (a): {                                                                   \
         if constexpr (kPacked) {                                                            \
             _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
-                g_u1p<(a)>(*(float2(*)[16]) & x[i], MR, (const float2 *)(MR + 4));         \
+                g_u1p<(a)>(*(float2(*)[16]) & x[i], (const float2 *)M);                     \
         } else {                                                                            \
             _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u1<(a)>(x[i], M);               \
         }                                                                                   \
@@ -897,14 +882,20 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
     const int nvb = g.nvb;
     uint32_t braw0 = 0, bsw0 = 0;
 #pragma unroll
-    for (int b = 0; b < TB; ++b)
+    for (int b = 0; b < TB; ++b) {
+        const uint2 vb = *(const uint2 *)g.vbit[b];
         if (b < nvb && ((ctid >> b) & 1)) {
-            braw0 |= g.vraw[b];
-            bsw0 ^= g.vsw[b];
+            braw0 |= vb.x;
+            bsw0 ^= vb.y;
         }
+    }
     uint32_t so[16];
 #pragma unroll
-    for (int l = 0; l < 16; ++l) so[l] = g.sw_off[l];
+    for (int l = 0; l < 16; l += 2) {
+        const uint2 w = *(const uint2 *)&g.sw_off[l];
+        so[l] = w.x;
+        so[l + 1] = w.y;
+    }
     const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off);
     const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
     const int nsub = g.nsub;
@@ -919,8 +910,8 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
             bsw[i] = bsw0;
             for (int b = TB; b < nvb; ++b)
                 if ((v >> b) & 1) {
-                    braw[i] |= g.vraw[b];
-                    bsw[i] ^= g.vsw[b];
+                    braw[i] |= g.vbit[b][0];
+                    bsw[i] ^= g.vbit[b][1];
                 }
         }
         C x[NV][16];
@@ -1030,7 +1021,7 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
     const StvGroup *groups = (const StvGroup *)(rec.b + P->ops_off);
     const uint8_t *mat = rec.b + P->mat_off;
     const uint32_t esz = sizeof(C);
-    const uint32_t tab_pad = (P->tab_entries * 16u + 127u) & ~127u;       // 16-B table entries
+    const uint32_t tab_pad = (P->tab_entries * esz + 127u) & ~127u;
     uint8_t *hk = smem;                                                    // 1024 B: chunk hashes
     typename TabEnt<C>::T *tables = (typename TabEnt<C>::T *)(smem + 1024);
     C *tiles = (C *)(smem + 1024 + tab_pad);
@@ -1320,7 +1311,7 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
                               int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st,
                               int *kernels) {
     const size_t esz = c128 ? 16 : 8;
-    const size_t smem = 1024 + (((size_t)tab_entries * 16 + 127u) & ~(size_t)127) + (size_t)kGStages * (esz << S);
+    const size_t smem = 1024 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)kGStages * (esz << S);
     const uint64_t ntiles = 1ull << (n_local - S);
     if (smem > 227 * 1024 || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
     static thread_local RecParam rp;

@@ -128,9 +128,8 @@ struct alignas(16) StvGroup {
     int32_t nvb;               // number of vector bits (S - 4)
     int32_t pair16;            // complex64 with tpos[0] == 0: amplitudes l, l|1 share a 16-B chunk
     int32_t tpos[4];
-    uint16_t sw_off[16];       // swizzled tile offset (amplitudes) of local index l
-    uint16_t vsw[STV_MAX_TILE_BITS - 4];    // swizzled offset of vector bit b
-    uint16_t vraw[STV_MAX_TILE_BITS - 4];   // raw tile offset (1 << position) of vector bit b
+    uint32_t sw_off[16];       // swizzled tile offset (amplitudes) of local index l
+    uint32_t vbit[STV_MAX_TILE_BITS - 4][2];   // vector bit b: {raw tile offset 1 << position, swizzled offset}
 };
 
 // Per-tile phase table of one group DIAG sub-op, over index e = l | (r << 4):
@@ -139,7 +138,7 @@ struct alignas(16) StvGroup {
 // Per-tile term {a, b, ang}: a >= 0: index bit a of e times bit b of the
 // tile's full base; a == -1: bit b of the base; a <= -2: bits (-2 - a) and b.
 // Entries live in shared memory at ent_off + r * STV_TAB_STRIDE + l (rows padded against
-// bank conflicts between lanes with different r; rows are read as 16-B pairs).
+// bank conflicts between lanes with different r).
 struct alignas(16) StvDTab {
     uint32_t stat_off;         // byte offset (pass record) of uint64 stat[16 << m]
     uint32_t term_off;         // byte offset of StvTerm[nterm]
@@ -149,4 +148,4 @@ struct alignas(16) StvDTab {
     uint16_t vraw[STV_MAX_VBITS];   // raw tile offsets of the V-bits (0 for unused)
     uint16_t pad;
 };
-#define STV_TAB_STRIDE 18        // entries per table row: 16 + 2 pad (16-B aligned rows, no bank conflicts)
+#define STV_TAB_STRIDE 17        // entries per table row: 16 + 1 pad (rows of different lanes hit different banks)

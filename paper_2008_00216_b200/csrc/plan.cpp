@@ -553,9 +553,8 @@ static size_t diag_table_bytes(const QForm &f, uint64_t vmask, int amp_bytes, in
     for (uint64_t u : sets) {
         const int m = __builtin_popcountll(u);
         bytes += sizeof(StvDTab) + sizeof(StvSub) + ((size_t)128 << m) + 32;
-        *tab_smem += (size_t)(STV_TAB_STRIDE * 16) << m;
+        *tab_smem += (size_t)(STV_TAB_STRIDE * amp_bytes) << m;
     }
-    (void)amp_bytes;
     *ntab = (int)sets.size();
     return bytes;
 }
@@ -1066,17 +1065,6 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                 align(b, 16);
                 return off;
             };
-            // group sub-op matrices, complex64: re parts (scalars, broadcast operands of
-            // FFMA2), then (-im, im) pairs, so a complex multiply-add is two FFMA2
-            auto put_matrix_packed = [&](const std::vector<cd> &M) -> uint32_t {
-                if (c128) return put_matrix(M);
-                const uint32_t off = (uint32_t)(b.size() - at - hd.mat_off);
-                for (const cd &z : M) { float v = (float)z.real(); put(b, &v, 4); }
-                align(b, 8);
-                for (const cd &z : M) { float v[2] = {-(float)z.imag(), (float)z.imag()}; put(b, v, 8); }
-                align(b, 16);
-                return off;
-            };
             // matrices
             align(b, 16);
             hd.mat_off = (uint32_t)(b.size() - at);
@@ -1116,7 +1104,7 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                                 static const int pidx[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
                                 sub.code = (uint16_t)(SUBC_U2 + pidx[x][lbit(so.tg[1])]);
                             }
-                            const uint32_t mo = put_matrix_packed(so.M);
+                            const uint32_t mo = put_matrix(so.M);
                             if (mo % 16 || mo / 16 > 0xffff) throw std::runtime_error("matrix offset");
                             sub.arg = (uint16_t)(mo / 16);
                         } else if (so.type == OP_CNOT) {
@@ -1189,14 +1177,14 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                 g.pair16 = (!c128 && pos[0] == 0) ? 1 : 0;
                 const std::vector<int> vp = vector_bit_order(pos, hd.S, c128);
                 for (int v = 0; v < g.nvb; ++v) {
-                    g.vraw[v] = (uint16_t)(1u << vp[v]);
-                    g.vsw[v] = (uint16_t)swz_amp(1u << vp[v], c128);
+                    g.vbit[v][0] = 1u << vp[v];
+                    g.vbit[v][1] = swz_amp(1u << vp[v], c128);
                 }
                 for (int l = 0; l < 16; ++l) {
                     uint32_t off = 0;
                     for (int j = 0; j < 4; ++j)
                         if ((l >> j) & 1) off |= 1u << pos[j];
-                    g.sw_off[l] = (uint16_t)swz_amp(off, c128);
+                    g.sw_off[l] = swz_amp(off, c128);
                 }
                 align(b, 16);
                 g.nsub = (int)subs[i].size();

@@ -38,8 +38,7 @@ class Sub(ct.Structure):
 
 class Group(ct.Structure):
     _fields_ = [("nsub", ct.c_int32), ("sub_off", ct.c_uint32), ("nvb", ct.c_int32), ("pair16", ct.c_int32),
-                ("tpos", ct.c_int32 * 4), ("sw_off", ct.c_uint16 * 16), ("vsw", ct.c_uint16 * (MAXT - 4)),
-                ("vraw", ct.c_uint16 * (MAXT - 4)), ("pad", ct.c_uint8 * 8)]
+                ("tpos", ct.c_int32 * 4), ("sw_off", ct.c_uint32 * 16), ("vbit", (ct.c_uint32 * 2) * (MAXT - 4))]
 
 
 class DTab(ct.Structure):
@@ -57,7 +56,7 @@ class Pass(ct.Structure):
 
 
 assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 8 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
-assert ct.sizeof(Group) == 112 and ct.sizeof(DTab) == 32
+assert ct.sizeof(Group) == 176 and ct.sizeof(DTab) == 32
 
 U2_PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
 
@@ -154,10 +153,10 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
         c = sb.code
         ctl_raw, ctl_phys = sb.ctl & 0xFFFF, (sb.ctl >> 16) - 1
         if c < 4:
-            psi = PI._apply_dense(psi, n, [G[c]], _matrix_packed(blob, po + P.mat_off + 16 * sb.arg, 2, c128))
+            psi = PI._apply_dense(psi, n, [G[c]], _matrix(blob, po + P.mat_off + 16 * sb.arg, 2, c128))
         elif c < 10:
             a, b = U2_PAIRS[c - 4]
-            psi = PI._apply_dense(psi, n, [G[a], G[b]], _matrix_packed(blob, po + P.mat_off + 16 * sb.arg, 4, c128))
+            psi = PI._apply_dense(psi, n, [G[a], G[b]], _matrix(blob, po + P.mat_off + 16 * sb.arg, 4, c128))
         elif 10 <= c < 30:
             cl, t = (c - 10) // 4 - 1, (c - 10) % 4
             ctl = []

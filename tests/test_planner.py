@@ -246,7 +246,7 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
         if P.kind != 1 or not P.grouped:
             continue
         for gi in range(P.nops):
-            g = BE._at(blob, BE.Group, po + P.ops_off + 112 * gi)
+            g = BE._at(blob, BE.Group, po + P.ops_off + 176 * gi)
             ngroups += 1
             assert g.nvb == P.S - 4
             assert bool(g.pair16) == (not c128 and g.tpos[0] == 0)
@@ -255,7 +255,7 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
                 i = 0
                 for b in range(g.nvb):
                     if (v >> b) & 1:
-                        i |= g.vraw[b]
+                        i |= g.vbit[b][0]
                 for k in range(4):
                     if (l >> k) & 1:
                         i |= 1 << g.tpos[k]
@@ -265,7 +265,7 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
                 s = 0
                 for b in range(g.nvb):
                     if (v >> b) & 1:
-                        s ^= g.vsw[b]
+                        s ^= g.vbit[b][1]
                 return s ^ g.sw_off[l]
 
             seen = set()

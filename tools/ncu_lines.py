@@ -12,9 +12,9 @@ line_of = {}
 cur = None
 inl = None
 for ln in open(sys.argv[2]):
-    m = re.search(r'line (\d+)', ln)
+    m = re.search(r'File "([^"]+)", line (\d+)', ln)
     if '//##' in ln and m:
-        cur = int(m.group(1))
+        cur = int(m.group(2)) if m.group(1).endswith('kernels.cu') else -int(m.group(2))
         continue
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/', ln)
     if m:
@@ -28,4 +28,4 @@ src = open('/root/repo/paper_2008_00216_b200/csrc/kernels.cu').read().split('\n'
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 print('total', tot, 'samples', ts)
 for l, n in agg.most_common(top):
-    print('%6.2f%% %6.2f%%  L%-5s %s' % (100 * n / tot, 100 * samp[l] / ts, l, src[l - 1].strip()[:80] if l else ''))
+    print('%6.2f%% %6.2f%%  L%-5s %s' % (100 * n / tot, 100 * samp[l] / ts, l, (src[l - 1].strip()[:80] if l > 0 else ('<crt line %d>' % -l)) if l else ''))

@@ -16,7 +16,8 @@ bandwidth a one-pass-per-gate complex64 simulator would need to match this
 time (BASELINE.md "Derived context" defines the same quantity for the
 paper's CPU numbers).  It is whole-job (all ranks) and inversely
 proportional to sec/circuit, also reported.  The per-pass HBM fraction of
-peak is the `roofline` object (dominant kernel: the fused tile pass).
+peak is the `roofline` object (dominant kernel: the fused gate-group tile
+pass k_group_pass).
 """
 import argparse
 import json
@@ -130,14 +131,14 @@ def ncu_traffic():
 
 
 def roof(gbs, hbm, peak_kind, tflops, fp32_peak, tile_bytes, launches, tile_ms, flops_per_step):
-    """Roofline of the dominant kernel (k_tile_pass) against the resource that
+    """Roofline of the dominant kernel (k_group_pass) against the resource that
     binds it: HBM (algorithmic R+W bytes / time vs the measured copy peak) or
     the FP32 FMA pipe (algorithmic flops / time vs 148 x 128 x 2 x clock)."""
     if gbs is None:
         return None
     f_hbm = gbs / hbm
     f_alu = tflops / fp32_peak if tflops else 0.0
-    common = {"kernel": "k_tile_pass (fused tile pass)", "bytes_per_launch": tile_bytes, "launches": launches,
+    common = {"kernel": "k_group_pass (fused gate-group tile pass)", "bytes_per_launch": tile_bytes, "launches": launches,
               "avg_launch_ms": tile_ms / max(1, launches), "traffic": ncu_traffic(),
               "hbm": {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_hbm, "peak_kind": peak_kind},
               "alu": {"achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s", "frac": f_alu,

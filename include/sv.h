@@ -91,7 +91,8 @@ typedef struct {
 #define SV_OPT_ONE_GATE     0x08u /* one pass per gate (no fusion at all)      */
 #define SV_OPT_NO_DIAG_FOLD 0x10u /* never fold diagonal gates into matrices   */
 #define SV_OPT_NO_GROUPS    0x20u /* one shared-memory round trip per op (no register-resident gate groups) */
-#define SV_OPT_WARP_TILES   0x40u /* warp-per-tile kernel for passes with <= 10 tile bits (experimental)  */
+/* 0x40u reserved (was an experimental warp-per-tile kernel; ignored)                                     */
+#define SV_OPT_NO_VARIANTS  0x80u /* do not merge 2-qubit sub-op chains into per-tile variant matrices      */
 typedef struct {
     int32_t kmax;        /* max qubits of one fused dense op (1..5); 0 = default (4)     */
     int32_t tile_bits;   /* max tile bits |S| of a fused pass; 0 = default              */

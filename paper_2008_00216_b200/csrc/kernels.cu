@@ -711,11 +711,17 @@ __device__ __forceinline__ float2 cmul1(float2 m, float2 x) {
     return __ffma2_rn(make_float2(-x.y, x.x), make_float2(m.y, m.y), __fmul2_rn(x, make_float2(m.x, m.x)));
 }
 
+// one complex64 matrix entry as a single 64-bit uniform load (LDCU.64)
+__device__ __forceinline__ float2 ld_c64(const float2 *p) {
+    const unsigned long long w = *(const unsigned long long *)p;
+    return make_float2(__uint_as_float((unsigned)w), __uint_as_float((unsigned)(w >> 32)));
+}
+
 template <int A>
 __device__ __forceinline__ void g_u1p(float2 (&x)[16], const float2 *__restrict__ M) {
     float2 m[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) m[e] = M[e];
+    for (int e = 0; e < 4; ++e) m[e] = ld_c64(M + e);
 #pragma unroll
     for (int l = 0; l < 16; ++l) {
         if (l & (1 << A)) continue;
@@ -797,18 +803,39 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
 template <typename C, int NV>
 __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[NV], const StvSub *__restrict__ subs,
                                          int nsub, const uint8_t *__restrict__ mat, const StvDTab *__restrict__ tabs,
-                                         const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base) {
+                                         const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base,
+                                         uint32_t tord, uint64_t rank_bits) {
     constexpr bool kPacked = sizeof(C) == 8;
     for (int k = 0; k < nsub; ++k) {
-        const StvSub sb = subs[k];
-        const C *M = (const C *)(mat + ((uint32_t)sb.arg << 4));
-        const int code = sb.code;
-        if (code >= SUBC_U2 && code < SUBC_U2 + 6) {        // the common case first
-            switch (code) {
+        const uint2 ca = *(const uint2 *)&subs[k];         // code, arg: one LDCU.64
+        const int code = (int)ca.x;
+        const C *M = (const C *)(mat + ca.y);
+        int u2 = code - SUBC_U2;
+        if ((unsigned)(code - SUBC_U2V) < 6u) {             // per-tile variant: selector bits of the tile base
+            // selector byte c: tile-ordinal bit c, or (c & 0x80) a rank bit; unused selectors = 31 (always 0)
+            const uint32_t ctl = subs[k].ctl;
+            const uint32_t rb = (uint32_t)(rank_bits >> 32);   // rank bits sit at >= n_local >= 32 when present
+            uint32_t v = 0;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const uint32_t c = (ctl >> (8 + 8 * q)) & 0xffu;
+                const uint32_t b = (c & 0x80u) ? (rb >> (c & 31u)) : (tord >> (c & 31u));
+                v |= (b & 1u) << q;
+            }
+            M += v * 16;
+            u2 = code - SUBC_U2V;
+        }
+        if ((unsigned)u2 < 6u) {                              // the common case first
+            switch (u2 + SUBC_U2) {
 #define STV_U2(p, a, b)                                                                     \
     case SUBC_U2 + (p): {                                                                   \
         C m[16];                                                                            \
-        _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = M[e];                         \
+        if constexpr (kPacked) {                                                            \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e)                                  \
+                *(float2 *)&m[e] = ld_c64((const float2 *)M + e);                           \
+        } else {                                                                            \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = M[e];                     \
+        }                                                                                   \
         if constexpr (kPacked) {                                                            \
             _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
                 g_u2p<(a), (b)>(*(float2(*)[16]) & x[i], *(const float2(*)[16]) & m);      \
@@ -821,7 +848,7 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
 #undef STV_U2
             }
         } else if (code == SUBC_DIAG) {   // per-tile table row of each vector's V-bits
-            const StvDTab &d = tabs[sb.arg];
+            const StvDTab &d = tabs[ca.y];
             const uint32_t v0 = d.vraw[0], v1 = d.vraw[1], v2 = d.vraw[2];
             const uint32_t eo = d.ent_off;
 #pragma unroll
@@ -853,7 +880,7 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
 #undef STV_U1
 #define STV_CX(c, t)                                                                             \
     case SUBC_CNOT + 4 * ((c) + 1) + (t): {                                                      \
-        const uint32_t raw = sb.ctl & 0xffffu, ph = sb.ctl >> 16;                                \
+        const uint32_t ctl = subs[k].ctl, raw = ctl & 0xffffu, ph = ctl >> 16;                   \
         const bool pon = ph == 0 || ((full_base >> (ph - 1)) & 1);                               \
         _Pragma("unroll") for (int i = 0; i < NV; ++i)                                           \
             g_cnot<(c), (t)>(x[i], pon && (raw == 0 || (braw[i] & raw) != 0));                   \
@@ -876,7 +903,7 @@ template <typename C, int NT, int NV>
 __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
                                              const uint8_t *__restrict__ mat,
                                              const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base,
-                                             int ctid) {
+                                             uint32_t tord, int ctid) {
     constexpr int TB = NT == 128 ? 7 : 8;   // log2(NT)
     static_assert((1 << TB) == NT, "NT must be 128 or 256");
     const int nvb = g.nvb;
@@ -934,7 +961,7 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
                 for (int l = 0; l < 16; ++l) x[i][l] = tile[bsw[i] ^ so[l]];
             }
         }
-        run_subs<C, NV>(x, braw, subs, nsub, mat, tabs, tables, full_base);
+        run_subs<C, NV>(x, braw, subs, nsub, mat, tabs, tables, full_base, tord, P->rank_bits);
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             if (i > 0 && !live1) continue;
@@ -950,7 +977,7 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
     }
 }
 
-constexpr int kGStages = 2;        // double-buffered tiles (prefetch distance 1)
+constexpr int kGStagesDefault = 2;  // double-buffered tiles (prefetch distance 1)
 
 // Tile copy state that does not change from tile to tile (computed once per CTA).
 struct CopyPlan {
@@ -992,6 +1019,20 @@ __device__ __forceinline__ void tile_copy_fast(uint8_t *gstate, uint8_t *stile, 
             }
             roff = masked_add(roff, cp.d1, hmask);
         }
+    } else if ((hmask >> 32) == 0) {
+        // all tile bits below 2^32: 32-bit offset arithmetic from the tile's base pointer
+        uint8_t *tb = gstate + base * esz + cp.within;
+        const uint32_t m32 = (uint32_t)hmask, step = (uint32_t)cp.dstep;
+        uint32_t roff = (uint32_t)cp.roff0;
+        uint32_t k = 0;
+        for (uint32_t c = t; c < cp.total; c += NT, ++k) {
+            uint8_t *g = tb + (size_t)roff * esz;
+            const uint32_t slot = c ^ hash_t ^ hk[k];
+            uint8_t *sm = stile + slot * 16u;
+            if (kLoad) cp_async16(sm, g);
+            else *(uint4 *)g = *(const uint4 *)sm;
+            roff = ((roff | ~m32) + step) & m32;
+        }
     } else {
         uint64_t roff = cp.roff0;
         uint32_t k = 0;
@@ -1006,7 +1047,7 @@ __device__ __forceinline__ void tile_copy_fast(uint8_t *gstate, uint8_t *stile, 
     }
 }
 
-template <typename R, int NT, int NV>
+template <typename R, int NT, int NV, int kGStages>
 __global__ void __launch_bounds__(NT, sizeof(R) == 4 ? 3 : 2)
 k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
              uint32_t ntiles, int dbg_flags, const __grid_constant__ RecParam rec) {
@@ -1064,7 +1105,7 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
             __syncthreads();
         }
         for (int o = 0; o < nops; ++o) {
-            group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, tid);
+            group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, first + j * stride, tid);
             __syncthreads();
         }
         tile_copy_fast<false, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
@@ -1288,22 +1329,22 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
     return e;
 }
 
-template <typename R, int NT, int NV>
+template <typename R, int NT, int NV, int NS>
 static cudaError_t group_launch(void *state, const uint8_t *dblob, uint32_t pass_off, uint32_t ntiles, size_t smem,
                                 const RecParam &rp, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_group_pass<R, NT, NV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_group_pass<R, NT, NV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_pass<R, NT, NV>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_pass<R, NT, NV, NS>, NT, smem);
     if (occ < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)num_sms() * occ;
     if (grid > ntiles) grid = ntiles;
     static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
-    k_group_pass<R, NT, NV><<<(unsigned)grid, NT, smem, st>>>((typename C2T<R>::T *)state, dblob, pass_off, ntiles,
-                                                               dbg, rp);
+    k_group_pass<R, NT, NV, NS><<<(unsigned)grid, NT, smem, st>>>((typename C2T<R>::T *)state, dblob, pass_off,
+                                                                   ntiles, dbg, rp);
     return cudaGetLastError();
 }
 
@@ -1311,16 +1352,18 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
                               int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st,
                               int *kernels) {
     const size_t esz = c128 ? 16 : 8;
-    const size_t smem = 1024 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)kGStages * (esz << S);
+    static const int cfg = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
+    const int ns = cfg == 2 ? 3 : kGStagesDefault;
+    const size_t smem = 1024 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)ns * (esz << S);
     const uint64_t ntiles = 1ull << (n_local - S);
     if (smem > 227 * 1024 || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
     static thread_local RecParam rp;
     std::memcpy(rp.b, hrec, rec_bytes);
-    static const int cfg = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
     cudaError_t e;
-    if (c128) e = group_launch<double, 128, 1>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
-    else if (cfg == 1) e = group_launch<float, 128, 2>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
-    else e = group_launch<float, 256, 1>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    if (c128) e = group_launch<double, 128, 1, kGStagesDefault>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    else if (cfg == 1) e = group_launch<float, 128, 2, kGStagesDefault>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    else if (cfg == 2) e = group_launch<float, 256, 1, 3>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    else e = group_launch<float, 256, 1, kGStagesDefault>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
     ++*kernels;
     return e;
 }

@@ -685,6 +685,166 @@ static void add_gate(OpsEval &ev, const PGate &g, uint64_t S, const PlanOptions 
     tally(ev, amp_bytes, S);
 }
 
+// ---------------------------------------------------------------------------
+// Chains of 2-qubit sub-ops on the same pair P inside a gate group, separated
+// only by ops on other bits and by diagonal sub-ops whose terms on P couple P
+// to bits OUTSIDE the tile, are one 4x4 operator per tile: the diagonal factor
+// on P is fixed once the tile's outside bits are.  The chain becomes one dense
+// sub-op with 2^|sel| per-tile variants (products in complex128, rounded once;
+// Eq. 2 coalescing of PAPER.md L645-653 with the phases of P:L503-527 bound
+// per tile).  The kernel picks the variant from the tile base (a uniform
+// index) -- the parts of the diagonals on other bits stay as they were.
+// ---------------------------------------------------------------------------
+static const int kMaxSel = 3;
+
+static std::vector<cd> diag_on_pair(const QForm &part, int a, int b, const std::vector<int> &sel, int v) {
+    // 4x4 diagonal over P = (a < b) (local index bit0 = a, bit1 = b) for selector assignment v
+    std::vector<cd> D(16, cd(0, 0));
+    for (int l = 0; l < 4; ++l) {
+        uint64_t j = 0;
+        if (l & 1) j |= 1ull << a;
+        if (l & 2) j |= 1ull << b;
+        for (size_t i = 0; i < sel.size(); ++i)
+            if ((v >> i) & 1) j |= 1ull << sel[i];
+        D[(size_t)l * 4 + l] = std::polar(1.0, angle_of_turns(part.eval(j)));
+    }
+    return D;
+}
+
+static void merge_variant_chains(FOp &grp, uint64_t S, int nl) {
+    // selectors on global (rank) bits are encoded relative to bit 32 (pass_format.h)
+    const uint64_t sel_ok = nl >= 32 ? ~0ull : ((1ull << nl) - 1);
+    std::vector<FOp> &ops = grp.subs;
+    for (size_t i = 0; i < ops.size(); ++i) {
+        if (ops[i].type != OP_DENSE || ops[i].tg.size() != 2) continue;
+        const int a = ops[i].tg[0], b = ops[i].tg[1];
+        const uint64_t P = (1ull << a) | (1ull << b);
+        // previous op touching P
+        int j = (int)i - 1;
+        for (; j >= 0; --j) {
+            const FOp &o = ops[j];
+            if (o.type == OP_DIAG) continue;
+            if (o.qmask & P) break;
+        }
+        if (j < 0 || ops[j].type != OP_DENSE || ops[j].tg.size() != 2 || ops[j].dmask != P) continue;
+        // the P-parts of the diagonals in between must couple P only to bits outside the tile
+        bool ok = true;
+        std::vector<int> sel = ops[j].sel;
+        std::vector<QForm> parts;
+        for (size_t k = j + 1; k < i && ok; ++k) {
+            const FOp &o = ops[k];
+            if (o.type != OP_DIAG) continue;
+            QForm part;
+            for (auto &kv : o.form.lin)
+                if ((P >> kv.first) & 1) part.lin[kv.first] += kv.second;
+            for (auto &kv : o.form.quad) {
+                const int x = kv.first.first, y = kv.first.second;
+                const bool px = (P >> x) & 1, py = (P >> y) & 1;
+                if (!px && !py) continue;
+                if (px && py) { part.quad[kv.first] += kv.second; continue; }
+                const int other = px ? y : x;
+                if ((S >> other) & 1) { ok = false; break; }        // varies inside the tile
+                if (!((sel_ok >> other) & 1)) { ok = false; break; }
+                part.quad[kv.first] += kv.second;
+                if (std::find(sel.begin(), sel.end(), other) == sel.end()) sel.push_back(other);
+            }
+            parts.push_back(part);
+        }
+        for (int x : ops[i].sel)
+            if (std::find(sel.begin(), sel.end(), x) == sel.end()) sel.push_back(x);
+        if (!ok || (int)sel.size() > kMaxSel) continue;
+        // the per-tile constant parts of those diagonals (constant, terms on bits outside the
+        // tile only) ride along when the selector budget allows: they are scalars per tile
+        std::vector<bool> take_const(i, false);
+        {
+            size_t pi = 0;
+            for (size_t k = j + 1; k < i; ++k) {
+                const FOp &o = ops[k];
+                if (o.type != OP_DIAG) continue;
+                std::vector<int> s2 = sel;
+                auto need = [&](int q) {
+                    if (std::find(s2.begin(), s2.end(), q) == s2.end()) s2.push_back(q);
+                };
+                bool any = o.form.cst != 0;
+                for (auto &kv : o.form.lin)
+                    if (!((S >> kv.first) & 1)) { need(kv.first); any = true; if (!((sel_ok >> kv.first) & 1)) any = false, s2.assign(kMaxSel + 1, 0); }
+                for (auto &kv : o.form.quad)
+                    if (!((S >> kv.first.first) & 1) && !((S >> kv.first.second) & 1)) {
+                        need(kv.first.first);
+                        need(kv.first.second);
+                        any = true;
+                        if (!((sel_ok >> kv.first.first) & 1) || !((sel_ok >> kv.first.second) & 1))
+                            s2.assign(kMaxSel + 1, 0);                 // cannot encode: leave in place
+                    }
+                if (any && (int)s2.size() <= kMaxSel) {
+                    sel = s2;
+                    take_const[k] = true;
+                    QForm &part = parts[pi];
+                    part.cst += o.form.cst;
+                    for (auto &kv : o.form.lin)
+                        if (!((S >> kv.first) & 1)) part.lin[kv.first] += kv.second;
+                    for (auto &kv : o.form.quad)
+                        if (!((S >> kv.first.first) & 1) && !((S >> kv.first.second) & 1)) part.quad[kv.first] += kv.second;
+                }
+                ++pi;
+            }
+        }
+        std::sort(sel.begin(), sel.end());
+        const int nv = 1 << (int)sel.size();
+        auto variant_of = [&](const FOp &o, int v) -> const std::vector<cd> & {
+            if (o.Mv.empty()) return o.M;
+            int w = 0;
+            for (size_t q = 0; q < o.sel.size(); ++q) {
+                const size_t pos = std::find(sel.begin(), sel.end(), o.sel[q]) - sel.begin();
+                if ((v >> pos) & 1) w |= 1 << q;
+            }
+            return o.Mv[(size_t)w];
+        };
+        std::vector<std::vector<cd>> Mv((size_t)nv);
+        for (int v = 0; v < nv; ++v) {
+            std::vector<cd> M = variant_of(ops[j], v);
+            for (const QForm &part : parts) M = matmul(diag_on_pair(part, a, b, sel, v), M, 4);
+            Mv[(size_t)v] = matmul(variant_of(ops[i], v), M, 4);
+        }
+        // strip the moved parts from the diagonals; drop diagonals that became empty
+        const uint64_t out = ~S;
+        for (size_t k = j + 1; k < i; ++k) {
+            FOp &o = ops[k];
+            if (o.type != OP_DIAG) continue;
+            const bool tc = take_const[k];
+            if (tc) o.form.cst = 0;
+            for (auto it = o.form.lin.begin(); it != o.form.lin.end();) {
+                const bool mv = ((P >> it->first) & 1) || (tc && ((out >> it->first) & 1));
+                it = mv ? o.form.lin.erase(it) : std::next(it);
+            }
+            for (auto it = o.form.quad.begin(); it != o.form.quad.end();) {
+                const int x = it->first.first, y = it->first.second;
+                const bool mv = ((P >> x) & 1) || ((P >> y) & 1) || (tc && ((out >> x) & 1) && ((out >> y) & 1));
+                it = mv ? o.form.quad.erase(it) : std::next(it);
+            }
+            o.qmask = o.form.qubits();
+        }
+        FOp merged = ops[i];
+        merged.Mv = Mv;
+        merged.sel = sel;
+        merged.M = Mv[0];
+        ops[i] = merged;
+        ops.erase(ops.begin() + j);
+        --i;
+        for (size_t k = 0; k < ops.size();) {
+            if (ops[k].type == OP_DIAG && ops[k].form.trivial()) {
+                ops.erase(ops.begin() + (long)k);
+                if (k <= i) --i;
+            } else if (k > 0 && ops[k].type == OP_DIAG && ops[k - 1].type == OP_DIAG) {
+                ops[k - 1].form.add(ops[k].form);             // adjacent diagonals: one sub-op
+                ops[k - 1].qmask = ops[k - 1].form.qubits();
+                ops.erase(ops.begin() + (long)k);
+                if (k <= i) --i;
+            } else ++k;
+        }
+    }
+}
+
 // Algorithmic floating-point work per amplitude: a k-qubit
 // dense op costs 8 * 2^k flops (2^k complex multiply-adds), a diagonal phase
 // one complex multiply (6), a CNOT none.
@@ -847,6 +1007,9 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                 else S = S0;
             }
             pass.S = S;
+            if (!(opt.flags & SV_OPT_NO_VARIANTS))
+                for (FOp &o : pass.ops)
+                    if (o.type == OP_GROUP) merge_variant_chains(o, S, nl);
             plan.alg_bytes += amp_pass_bytes;
             plan.alg_flops += pass_flops_per_amp(pass.ops) * std::ldexp(1.0, nl);
         }
@@ -1102,11 +1265,28 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                             if (so.tg.size() == 1) sub.code = SUBC_U1 + x;
                             else {
                                 static const int pidx[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
-                                sub.code = (uint16_t)(SUBC_U2 + pidx[x][lbit(so.tg[1])]);
+                                sub.code = (so.Mv.empty() ? SUBC_U2 : SUBC_U2V) + pidx[x][lbit(so.tg[1])];
                             }
-                            const uint32_t mo = put_matrix(so.M);
-                            if (mo % 16 || mo / 16 > 0xffff) throw std::runtime_error("matrix offset");
-                            sub.arg = (uint16_t)(mo / 16);
+                            if (so.Mv.empty()) sub.arg = put_matrix(so.M);
+                            else {
+                                sub.arg = put_matrix(so.Mv[0]);
+                                for (size_t v = 1; v < so.Mv.size(); ++v) put_matrix(so.Mv[v]);
+                                // selector q as a bit of the tile ordinal t (base = pdep(t, out_mask)),
+                                // or 0x80 | physical bit for a global (rank) bit: both uniform per CTA tile
+                                sub.ctl = (uint32_t)so.sel.size();
+                                for (size_t q = 0; q < 3; ++q) {
+                                    uint32_t code = 31;                       // unused: tile-ordinal bit 31 = 0
+                                    if (q < so.sel.size()) {
+                                        const int p = so.sel[q];
+                                        if (p < n_local) code = (uint32_t)__builtin_popcountll(hd.out_mask & ((1ull << p) - 1));
+                                        else {
+                                            if (p < 32) throw std::runtime_error("rank selector below bit 32");
+                                            code = 0x80u | (uint32_t)(p - 32);
+                                        }
+                                    }
+                                    sub.ctl |= code << (8 + 8 * q);
+                                }
+                            }
                         } else if (so.type == OP_CNOT) {
                             int c = -1;
                             // a control on one of the group's 4 positions (a T bit or a padding
@@ -1115,7 +1295,7 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                                 c = lbit(so.c);
                             else if (loc[so.c] >= 0) sub.ctl = 1u << loc[so.c];
                             else sub.ctl = (uint32_t)(so.c + 1) << 16;
-                            sub.code = (uint16_t)(SUBC_CNOT + 4 * (c + 1) + lbit(so.t));
+                            sub.code = SUBC_CNOT + 4 * (c + 1) + lbit(so.t);
                         } else {
                             sub.code = SUBC_DIAG;
                         }
@@ -1164,7 +1344,7 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                         StvSub sub;
                         std::memset(&sub, 0, sizeof(sub));
                         sub.code = SUBC_DIAG;
-                        sub.arg = (uint16_t)tabs.size();
+                        sub.arg = (uint32_t)tabs.size();
                         tabs.push_back(d);
                         out.push_back(sub);
                     }
@@ -1246,6 +1426,23 @@ static std::string ops_json(const std::vector<FOp> &ops) {
             o << "],\"im\":[";
             for (size_t t = 0; t < f.M.size(); ++t) o << (t ? "," : "") << f.M[t].imag();
             o << "]";
+            if (!f.Mv.empty()) {
+                o << ",\"sel\":[";
+                for (size_t t = 0; t < f.sel.size(); ++t) o << (t ? "," : "") << f.sel[t];
+                o << "],\"vre\":[";
+                for (size_t v = 0; v < f.Mv.size(); ++v) {
+                    o << (v ? "," : "") << "[";
+                    for (size_t t = 0; t < f.Mv[v].size(); ++t) o << (t ? "," : "") << f.Mv[v][t].real();
+                    o << "]";
+                }
+                o << "],\"vim\":[";
+                for (size_t v = 0; v < f.Mv.size(); ++v) {
+                    o << (v ? "," : "") << "[";
+                    for (size_t t = 0; t < f.Mv[v].size(); ++t) o << (t ? "," : "") << f.Mv[v][t].imag();
+                    o << "]";
+                }
+                o << "]";
+            }
         } else if (f.type == OP_DIAG) {
             o << ",\"cst\":\"" << f.form.cst << "\",\"lin\":[";
             bool c = false;

@@ -79,6 +79,10 @@ struct FOp {
     uint64_t qmask = 0, dmask = 0;
     uint64_t T = 0;           // GROUP: tile bits held in registers (<= 4, actual physical)
     std::vector<FOp> subs;    // GROUP: sub-ops (DENSE k<=2, DIAG, CNOT) applied in registers
+    // DENSE 2-qubit sub-op with per-tile variants: Mv[v] is the matrix for the
+    // tile whose physical bits sel[i] (all outside the tile) equal bit i of v
+    std::vector<std::vector<cd>> Mv;
+    std::vector<int> sel;
 };
 
 struct PPass {

@@ -33,7 +33,7 @@ class Op(ct.Structure):
 
 
 class Sub(ct.Structure):
-    _fields_ = [("code", ct.c_uint16), ("arg", ct.c_uint16), ("ctl", ct.c_uint32)]
+    _fields_ = [("code", ct.c_int32), ("arg", ct.c_uint32), ("ctl", ct.c_uint32), ("pad", ct.c_uint32)]
 
 
 class Group(ct.Structure):
@@ -55,7 +55,7 @@ class Pass(ct.Structure):
                 ("tab_entries", ct.c_uint32), ("pad2", ct.c_int32)]
 
 
-assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 8 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
+assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
 assert ct.sizeof(Group) == 176 and ct.sizeof(DTab) == 32
 
 U2_PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
@@ -149,14 +149,37 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
     G = [pos2phys[g.tpos[i]] for i in range(4)]
     assert len(set(g.sw_off[l] for l in range(16))) == 16
     for k in range(g.nsub):
-        sb = _at(blob, Sub, po + g.sub_off + 8 * k)
+        sb = _at(blob, Sub, po + g.sub_off + 16 * k)
         c = sb.code
         ctl_raw, ctl_phys = sb.ctl & 0xFFFF, (sb.ctl >> 16) - 1
         if c < 4:
-            psi = PI._apply_dense(psi, n, [G[c]], _matrix(blob, po + P.mat_off + 16 * sb.arg, 2, c128))
+            psi = PI._apply_dense(psi, n, [G[c]], _matrix(blob, po + P.mat_off + sb.arg, 2, c128))
         elif c < 10:
             a, b = U2_PAIRS[c - 4]
-            psi = PI._apply_dense(psi, n, [G[a], G[b]], _matrix(blob, po + P.mat_off + 16 * sb.arg, 4, c128))
+            psi = PI._apply_dense(psi, n, [G[a], G[b]], _matrix(blob, po + P.mat_off + sb.arg, 4, c128))
+        elif 31 <= c < 37:
+            a, b = U2_PAIRS[c - 31]
+            nsel = sb.ctl & 0xFF
+            outbits = [b for b in range(64) if (P.out_mask >> b) & 1]
+            sel = []
+            for i in range(3):
+                code = (sb.ctl >> (8 + 8 * i)) & 0xFF
+                if i >= nsel:
+                    assert code == 31                          # unused selector: tile-ordinal bit 31
+                    continue
+                # tile-ordinal bit index (base = pdep(t, out_mask)) or 0x80 | (global bit - 32)
+                sel.append(32 + (code & 0x7F) if code & 0x80 else outbits[code])
+            assert all(s_ not in pos2phys for s_ in sel)      # selectors are outside the tile
+            esz = 16 if c128 else 8
+            jj = np.arange(1 << n)
+            out = np.zeros_like(psi)
+            for v in range(1 << nsel):
+                M = _matrix(blob, po + P.mat_off + sb.arg + v * 16 * esz, 4, c128)
+                m = np.ones(1 << n, dtype=bool)
+                for i, s_ in enumerate(sel):
+                    m &= ((jj >> s_) & 1) == ((v >> i) & 1)
+                out[m] = PI._apply_dense(psi, n, [G[a], G[b]], M)[m]
+            psi = out
         elif 10 <= c < 30:
             cl, t = (c - 10) // 4 - 1, (c - 10) % 4
             ctl = []

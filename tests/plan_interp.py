@@ -76,7 +76,20 @@ def run(plan, x0=0, psi=None):
                 psi = _bitswap(psi, n, gb, lb)
             continue
         for op in _flat(ps["ops"]):
-            if op["type"] == 1:
+            if op["type"] == 1 and "sel" in op:
+                # per-tile variants: the selector bits are untouched by the op, so each
+                # selector value's subspace is invariant
+                D = 1 << len(op["tg"])
+                j = np.arange(1 << n)
+                out = np.zeros_like(psi)
+                for v, (vr, vi) in enumerate(zip(op["vre"], op["vim"])):
+                    M = (np.array(vr) + 1j * np.array(vi)).reshape(D, D)
+                    m = np.ones(1 << n, dtype=bool)
+                    for i, b in enumerate(op["sel"]):
+                        m &= ((j >> b) & 1) == ((v >> i) & 1)
+                    out[m] = _apply_dense(psi, n, op["tg"], M)[m]
+                psi = out
+            elif op["type"] == 1:
                 D = 1 << len(op["tg"])
                 M = (np.array(op["re"]) + 1j * np.array(op["im"])).reshape(D, D)
                 psi = _apply_dense(psi, n, op["tg"], M)

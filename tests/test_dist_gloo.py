@@ -90,7 +90,19 @@ def _run_dist(rank, world, port, n, seed, tile_bits, q):
                 nremap += 1
                 continue
             for op in PI._flat(ps["ops"]):
-                if op["type"] == 1:
+                if op["type"] == 1 and "sel" in op:
+                    # per-tile variants selected by bits outside the tile (global bits: this rank's)
+                    assert max(op["tg"]) < nl
+                    D = 1 << len(op["tg"])
+                    out = np.zeros_like(shard)
+                    for v, (vr, vi) in enumerate(zip(op["vre"], op["vim"])):
+                        M = (np.array(vr) + 1j * np.array(vi)).reshape(D, D)
+                        m = np.ones(1 << nl, dtype=bool)
+                        for i, b in enumerate(op["sel"]):
+                            m &= ((full_j >> np.uint64(b)) & np.uint64(1)) == np.uint64((v >> i) & 1)
+                        out[m] = PI._apply_dense(shard, nl, op["tg"], M)[m]
+                    shard = out
+                elif op["type"] == 1:
                     assert max(op["tg"]) < nl
                     D = 1 << len(op["tg"])
                     M = (np.array(op["re"]) + 1j * np.array(op["im"])).reshape(D, D)

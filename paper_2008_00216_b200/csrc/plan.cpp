@@ -711,6 +711,141 @@ static std::vector<cd> diag_on_pair(const QForm &part, int a, int b, const std::
     return D;
 }
 
+// Re-express dense op o (2 qubits, maybe with variants) over selector set `sel`
+// and multiply the diagonal `part` (over o's pair + selector bits) on the left
+// (after o) or on the right (before o).
+static void fold_diag_into(FOp &o, const QForm &part, const std::vector<int> &part_sel, bool after) {
+    std::vector<int> sel = o.sel;
+    for (int x : part_sel)
+        if (std::find(sel.begin(), sel.end(), x) == sel.end()) sel.push_back(x);
+    std::sort(sel.begin(), sel.end());
+    const int nv = 1 << (int)sel.size();
+    const int a = o.tg[0], b = o.tg[1];
+    std::vector<std::vector<cd>> Mv((size_t)nv);
+    for (int v = 0; v < nv; ++v) {
+        int w = 0;
+        for (size_t q = 0; q < o.sel.size(); ++q) {
+            const size_t pos = std::find(sel.begin(), sel.end(), o.sel[q]) - sel.begin();
+            if ((v >> pos) & 1) w |= 1 << q;
+        }
+        const std::vector<cd> &M = o.Mv.empty() ? o.M : o.Mv[(size_t)w];
+        const std::vector<cd> D = diag_on_pair(part, a, b, sel, v);
+        Mv[(size_t)v] = after ? matmul(D, M, 4) : matmul(M, D, 4);
+    }
+    o.Mv = Mv;
+    o.sel = sel;
+    o.M = Mv[0];
+}
+
+// Move the parts of group diagonal sub-ops that a neighbouring 2-qubit dense
+// sub-op can carry as per-tile variants into that op: for a group bit j, the
+// terms of the diagonal on j (linear, and pairs with bits OUTSIDE the tile)
+// commute with every op that acts on j only diagonally, so they slide to the
+// previous or next dense op on j and become part of its matrix (the outside
+// bits become selectors).  Constant and outside-only terms are per-tile
+// scalars and ride on any dense op.  Terms on two in-tile bits stay.
+static void absorb_diagonals(FOp &grp, uint64_t S, int nl) {
+    std::vector<FOp> &ops = grp.subs;
+    const uint64_t sel_ok = nl >= 32 ? ~0ull : ((1ull << nl) - 1);
+    auto is_pair_dense = [](const FOp &o) { return o.type == OP_DENSE && o.tg.size() == 2; };
+    for (size_t k = 0; k < ops.size(); ++k) {
+        if (ops[k].type != OP_DIAG) continue;
+        QForm &F = ops[k].form;
+        // candidate group bits: in-tile bits with movable terms
+        std::vector<int> bits;
+        for (auto &kv : F.lin)
+            if ((S >> kv.first) & 1) bits.push_back(kv.first);
+        for (auto &kv : F.quad) {
+            const int x = kv.first.first, y = kv.first.second;
+            const bool ix = (S >> x) & 1, iy = (S >> y) & 1;
+            if (ix != iy) bits.push_back(ix ? x : y);
+        }
+        std::sort(bits.begin(), bits.end());
+        bits.erase(std::unique(bits.begin(), bits.end()), bits.end());
+        for (int j : bits) {
+            QForm part;
+            std::vector<int> psel;
+            bool ok = true;
+            if (F.lin.count(j)) part.lin[j] = F.lin[j];
+            for (auto &kv : F.quad) {
+                const int x = kv.first.first, y = kv.first.second;
+                if (x != j && y != j) continue;
+                const int other = x == j ? y : x;
+                if ((S >> other) & 1) continue;                      // in-tile partner: stays
+                if (!((sel_ok >> other) & 1)) { ok = false; break; }
+                part.quad[kv.first] = kv.second;
+                if (std::find(psel.begin(), psel.end(), other) == psel.end()) psel.push_back(other);
+            }
+            if (!ok || (part.lin.empty() && part.quad.empty())) continue;
+            // nearest ops acting on j non-diagonally, before and after
+            int prev = -1, next = -1;
+            for (int i = (int)k - 1; i >= 0; --i)
+                if ((ops[i].dmask >> j) & 1) { prev = i; break; }
+            for (size_t i = k + 1; i < ops.size(); ++i)
+                if ((ops[i].dmask >> j) & 1) { next = (int)i; break; }
+            auto nsel_after = [&](int i) {
+                std::vector<int> s2 = ops[i].sel;
+                for (int x : psel)
+                    if (std::find(s2.begin(), s2.end(), x) == s2.end()) s2.push_back(x);
+                return (int)s2.size();
+            };
+            int tgt = -1;
+            bool after = false;
+            const int cn = next >= 0 && is_pair_dense(ops[next]) ? nsel_after(next) : 99;
+            const int cp = prev >= 0 && is_pair_dense(ops[prev]) ? nsel_after(prev) : 99;
+            if (cn <= kMaxSel && cn <= cp) { tgt = next; after = false; }
+            else if (cp <= kMaxSel) { tgt = prev; after = true; }
+            if (tgt < 0) continue;
+            fold_diag_into(ops[tgt], part, psel, after);
+            for (auto &kv : part.lin) F.lin.erase(kv.first);
+            for (auto &kv : part.quad) F.quad.erase(kv.first);
+        }
+        // per-tile scalars: constant and outside-only terms onto any dense pair op in the group
+        {
+            QForm cpart;
+            std::vector<int> csel;
+            bool ok = true;
+            cpart.cst = F.cst;
+            for (auto &kv : F.lin)
+                if (!((S >> kv.first) & 1)) {
+                    cpart.lin[kv.first] = kv.second;
+                    if (!((sel_ok >> kv.first) & 1)) ok = false;
+                    if (std::find(csel.begin(), csel.end(), kv.first) == csel.end()) csel.push_back(kv.first);
+                }
+            for (auto &kv : F.quad) {
+                const int x = kv.first.first, y = kv.first.second;
+                if (((S >> x) & 1) || ((S >> y) & 1)) continue;
+                cpart.quad[kv.first] = kv.second;
+                for (int q : {x, y}) {
+                    if (!((sel_ok >> q) & 1)) ok = false;
+                    if (std::find(csel.begin(), csel.end(), q) == csel.end()) csel.push_back(q);
+                }
+            }
+            if (ok && !cpart.trivial()) {
+                int best = -1, bn = 99;
+                for (size_t i = 0; i < ops.size(); ++i) {
+                    if (!is_pair_dense(ops[i])) continue;
+                    std::vector<int> s2 = ops[i].sel;
+                    for (int x : csel)
+                        if (std::find(s2.begin(), s2.end(), x) == s2.end()) s2.push_back(x);
+                    if ((int)s2.size() < bn) { bn = (int)s2.size(); best = (int)i; }
+                }
+                if (best >= 0 && bn <= kMaxSel) {
+                    fold_diag_into(ops[best], cpart, csel, true);   // scalars commute: any side
+                    F.cst = 0;
+                    for (auto &kv : cpart.lin) F.lin.erase(kv.first);
+                    for (auto &kv : cpart.quad) F.quad.erase(kv.first);
+                }
+            }
+        }
+        ops[k].qmask = F.qubits();
+    }
+    for (size_t k = 0; k < ops.size();) {
+        if (ops[k].type == OP_DIAG && ops[k].form.trivial()) ops.erase(ops.begin() + (long)k);
+        else ++k;
+    }
+}
+
 static void merge_variant_chains(FOp &grp, uint64_t S, int nl) {
     // selectors on global (rank) bits are encoded relative to bit 32 (pass_format.h)
     const uint64_t sel_ok = nl >= 32 ? ~0ull : ((1ull << nl) - 1);
@@ -1009,7 +1144,10 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
             pass.S = S;
             if (!(opt.flags & SV_OPT_NO_VARIANTS))
                 for (FOp &o : pass.ops)
-                    if (o.type == OP_GROUP) merge_variant_chains(o, S, nl);
+                    if (o.type == OP_GROUP) {
+                        absorb_diagonals(o, S, nl);
+                        merge_variant_chains(o, S, nl);
+                    }
             plan.alg_bytes += amp_pass_bytes;
             plan.alg_flops += pass_flops_per_amp(pass.ops) * std::ldexp(1.0, nl);
         }

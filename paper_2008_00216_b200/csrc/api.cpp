@@ -27,8 +27,8 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
                              cudaStream_t st, int *kernels);
 cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off,
-                              int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st,
-                              int *kernels);
+                              int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, double flops_per_amp,
+                              cudaStream_t st, int *kernels);
 cudaError_t launch_cnot(bool c128, void *state, int c, int t, int n_local, cudaStream_t st, int *kernels);
 cudaError_t launch_bitswap(bool c128, void *state, int a, int b, int n_bits, cudaStream_t st, int *kernels);
 cudaError_t launch_norm(bool c128, const void *state, uint64_t N, double *part, int np, double *out, cudaStream_t st,
@@ -328,7 +328,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
         return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
     }
     const int enc_local = s->n_local;   // virtual: the whole buffer is addressed directly
-    Encoded enc = encode(plan, enc_local, s->c128());
+    Encoded enc = encode(plan, enc_local, s->c128(), s->virt ? 0 : (uint64_t)s->rank << s->n_local);
     // rank bits into every pass header
     for (uint32_t off : enc.pass_off) {
         StvPass *hp = (StvPass *)&enc.blob[off];
@@ -365,7 +365,8 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
             kind = hp->h == 0 ? 1 : 2;
             if (hp->grouped)
                 e = launch_group_pass(s->c128(), s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
-                                      enc_local, hp->rec_bytes, hp->tab_entries, s->stream, &kernels);
+                                      enc_local, hp->rec_bytes, hp->tab_entries, pass_flops_per_amp(ps.ops),
+                                      s->stream, &kernels);
             else
                 e = launch_tile_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->rec_bytes,
                                      hp->ntab, s->stream, &kernels);

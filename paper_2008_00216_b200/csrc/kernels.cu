@@ -808,20 +808,13 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
     constexpr bool kPacked = sizeof(C) == 8;
     for (int k = 0; k < nsub; ++k) {
         const uint2 ca = *(const uint2 *)&subs[k];         // code, arg: one LDCU.64
-        const int code = (int)ca.x;
+        const int code = (int)(ca.x & 0xffu);
         const C *M = (const C *)(mat + ca.y);
         int u2 = code - SUBC_U2;
-        if ((unsigned)(code - SUBC_U2V) < 6u) {             // per-tile variant: selector bits of the tile base
-            // selector byte c: tile-ordinal bit c, or (c & 0x80) a rank bit; unused selectors = 31 (always 0)
-            const uint32_t ctl = subs[k].ctl;
-            const uint32_t rb = (uint32_t)(rank_bits >> 32);   // rank bits sit at >= n_local >= 32 when present
-            uint32_t v = 0;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                const uint32_t c = (ctl >> (8 + 8 * q)) & 0xffu;
-                const uint32_t b = (c & 0x80u) ? (rb >> (c & 31u)) : (tord >> (c & 31u));
-                v |= (b & 1u) << q;
-            }
+        if ((unsigned)(code - SUBC_U2V) < 6u) {             // per-tile variant: selector bits of the tile ordinal
+            const uint32_t w = ca.x >> 8;
+            const uint32_t v = ((tord >> (w & 31u)) & 1u) | (((tord >> ((w >> 5) & 31u)) & 1u) << 1) |
+                               (((tord >> ((w >> 10) & 31u)) & 1u) << 2);
             M += v * 16;
             u2 = code - SUBC_U2V;
         }
@@ -1349,10 +1342,13 @@ static cudaError_t group_launch(void *state, const uint8_t *dblob, uint32_t pass
 }
 
 cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off,
-                              int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, cudaStream_t st,
-                              int *kernels) {
+                              int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, double flops_per_amp,
+                              cudaStream_t st, int *kernels) {
     const size_t esz = c128 ? 16 : 8;
-    static const int cfg = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
+    static const int cfg0 = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
+    static const double light = getenv("STV_LIGHT") ? atof(getenv("STV_LIGHT")) : 0.0;
+    // light passes (little FP work per amplitude) are HBM-latency-bound: prefetch 2 tiles ahead
+    const int cfg = (cfg0 == 0 && !c128 && flops_per_amp < light) ? 2 : cfg0;
     const int ns = cfg == 2 ? 3 : kGStagesDefault;
     const size_t smem = 1024 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)ns * (esz << S);
     const uint64_t ntiles = 1ull << (n_local - S);

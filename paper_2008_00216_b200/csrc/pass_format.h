@@ -107,25 +107,22 @@ static constexpr uint32_t swz_mask(int bit) {
 static constexpr uint32_t kSwzM0 = swz_mask(0), kSwzM1 = swz_mask(1), kSwzM2 = swz_mask(2);
 #endif
 
-// sub-op dispatch codes (dense, so the device switch is one jump table)
+// sub-op dispatch codes (low 8 bits of StvSub.code)
 #define SUBC_U1 0                // + a (0..3)
 #define SUBC_U2 4                // + pair index of (a<b): 01 02 03 12 13 23 -> 0..5
 #define SUBC_CNOT 10             // + 4 * (c + 1) + t, c = in-register control or -1
 #define SUBC_DIAG 30
-#define SUBC_U2V 31              // + pair index: U2 with per-tile variants (ctl = nsel | sel_i << (8 + 8 i))
+#define SUBC_U2V 31              // + pair index: U2 with per-tile variants (selectors in code bits 8..22)
 #define SUBC_N 37
 
-// one sub-op (read with one 64-bit uniform constant load for code + arg)
 struct alignas(16) StvSub {
-    int32_t code;              // SUBC_*
+    int32_t code;              // bits 0..7: SUBC_*; U2V: bits 8+5i (i < 3) = selector i, a bit index of the
+                               // tile ordinal t (base = pdep(t, out_mask)), 31 = unused (always 0); variant
+                               // v (matrices consecutive from arg) has bit i = selector i of this tile --
+                               // uniform per CTA, so matrix loads stay uniform (LDCU)
     uint32_t arg;              // U1/U2/U2V: matrix byte offset in the pass matrix area; DIAG: table index
     uint32_t ctl;              // CNOT: bits 0..15 raw tile offset of a control on a vector bit (0 = none);
                                //       bits 16..23 physical control bit + 1 outside the tile (0 = none)
-                               // U2V: bits 0..7 number of selector bits; byte i+1 (i < 3) = selector i: a bit
-                               //      index of the tile ordinal t (base = pdep(t, out_mask)), or 0x80 | (physical
-                               //      global bit - 32) (a bit of rank_bits); unused = 31; variant v (matrices
-                               //      consecutive from arg) has bit i = selector i of this tile -- uniform per
-                               //      CTA, so matrix loads stay LDCU
     uint32_t pad;
 };
 

@@ -746,7 +746,8 @@ static void fold_diag_into(FOp &o, const QForm &part, const std::vector<int> &pa
 // scalars and ride on any dense op.  Terms on two in-tile bits stay.
 static void absorb_diagonals(FOp &grp, uint64_t S, int nl) {
     std::vector<FOp> &ops = grp.subs;
-    const uint64_t sel_ok = nl >= 32 ? ~0ull : ((1ull << nl) - 1);
+    const uint64_t sel_ok = ~0ull;   // global-bit selectors are resolved per rank at encode time
+    (void)nl;
     auto is_pair_dense = [](const FOp &o) { return o.type == OP_DENSE && o.tg.size() == 2; };
     for (size_t k = 0; k < ops.size(); ++k) {
         if (ops[k].type != OP_DIAG) continue;
@@ -848,7 +849,8 @@ static void absorb_diagonals(FOp &grp, uint64_t S, int nl) {
 
 static void merge_variant_chains(FOp &grp, uint64_t S, int nl) {
     // selectors on global (rank) bits are encoded relative to bit 32 (pass_format.h)
-    const uint64_t sel_ok = nl >= 32 ? ~0ull : ((1ull << nl) - 1);
+    const uint64_t sel_ok = ~0ull;   // global-bit selectors are resolved per rank at encode time
+    (void)nl;
     std::vector<FOp> &ops = grp.subs;
     for (size_t i = 0; i < ops.size(); ++i) {
         if (ops[i].type != OP_DENSE || ops[i].tg.size() != 2) continue;
@@ -983,7 +985,7 @@ static void merge_variant_chains(FOp &grp, uint64_t S, int nl) {
 // Algorithmic floating-point work per amplitude: a k-qubit
 // dense op costs 8 * 2^k flops (2^k complex multiply-adds), a diagonal phase
 // one complex multiply (6), a CNOT none.
-static double pass_flops_per_amp(const std::vector<FOp> &ops) {
+double pass_flops_per_amp(const std::vector<FOp> &ops) {
     double f = 0;
     for (const FOp &o : ops) {
         if (o.type == OP_GROUP) f += pass_flops_per_amp(o.subs);
@@ -1321,7 +1323,7 @@ static std::vector<GroupTable> split_group_diag(const QForm &f, const std::vecto
     return out;
 }
 
-Encoded encode(const Plan &p, int n_local, bool c128) {
+Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
     Encoded e;
     std::vector<uint8_t> &b = e.blob;
     const size_t esz = c128 ? 16 : 8;
@@ -1407,22 +1409,29 @@ Encoded encode(const Plan &p, int n_local, bool c128) {
                             }
                             if (so.Mv.empty()) sub.arg = put_matrix(so.M);
                             else {
-                                sub.arg = put_matrix(so.Mv[0]);
-                                for (size_t v = 1; v < so.Mv.size(); ++v) put_matrix(so.Mv[v]);
-                                // selector q as a bit of the tile ordinal t (base = pdep(t, out_mask)),
-                                // or 0x80 | physical bit for a global (rank) bit: both uniform per CTA tile
-                                sub.ctl = (uint32_t)so.sel.size();
+                                // selectors on local bits become bits of the tile ordinal t (base =
+                                // pdep(t, out_mask)); global-bit selectors are fixed for this rank
+                                std::vector<int> tsel;                 // tile-ordinal bit per kept selector
+                                std::vector<size_t> keep;
+                                uint32_t vfix = 0;
+                                for (size_t q = 0; q < so.sel.size(); ++q) {
+                                    const int p = so.sel[q];
+                                    if (p < n_local) {
+                                        tsel.push_back(__builtin_popcountll(hd.out_mask & ((1ull << p) - 1)));
+                                        keep.push_back(q);
+                                    } else if ((rank_bits >> p) & 1) vfix |= 1u << q;
+                                }
+                                for (size_t v = 0; v < ((size_t)1 << keep.size()); ++v) {
+                                    uint32_t full = vfix;
+                                    for (size_t q = 0; q < keep.size(); ++q)
+                                        if ((v >> q) & 1) full |= 1u << keep[q];
+                                    const uint32_t off = put_matrix(so.Mv[full]);
+                                    if (v == 0) sub.arg = off;
+                                }
+                                if (keep.empty()) sub.code = SUBC_U2 + (sub.code - SUBC_U2V);
                                 for (size_t q = 0; q < 3; ++q) {
-                                    uint32_t code = 31;                       // unused: tile-ordinal bit 31 = 0
-                                    if (q < so.sel.size()) {
-                                        const int p = so.sel[q];
-                                        if (p < n_local) code = (uint32_t)__builtin_popcountll(hd.out_mask & ((1ull << p) - 1));
-                                        else {
-                                            if (p < 32) throw std::runtime_error("rank selector below bit 32");
-                                            code = 0x80u | (uint32_t)(p - 32);
-                                        }
-                                    }
-                                    sub.ctl |= code << (8 + 8 * q);
+                                    const uint32_t c = q < tsel.size() ? (uint32_t)tsel[q] : 31u;   // 31: always 0
+                                    sub.code |= (int32_t)(c << (8 + 5 * q));
                                 }
                             }
                         } else if (so.type == OP_CNOT) {

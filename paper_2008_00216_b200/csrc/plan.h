@@ -128,9 +128,14 @@ struct Encoded {
     std::vector<uint8_t> blob;
     std::vector<uint32_t> pass_off;   // byte offset of each pass's PassDesc
 };
-Encoded encode(const Plan &p, int n_local, bool c128);
+// rank_bits: this rank's global bit values (physical positions >= n_local); selectors of
+// per-tile variant ops on global bits are resolved here.
+Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits = 0);
 
 std::string plan_to_json(const Plan &p);
+
+// Algorithmic floating-point work per amplitude of a pass's ops.
+double pass_flops_per_amp(const std::vector<FOp> &ops);
 
 // Exact conversion helpers.
 uint64_t turns_of_angle(double rad);   // rad/(2 pi) * 2^64, rounded, mod 2^64

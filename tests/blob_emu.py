@@ -150,7 +150,7 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
     assert len(set(g.sw_off[l] for l in range(16))) == 16
     for k in range(g.nsub):
         sb = _at(blob, Sub, po + g.sub_off + 16 * k)
-        c = sb.code
+        c = sb.code & 0xFF
         ctl_raw, ctl_phys = sb.ctl & 0xFFFF, (sb.ctl >> 16) - 1
         if c < 4:
             psi = PI._apply_dense(psi, n, [G[c]], _matrix(blob, po + P.mat_off + sb.arg, 2, c128))
@@ -159,21 +159,17 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
             psi = PI._apply_dense(psi, n, [G[a], G[b]], _matrix(blob, po + P.mat_off + sb.arg, 4, c128))
         elif 31 <= c < 37:
             a, b = U2_PAIRS[c - 31]
-            nsel = sb.ctl & 0xFF
-            outbits = [b for b in range(64) if (P.out_mask >> b) & 1]
+            outbits = [b_ for b_ in range(64) if (P.out_mask >> b_) & 1]
             sel = []
             for i in range(3):
-                code = (sb.ctl >> (8 + 8 * i)) & 0xFF
-                if i >= nsel:
-                    assert code == 31                          # unused selector: tile-ordinal bit 31
-                    continue
-                # tile-ordinal bit index (base = pdep(t, out_mask)) or 0x80 | (global bit - 32)
-                sel.append(32 + (code & 0x7F) if code & 0x80 else outbits[code])
+                code = (sb.code >> (8 + 5 * i)) & 31
+                if code != 31:
+                    sel.append(outbits[code])                  # tile-ordinal bit -> physical bit
             assert all(s_ not in pos2phys for s_ in sel)      # selectors are outside the tile
             esz = 16 if c128 else 8
             jj = np.arange(1 << n)
             out = np.zeros_like(psi)
-            for v in range(1 << nsel):
+            for v in range(1 << len(sel)):
                 M = _matrix(blob, po + P.mat_off + sb.arg + v * 16 * esz, 4, c128)
                 m = np.ones(1 << n, dtype=bool)
                 for i, s_ in enumerate(sel):

@@ -24,12 +24,18 @@ def rand_u(d):
 
 
 def circuit(m, diag, qs=(4, 5, 6, 7)):
+    """diag: None; 'out' = controlled phase to a qubit outside the tile (folds into per-tile
+    variant matrices); 'v' = to an in-tile qubit outside the group (a per-tile table sub-op)."""
     pairs = [(qs[0], qs[1]), (qs[1], qs[2]), (qs[2], qs[3]), (qs[3], qs[0])]
     g = []
+    if diag == "v":   # dense gates pull the partner qubits into the tile (V-bits of the group)
+        g += [("h", (9,), ()), ("h", (10,), ()), ("h", (11,), ())]
     for i in range(m):
         g.append(("u2", pairs[i % 4], rand_u(4)))
-        if diag:
+        if diag == "out":
             g.append(("cphase", (pairs[i % 4][0], 20 + i % 5), ((1, 6),)))
+        elif diag == "v":
+            g.append(("cphase", (pairs[i % 4][0], 9 + i % 3), ((1, 6),)))
     return g
 
 
@@ -44,14 +50,14 @@ def run(gates, reps=3):
 
 
 out = {}
-for diag in (False, True):
+for diag in (None, "out", "v"):
     pts = {}
     for m in (4, 16, 48):
         ms, npass, ops = run(circuit(m, diag))
         pts[m] = ms
-        out[f"{'u2d' if diag else 'u2'}_m{m}"] = {"ms": ms, "passes": npass, "ops": ops}
+        out[f"u2{diag or ''}_m{m}"] = {"ms": ms, "passes": npass, "ops": ops}
     per = (pts[48] - pts[16]) / 32
     fma_ms = 8 * 2 * 2 ** n / (148 * 4 * 32 * 1.965e9) * 1e3   # 8 FFMA2/amp, 2 cycles per warp FFMA2
-    out[f"{'u2d' if diag else 'u2'}_per_u2_ms"] = per
-    out[f"{'u2d' if diag else 'u2'}_fma_fraction"] = fma_ms / per
+    out[f"u2{diag or ''}_per_u2_ms"] = per
+    out[f"u2{diag or ''}_fma_fraction"] = fma_ms / per
 print(json.dumps(out, indent=1))

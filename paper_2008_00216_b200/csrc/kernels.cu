@@ -637,14 +637,23 @@ __device__ __forceinline__ C cmul(C a, C b) {
     return r;
 }
 
-// exp(2 pi i ph / 2^64) in double precision, rounded once to the state's type
+// exp(2 pi i ph / 2^64): complex128 in double precision; complex64 from the top
+// 32 bits of the turn count in single precision (argument quantum 2^-31 turn,
+// |error| < 2e-7 rad, far inside the complex64 bars)
 template <typename C>
 __device__ __forceinline__ C unit_phase(uint64_t ph) {
-    double s, c;
-    sincospi((double)(int64_t)ph * 1.0842021724855044340074528008699e-19, &s, &c);   // 2^-63
     C r;
-    r.x = (decltype(r.x))c;
-    r.y = (decltype(r.y))s;
+    if constexpr (sizeof(C) == 8) {
+        float s, c;
+        sincospif((float)(int32_t)(uint32_t)(ph >> 32) * 4.656612873077393e-10f, &s, &c);   // 2^-31
+        r.x = c;
+        r.y = s;
+    } else {
+        double s, c;
+        sincospi((double)(int64_t)ph * 1.0842021724855044340074528008699e-19, &s, &c);   // 2^-63
+        r.x = c;
+        r.y = s;
+    }
     return r;
 }
 

@@ -783,7 +783,8 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
         const StvDTab &d = tabs[t];
         const uint64_t *stat = (const uint64_t *)(grec + d.stat_off);
         const StvTerm *tm = (const StvTerm *)((const uint8_t *)P + d.term_off);
-        const int ne = 16 << d.m, nterm = d.nterm;
+        const int lb4 = d.half ? 3 : 4, stride = d.half ? STV_TAB_STRIDE_H : STV_TAB_STRIDE;
+        const int ne = (1 << lb4) << d.m, nterm = d.nterm;
         // per-tile coefficients: lane b < 4 + m sums the terms on index bit b, lane 31 the constant
         uint64_t lam = 0;
         for (int i = 0; i < nterm; ++i) {
@@ -802,8 +803,20 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
 #pragma unroll
             for (int b = 0; b < 7; ++b)
                 if ((e >> b) & 1) ph += lb[b];
-            tables[d.ent_off + (uint32_t)(e >> 4) * STV_TAB_STRIDE + (e & 15)] = unit_phase<C>(ph);
+            tables[d.ent_off + (uint32_t)(e >> lb4) * stride + (e & ((1 << lb4) - 1))] = unit_phase<C>(ph);
         }
+    }
+}
+
+// half-table diagonal: amplitudes with local bit J set times row[l without bit J]
+template <int J, typename C>
+__device__ __forceinline__ void g_diagh(C (&x)[16], const C *__restrict__ row) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (!(l & (1 << J))) continue;
+        const int c = ((l >> (J + 1)) << J) | (l & ((1 << J) - 1));
+        if constexpr (sizeof(C) == 8) *(float2 *)&x[l] = cmul1(*(const float2 *)&row[c], *(float2 *)&x[l]);
+        else x[l] = cmul(x[l], row[c]);
     }
 }
 
@@ -864,6 +877,22 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
                 } else {
 #pragma unroll
                     for (int l = 0; l < 16; ++l) x[i][l] = cmul(x[i][l], row[l]);
+                }
+            }
+        } else if ((unsigned)(code - SUBC_DIAGH) < 4u) {   // half table on local bit j
+            const StvDTab &d = tabs[ca.y];
+            const uint32_t eo = d.ent_off;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                uint32_t r = 0;
+#pragma unroll
+                for (int q = 0; q < STV_MAX_VBITS_H; ++q) r |= ((braw[i] & d.vraw[q]) ? 1u : 0u) << q;
+                const typename TabEnt<C>::T *row = tables + eo + r * STV_TAB_STRIDE_H;
+                switch (code - SUBC_DIAGH) {
+                case 0: g_diagh<0>(x[i], row); break;
+                case 1: g_diagh<1>(x[i], row); break;
+                case 2: g_diagh<2>(x[i], row); break;
+                default: g_diagh<3>(x[i], row); break;
                 }
             }
         } else {

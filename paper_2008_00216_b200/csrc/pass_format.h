@@ -21,7 +21,8 @@
 
 #define STV_GROUP_BITS 4
 #define STV_MAX_TABLES 32
-#define STV_MAX_VBITS 3          // in-tile bits outside the group a diag table may index
+#define STV_MAX_VBITS 3          // in-tile bits outside the group a full diag table may index
+#define STV_MAX_VBITS_H 6        // ... a half diag table may index
 
 #define STV_MAX_TILE_BITS 14
 #define STV_MAX_K 4
@@ -113,7 +114,8 @@ static constexpr uint32_t kSwzM0 = swz_mask(0), kSwzM1 = swz_mask(1), kSwzM2 = s
 #define SUBC_CNOT 10             // + 4 * (c + 1) + t, c = in-register control or -1
 #define SUBC_DIAG 30
 #define SUBC_U2V 31              // + pair index: U2 with per-tile variants (selectors in code bits 8..22)
-#define SUBC_N 37
+#define SUBC_DIAGH 37            // + j: half-table diagonal on local bit j (arg = table index)
+#define SUBC_N 41
 
 struct alignas(16) StvSub {
     int32_t code;              // bits 0..7: SUBC_*; U2V: bits 8+5i (i < 3) = selector i, a bit index of the
@@ -144,12 +146,19 @@ struct alignas(16) StvGroup {
 // Entries live in shared memory at ent_off + r * STV_TAB_STRIDE + l (rows padded against
 // bank conflicts between lanes with different r).
 struct alignas(16) StvDTab {
-    uint32_t stat_off;         // byte offset (pass record) of uint64 stat[16 << m]
+    uint32_t stat_off;         // byte offset (pass record) of uint64 stat[(half ? 8 : 16) << m]
     uint32_t term_off;         // byte offset of StvTerm[nterm]
     int32_t nterm;
     int32_t m;
     uint32_t ent_off;          // first entry in the shared-memory table area
-    uint16_t vraw[STV_MAX_VBITS];   // raw tile offsets of the V-bits (0 for unused)
-    uint16_t pad;
+    int32_t half;              // 0: full table over l (16) x r; 1: half table (below)
+    uint16_t vraw[STV_MAX_VBITS_H];   // raw tile offsets of the V-bits (0 for unused)
+    uint16_t pad[2];
 };
+// Half table (code SUBC_DIAGH + j): every term of the diagonal contains local bit j,
+// so amplitudes with l_j = 0 are unchanged; the table is over (the 3 other local
+// bits in ascending order) x r, rows of 8 entries at stride STV_TAB_STRIDE_H, and
+// its per-tile terms are all constants (a == -1 or <= -2).  QFT-like diagonals
+// (one target coupled to many qubits) take m <= STV_MAX_VBITS_H V-bits this way.
+#define STV_TAB_STRIDE_H 9
 #define STV_TAB_STRIDE 17        // entries per table row: 16 + 1 pad (rows of different lanes hit different banks)

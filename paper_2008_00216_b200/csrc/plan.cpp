@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <sstream>
 
 namespace stv {
@@ -537,7 +538,27 @@ struct OpsEval {
 // Shared-memory bytes (pass record + table area) of a group diagonal sub-op:
 // the greedy split of its terms into tables of <= STV_MAX_VBITS V-bits
 // (vmask = in-tile qubits outside the group; mirrors split_group_diag).
-static size_t diag_table_bytes(const QForm &f, uint64_t vmask, int amp_bytes, int *ntab, size_t *tab_smem) {
+static size_t diag_table_bytes(const QForm &f, uint64_t vmask, uint64_t T, int amp_bytes, int *ntab,
+                               size_t *tab_smem) {
+    // one half table when every term contains one group bit j (mirrors half_table)
+    if (f.cst == 0)
+        for (uint64_t tt = T; tt; tt &= tt - 1) {
+            const int j = __builtin_ctzll(tt);
+            bool ok = true;
+            uint64_t vb = 0;
+            for (auto &kv : f.lin) ok &= kv.first == j;
+            for (auto &kv : f.quad) {
+                const int x = kv.first.first, y = kv.first.second;
+                if (x != j && y != j) { ok = false; break; }
+                vb |= vmask & (1ull << (x == j ? y : x));
+            }
+            const int m = __builtin_popcountll(vb);
+            if (!ok || m > STV_MAX_VBITS_H) continue;
+            *ntab = 1;
+            *tab_smem += (size_t)(STV_TAB_STRIDE_H * amp_bytes) << m;
+            return sizeof(StvDTab) + sizeof(StvSub) + ((size_t)64 << m) + 32 +
+                   sizeof(StvTerm) * (f.lin.size() + f.quad.size());
+        }
     std::vector<uint64_t> sets;
     auto place = [&](uint64_t need) {
         for (uint64_t &u : sets)
@@ -580,7 +601,7 @@ static void tally(OpsEval &ev, int amp_bytes, uint64_t S = 0) {
             if (o.type == OP_DIAG) {
                 // per-tile tables over the group bits + V-bits, split as the encoder does
                 int ntb = 0;
-                ev.rec += diag_table_bytes(o.form, S & ~grp.T, amp_bytes, &ntb, &ev.tab);
+                ev.rec += diag_table_bytes(o.form, S & ~grp.T, grp.T, amp_bytes, &ntb, &ev.tab);
                 ev.ntab += ntb;
             }
         }
@@ -1016,8 +1037,10 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
     // CTAs per SM when the tiles allow it
     const size_t tile_b = (size_t)amp_bytes << opt.tile_bits;
     const size_t rec_limit = std::min(kMaxRecBytes, (size_t)STV_REC_PARAM_BYTES);
+    // (diagonal-heavy passes, e.g. the QFT of c3, trade the third CTA for full-size tiles:
+    // a 16 KB table area measured best on c3, 306 vs 506 ms/circuit at 8 KB)
     size_t tab_limit = 16 * 1024;
-    if (2 * tile_b + 2048 < 74 * 1024) tab_limit = std::max((size_t)4096, 74 * 1024 - 2 * tile_b - 2048);
+    if (const char *e = getenv("STV_TAB_LIMIT")) tab_limit = (size_t)atoi(e);
 
     while (true) {
         while (first < G && done[first]) ++first;
@@ -1258,14 +1281,71 @@ static std::vector<int> vector_bit_order(const std::vector<int> &pos, int S, boo
 
 // One per-tile phase table of a group diagonal sub-op (pass_format.h StvDTab).
 struct GroupTable {
-    std::vector<int> vpos;           // tile positions of its V-bits (<= STV_MAX_VBITS)
-    std::vector<uint64_t> stat;      // static phases, index l | r << 4
+    std::vector<int> vpos;           // tile positions of its V-bits (<= STV_MAX_VBITS, or _H for half)
+    std::vector<uint64_t> stat;      // static phases, index l | r << 4 (half: l' | r << 3)
     std::vector<StvTerm> terms;      // per-tile terms
+    int half = -1;                   // >= 0: half table on local bit `half`
 };
+
+// A diagonal whose every term contains local bit j (no constant) and that has at
+// most STV_MAX_VBITS_H V-bits: one half table (pass_format.h).
+static bool half_table(const QForm &f, const std::vector<int> &pos, const int *loc, GroupTable &gt) {
+    if (f.cst != 0) return false;
+    auto local = [&](int phys) -> int {
+        if (loc[phys] < 0) return -1;
+        auto it = std::find(pos.begin(), pos.end(), loc[phys]);
+        return it == pos.end() ? -1 : (int)(it - pos.begin());
+    };
+    auto is_v = [&](int phys) { return loc[phys] >= 0 && local(phys) < 0; };
+    for (int j = 0; j < 4; ++j) {
+        const int pj = [&] { for (auto &kv : f.lin) if (local(kv.first) == j) return kv.first;
+                             for (auto &kv : f.quad) { if (local(kv.first.first) == j) return kv.first.first;
+                                                       if (local(kv.first.second) == j) return kv.first.second; }
+                             return -1; }();
+        if (pj < 0) continue;
+        bool ok = true;
+        std::vector<int> vp;
+        for (auto &kv : f.lin) ok &= kv.first == pj;
+        for (auto &kv : f.quad) {
+            const int x = kv.first.first, y = kv.first.second;
+            if (x != pj && y != pj) { ok = false; break; }
+            const int o = x == pj ? y : x;
+            if (is_v(o) && std::find(vp.begin(), vp.end(), loc[o]) == vp.end()) vp.push_back(loc[o]);
+        }
+        if (!ok || (int)vp.size() > STV_MAX_VBITS_H) continue;
+        std::sort(vp.begin(), vp.end());
+        gt.vpos = vp;
+        gt.half = j;
+        const int m = (int)vp.size();
+        gt.stat.assign((size_t)8 << m, 0);
+        // index bits: 0..2 = the other local bits ascending, 3.. = V-bits
+        auto ibit = [&](int phys) -> int {
+            const int l = local(phys);
+            if (l >= 0) return l < j ? l : l - 1;
+            return 3 + (int)(std::find(vp.begin(), vp.end(), loc[phys]) - vp.begin());
+        };
+        for (auto &kv : f.lin)
+            for (auto &e : gt.stat) e += kv.second;                 // l_j = 1 for every entry
+        for (auto &kv : f.quad) {
+            const int x = kv.first.first, y = kv.first.second;
+            const int o = x == pj ? y : x;
+            if (loc[o] < 0) { gt.terms.push_back({-1, o, kv.second}); continue; }   // per-tile constant
+            const int b = ibit(o);
+            for (size_t e = 0; e < gt.stat.size(); ++e)
+                if ((e >> b) & 1) gt.stat[e] += kv.second;
+        }
+        return true;
+    }
+    return false;
+}
 
 // Split a group's diagonal form into tables of <= STV_MAX_VBITS V-bits each
 // (diagonal terms commute and add, so the split is exact).
 static std::vector<GroupTable> split_group_diag(const QForm &f, const std::vector<int> &pos, const int *loc) {
+    {
+        GroupTable gt;
+        if (half_table(f, pos, loc, gt)) return {gt};
+    }
     struct Item { int x, y; uint64_t ang; };   // y = -1: linear term on x
     std::vector<Item> items;
     for (auto &kv : f.lin) items.push_back({kv.first, -1, kv.second});
@@ -1478,6 +1558,7 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         StvDTab d;
                         std::memset(&d, 0, sizeof(d));
                         d.m = (int)gt.vpos.size();
+                        d.half = gt.half >= 0 ? 1 : 0;
                         for (int v = 0; v < d.m; ++v) d.vraw[v] = (uint16_t)(1u << gt.vpos[v]);
                         d.nterm = (int)gt.terms.size();
                         align(b, 16);
@@ -1487,10 +1568,10 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         d.term_off = (uint32_t)(b.size() - at);
                         put(b, gt.terms.data(), gt.terms.size() * sizeof(StvTerm));
                         d.ent_off = ent;
-                        ent += (uint32_t)(STV_TAB_STRIDE << d.m);
+                        ent += (uint32_t)((d.half ? STV_TAB_STRIDE_H : STV_TAB_STRIDE) << d.m);
                         StvSub sub;
                         std::memset(&sub, 0, sizeof(sub));
-                        sub.code = SUBC_DIAG;
+                        sub.code = d.half ? SUBC_DIAGH + gt.half : SUBC_DIAG;
                         sub.arg = (uint32_t)tabs.size();
                         tabs.push_back(d);
                         out.push_back(sub);

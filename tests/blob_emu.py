@@ -43,7 +43,8 @@ class Group(ct.Structure):
 
 class DTab(ct.Structure):
     _fields_ = [("stat_off", ct.c_uint32), ("term_off", ct.c_uint32), ("nterm", ct.c_int32), ("m", ct.c_int32),
-                ("ent_off", ct.c_uint32), ("vraw", ct.c_uint16 * 3), ("pad", ct.c_uint16), ("pad2", ct.c_uint32)]
+                ("ent_off", ct.c_uint32), ("half", ct.c_int32), ("vraw", ct.c_uint16 * 6), ("pad", ct.c_uint16 * 2),
+                ("pad2", ct.c_uint32 * 2)]
 
 
 class Pass(ct.Structure):
@@ -56,7 +57,7 @@ class Pass(ct.Structure):
 
 
 assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
-assert ct.sizeof(Group) == 176 and ct.sizeof(DTab) == 32
+assert ct.sizeof(Group) == 176 and ct.sizeof(DTab) == 48
 
 U2_PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
 
@@ -192,6 +193,28 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
                 psi = PI._cnot(psi, n, ctl[0], G[t])
             else:
                 psi = psi[np.arange(1 << n) ^ (1 << G[t])]
+        elif 37 <= c < 41:
+            jb = c - 37                                       # half table on local bit jb
+            d = _at(blob, DTab, po + P.tab_off + ct.sizeof(DTab) * sb.arg)
+            assert d.half == 1
+            vq = [d.vraw[i].bit_length() - 1 for i in range(d.m)]
+            assert all(q not in [g.tpos[i] for i in range(4)] for q in vq)
+            stat = np.frombuffer(blob, dtype=np.uint64, count=8 << d.m, offset=po + d.stat_off)
+            e = np.zeros(1 << n, dtype=np.uint64)
+            others = [k2 for k2 in range(4) if k2 != jb]
+            for i, k2 in enumerate(others):
+                e |= _bits(j, G[k2]) << np.uint64(i)
+            for i, q in enumerate(vq):
+                e |= _bits(j, pos2phys[q]) << np.uint64(3 + i)
+            ph = stat[e.astype(np.int64)].copy()
+            for t in _terms(blob, po + d.term_off, d.nterm):
+                assert t.a < 0                                # per-tile terms are constants
+                on = _bits(j, t.b)
+                if t.a <= -2:
+                    on = on * _bits(j, -2 - t.a)
+                ph += on * np.uint64(t.ang)
+            ph = ph * _bits(j, G[jb])                          # amplitudes with l_j = 0 unchanged
+            psi = _phase_apply(psi, ph)
         else:
             assert c == 30
             d = _at(blob, DTab, po + P.tab_off + ct.sizeof(DTab) * sb.arg)

@@ -156,6 +156,20 @@ sv_status sv_read_state(sv_state *s, uint64_t first, uint64_t count, void *out);
  * (deterministic). */
 sv_status sv_norm(sv_state *s, double *out);
 
+/* Measurement sampling ("Simulating
+ * measurements is then straightforward"; SPEC S:L286-292 sample_measurement).
+ *   out[s] (s < shots) = logical basis index j drawn with probability |a_j|^2 / sum |a|^2.
+ * Draws: u_s = (splitmix64(seed + s) >> 11) * 2^-53 (counter-based, so the result is
+ * deterministic given seed); the sample is the first index, in the state's STORAGE order
+ * (physical order through the frame, rank-major across GPUs), at which the fp64 inclusive
+ * cumulative sum of |a|^2 exceeds u_s * total; it is returned as a logical index.
+ * Cumulative sums: 4096-amplitude chunks, each summed as 32 lanes x 128 consecutive
+ * amplitudes then a fixed warp tree, chunk totals prefix-summed on the host in order.
+ * out: caller host memory of `shots` uint64.  shots == 0 is a no-op.
+ * Errors: SV_ERR_INVALID_ARG (NULL out with shots > 0, total mass <= 0 or not finite).
+ * Distributed: collective; every rank returns all samples. */
+sv_status sv_sample(sv_state *s, uint64_t seed, size_t shots, uint64_t *out);
+
 typedef struct {
     double plan_ms;        /* host planning time of the last sv_apply_circuit      */
     double run_ms;         /* device time of all passes (events on the stream)     */

@@ -32,7 +32,7 @@ PASS_KINDS = ["tile", "tile_low", "tile_high", "diag", "cnot", "remap", "init", 
 
 # every entry point declared in include/sv.h
 EXPORTS = ["sv_create", "sv_wrap", "sv_create_dist", "sv_create_virtual", "sv_set_basis",
-           "sv_set_uniform", "sv_apply_circuit", "sv_get_amplitudes", "sv_read_state", "sv_norm",
+           "sv_set_uniform", "sv_apply_circuit", "sv_get_amplitudes", "sv_read_state", "sv_norm", "sv_sample",
            "sv_last_run_stats", "sv_get_frame", "sv_plan_json", "sv_plan_blob", "sv_remap_peers", "sv_destroy",
            "sv_last_error", "sv_version"]
 
@@ -86,6 +86,7 @@ def lib():
         L.sv_get_amplitudes.argtypes = [vp, ctypes.POINTER(u64), u64, sz, vp]
         L.sv_read_state.argtypes = [vp, u64, u64, vp]
         L.sv_norm.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
+        L.sv_sample.argtypes = [vp, u64, sz, ctypes.POINTER(u64)]
         L.sv_last_run_stats.argtypes = [vp, ctypes.POINTER(Stats)]
         L.sv_get_frame.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(u64)]
         L.sv_plan_json.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(Gate), sz,
@@ -280,6 +281,12 @@ class State:
         v = ctypes.c_double()
         _check(lib().sv_norm(self._h, ctypes.byref(v)))
         return v.value
+
+    def sample(self, shots: int, seed: int = 0):
+        """Logical basis indices drawn from |a|^2 (include/sv.h sv_sample), uint64 numpy array."""
+        out = np.zeros(max(1, shots), dtype=np.uint64)
+        _check(lib().sv_sample(self._h, seed, shots, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+        return out[:shots]
 
     def stats(self) -> dict:
         s = Stats()

@@ -26,6 +26,10 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
                              uint32_t rec_bytes, int ntab, cudaStream_t st, int *kernels);
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
                              cudaStream_t st, int *kernels);
+cudaError_t launch_sample_mass(bool c128, const void *state, uint64_t N, double *mass, uint64_t nchunks,
+                               cudaStream_t st, int *kernels);
+cudaError_t launch_sample_find(bool c128, const void *state, uint64_t N, const uint64_t *chunk, const double *res,
+                               uint64_t nshots, uint64_t *out, cudaStream_t st, int *kernels);
 cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off,
                               int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, double flops_per_amp,
                               cudaStream_t st, int *kernels);
@@ -499,6 +503,112 @@ sv_status sv_norm(sv_state *s, double *out) {
     }
     CK(s, cudaMemcpyAsync(out, s->dnorm + kNormParts, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
     CK(s, cudaStreamSynchronize(s->stream));
+    return SV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sv_sample (include/sv.h): chunk masses on the device, host prefix sums and shot
+// routing, one warp per shot on the device, frame mapping on the host.
+// ---------------------------------------------------------------------------
+static uint64_t splitmix_out(uint64_t seed, uint64_t s) {   // (s+1)-th output of splitmix64(seed)
+    uint64_t z = seed + (s + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+sv_status sv_sample(sv_state *s, uint64_t seed, size_t shots, uint64_t *out) {
+    sv_status st = check_state(s);
+    if (st) return st;
+    if (!shots) return SV_OK;
+    if (!out) return fail(SV_ERR_INVALID_ARG, "out is NULL");
+    const uint64_t N = s->nloc_amps();
+    const uint64_t nch = (N + 4095) / 4096;
+    double *dmass = nullptr, *dres = nullptr;
+    uint64_t *dchunk = nullptr, *dout = nullptr;
+    auto cleanup = [&]() {
+        cudaFree(dmass); cudaFree(dres); cudaFree(dchunk); cudaFree(dout);
+    };
+    if (cudaMalloc(&dmass, nch * sizeof(double)) != cudaSuccess) { cleanup(); return fail(SV_ERR_OUT_OF_MEMORY, "sample"); }
+    int k = 0;
+    cudaError_t e = launch_sample_mass(s->c128(), s->buf, N, dmass, nch, s->stream, &k);
+    std::vector<double> mass(nch), pre(nch + 1, 0.0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(mass.data(), dmass, nch * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample mass"); }
+    for (uint64_t c = 0; c < nch; ++c) pre[c + 1] = pre[c] + mass[c];
+    // per-rank masses (distributed: every rank needs all of them)
+    std::vector<double> rmass((size_t)s->world, 0.0);
+    rmass[(size_t)s->rank] = pre[nch];
+    if (s->world > 1) {
+        double *d = nullptr;
+        cudaMalloc(&d, s->world * sizeof(double));
+        cudaMemcpyAsync(d, rmass.data(), s->world * sizeof(double), cudaMemcpyHostToDevice, s->stream);
+        int r = g_nccl.allReduce(d, d, (size_t)s->world, ncclFloat64, ncclSum, s->comm, s->stream);
+        cudaMemcpyAsync(rmass.data(), d, s->world * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+        cudaStreamSynchronize(s->stream);
+        cudaFree(d);
+        if (r) { cleanup(); s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (sample mass)"); }
+    }
+    std::vector<double> rpre((size_t)s->world + 1, 0.0);
+    for (int r = 0; r < s->world; ++r) rpre[(size_t)r + 1] = rpre[(size_t)r] + rmass[(size_t)r];
+    const double total = rpre[(size_t)s->world];
+    if (!(total > 0) || !std::isfinite(total)) { cleanup(); return fail(SV_ERR_INVALID_ARG, "state has no probability mass"); }
+    // route the shots: owner rank, chunk, residual
+    std::vector<uint64_t> mine, hchunk;
+    std::vector<double> hres;
+    for (size_t sh = 0; sh < shots; ++sh) {
+        const double u = (double)(splitmix_out(seed, sh) >> 11) * 0x1.0p-53;
+        const double target = u * total;
+        int owner = s->world - 1;
+        for (int r = 0; r < s->world; ++r)
+            if (target < rpre[(size_t)r + 1] && rmass[(size_t)r] > 0) { owner = r; break; }
+        while (owner > 0 && rmass[(size_t)owner] <= 0) --owner;
+        if (owner != s->rank) continue;
+        const double t = target - rpre[(size_t)owner];
+        // first chunk whose inclusive prefix exceeds t (clamped to the last chunk with mass)
+        uint64_t c = (uint64_t)(std::upper_bound(pre.begin() + 1, pre.end(), t) - (pre.begin() + 1));
+        if (c >= nch) c = nch - 1;
+        while (c > 0 && mass[c] <= 0) --c;
+        mine.push_back(sh);
+        hchunk.push_back(c);
+        hres.push_back(t - pre[c]);
+    }
+    std::vector<uint64_t> phys(mine.size());
+    if (!mine.empty()) {
+        const size_t m = mine.size();
+        if (cudaMalloc(&dchunk, m * 8) || cudaMalloc(&dres, m * 8) || cudaMalloc(&dout, m * 8)) {
+            cleanup();
+            return fail(SV_ERR_OUT_OF_MEMORY, "sample");
+        }
+        e = cudaMemcpyAsync(dchunk, hchunk.data(), m * 8, cudaMemcpyHostToDevice, s->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dres, hres.data(), m * 8, cudaMemcpyHostToDevice, s->stream);
+        if (e == cudaSuccess) e = launch_sample_find(s->c128(), s->buf, N, dchunk, dres, m, dout, s->stream, &k);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(phys.data(), dout, m * 8, cudaMemcpyDeviceToHost, s->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample find"); }
+    }
+    // physical -> logical through the frame
+    std::vector<uint64_t> res(shots, 0);
+    const uint64_t rb = s->virt ? 0 : (uint64_t)s->rank << s->n_local;
+    for (size_t i = 0; i < mine.size(); ++i) {
+        const uint64_t Q = (phys[i] | rb) ^ s->xmask;
+        uint64_t j = 0;
+        for (int q = 0; q < s->n; ++q) j |= ((Q >> s->perm[q]) & 1ull) << q;
+        res[mine[i]] = j;
+    }
+    if (s->world > 1) {   // every rank returns all samples: sum of the per-rank arrays
+        uint64_t *d = nullptr;
+        cudaMalloc(&d, shots * 8);
+        cudaMemcpyAsync(d, res.data(), shots * 8, cudaMemcpyHostToDevice, s->stream);
+        int r = g_nccl.allReduce(d, d, shots, 5 /*ncclUint64*/, ncclSum, s->comm, s->stream);
+        cudaMemcpyAsync(res.data(), d, shots * 8, cudaMemcpyDeviceToHost, s->stream);
+        cudaStreamSynchronize(s->stream);
+        cudaFree(d);
+        if (r) { cleanup(); s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (samples)"); }
+    }
+    std::memcpy(out, res.data(), shots * 8);
+    cleanup();
     return SV_OK;
 }
 

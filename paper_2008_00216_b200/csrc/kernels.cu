@@ -19,6 +19,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <cstring>
+#include <algorithm>
 
 #include "pass_format.h"
 
@@ -1266,6 +1267,95 @@ __global__ void __launch_bounds__(STV_THREADS) k_norm_final(const double *part, 
         __syncthreads();
     }
     if (threadIdx.x == 0) *out = red[0];
+}
+
+// ---------------------------------------------------------------------------
+// measurement sampling (NEXT #3): chunk masses, then one warp per shot finds the
+// first index whose cumulative |a|^2 exceeds the shot's residual in its chunk.
+// Both kernels sum a chunk in the same order (lane-contiguous 128 amplitudes, then
+// a fixed shuffle tree), so chunk totals and in-chunk scans agree bit for bit.
+// ---------------------------------------------------------------------------
+constexpr int kSampChunk = 4096;
+static int num_sms();
+
+template <typename C>
+__device__ __forceinline__ double amp2(const C *__restrict__ st, uint64_t i, uint64_t N) {
+    if (i >= N) return 0.0;
+    const C a = st[i];
+    return (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+}
+
+template <typename C>
+__global__ void __launch_bounds__(256) k_sample_mass(const C *__restrict__ st, uint64_t N, uint64_t nchunks,
+                                                     double *__restrict__ mass) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t per = kSampChunk / 32;
+    for (uint64_t c = blockIdx.x * 8ull + (threadIdx.x >> 5); c < nchunks; c += gridDim.x * 8ull) {
+        const uint64_t b = c * kSampChunk + lane * per;
+        double acc = 0;
+        for (uint64_t k = 0; k < per; ++k) acc += amp2(st, b + k, N);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {                 // fixed tree
+            const double v = __shfl_xor_sync(0xffffffffu, acc, o);
+            acc = ((lane & o) ? v + acc : acc + v);
+        }
+        if (lane == 0) mass[c] = acc;
+    }
+}
+
+// shot s: chunk[s], residual res[s] (u * total - prefix before the chunk) -> out[s] = physical index
+template <typename C>
+__global__ void __launch_bounds__(256) k_sample_find(const C *__restrict__ st, uint64_t N, const uint64_t *chunk,
+                                                     const double *res, uint64_t nshots, uint64_t *out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t per = kSampChunk / 32;
+    for (uint64_t s = blockIdx.x * 8ull + (threadIdx.x >> 5); s < nshots; s += gridDim.x * 8ull) {
+        const uint64_t c = chunk[s];
+        const double r = res[s];
+        const uint64_t b = c * kSampChunk + lane * per;
+        double acc = 0;
+        for (uint64_t k = 0; k < per; ++k) acc += amp2(st, b + k, N);
+        // inclusive prefix of lane sums in lane order (sequential over lanes: left to right)
+        double incl = acc;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const double excl = incl - acc;
+        const unsigned hit = __ballot_sync(0xffffffffu, incl > r);
+        // first lane whose inclusive sum exceeds r (rounding: fall back to the last lane)
+        const int L = hit ? __ffs(hit) - 1 : 31;
+        if (lane == L) {
+            double cum = excl;
+            uint64_t pick = b + per - 1, last_nz = ~0ull;
+            for (uint64_t k = 0; k < per; ++k) {
+                const double p = amp2(st, b + k, N);
+                if (p > 0) last_nz = b + k;
+                cum += p;
+                if (cum > r && p > 0) { pick = b + k; break; }
+                if (k == per - 1 && last_nz != ~0ull) pick = last_nz;
+            }
+            out[s] = pick < N ? pick : N - 1;
+        }
+    }
+}
+
+cudaError_t launch_sample_mass(bool c128, const void *state, uint64_t N, double *mass, uint64_t nchunks,
+                               cudaStream_t st, int *kernels) {
+    const unsigned g = (unsigned)std::min<uint64_t>((nchunks + 7) / 8, (uint64_t)num_sms() * 16);
+    if (c128) k_sample_mass<double2><<<g, 256, 0, st>>>((const double2 *)state, N, nchunks, mass);
+    else k_sample_mass<float2><<<g, 256, 0, st>>>((const float2 *)state, N, nchunks, mass);
+    ++*kernels;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_find(bool c128, const void *state, uint64_t N, const uint64_t *chunk, const double *res,
+                               uint64_t nshots, uint64_t *out, cudaStream_t st, int *kernels) {
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nshots + 7) / 8, (uint64_t)num_sms() * 16));
+    if (c128) k_sample_find<double2><<<g, 256, 0, st>>>((const double2 *)state, N, chunk, res, nshots, out);
+    else k_sample_find<float2><<<g, 256, 0, st>>>((const float2 *)state, N, chunk, res, nshots, out);
+    ++*kernels;
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

@@ -765,6 +765,75 @@ static void fold_diag_into(FOp &o, const QForm &part, const std::vector<int> &pa
 // previous or next dense op on j and become part of its matrix (the outside
 // bits become selectors).  Constant and outside-only terms are per-tile
 // scalars and ride on any dense op.  Terms on two in-tile bits stay.
+// Pass level: a diagonal term none of whose bits is one of its group's register
+// bits (a "V-bit" term) moves to the nearest group of the pass that holds one of
+// its in-tile bits in registers, provided no group in between acts non-diagonally
+// on its bits (diagonal terms commute with everything else).  There it is a
+// group-bit term that absorb_diagonals can fold into a matrix, instead of a
+// per-vector table factor.
+static void relocate_v_terms(std::vector<FOp> &ops, uint64_t S) {
+    const int ng = (int)ops.size();
+    for (int a = 0; a < ng; ++a) {
+        if (ops[a].type != OP_GROUP) continue;
+        for (FOp &d : ops[a].subs) {
+            if (d.type != OP_DIAG) continue;
+            const uint64_t TA = ops[a].T;
+            std::vector<std::pair<std::vector<int>, uint64_t>> moved_terms;   // (bits, angle) per target group
+            auto try_move = [&](uint64_t X) -> int {
+                if ((X & TA) || !(X & S)) return -1;                 // touches A's bits, or outside only
+                int best = -1, bd = 1 << 30;
+                for (int dir : {1, -1}) {
+                    for (int b = a + dir; b >= 0 && b < ng; b += dir) {
+                        if (ops[b].type != OP_GROUP) break;
+                        if (ops[b].T & X & S) {                          // holds one of the bits: target
+                            if (std::abs(b - a) < bd) { bd = std::abs(b - a); best = b; }
+                            break;
+                        }
+                        if (ops[b].dmask & X) break;                     // blocked
+                    }
+                }
+                return best;
+            };
+            std::vector<std::vector<QForm>> add(ng);
+            for (auto it = d.form.lin.begin(); it != d.form.lin.end();) {
+                const int b = try_move(1ull << it->first);
+                if (b >= 0) {
+                    QForm q;
+                    q.lin[it->first] = it->second;
+                    add[b].push_back(q);
+                    it = d.form.lin.erase(it);
+                } else ++it;
+            }
+            for (auto it = d.form.quad.begin(); it != d.form.quad.end();) {
+                const int b = try_move((1ull << it->first.first) | (1ull << it->first.second));
+                if (b >= 0) {
+                    QForm q;
+                    q.quad[it->first] = it->second;
+                    add[b].push_back(q);
+                    it = d.form.quad.erase(it);
+                } else ++it;
+            }
+            d.qmask = d.form.qubits();
+            for (int b = 0; b < ng; ++b) {
+                if (add[b].empty()) continue;
+                FOp nd;
+                nd.type = OP_DIAG;
+                for (const QForm &q : add[b]) nd.form.add(q);
+                nd.qmask = nd.form.qubits();
+                std::vector<FOp> &sb = ops[b].subs;
+                if (b > a) sb.insert(sb.begin(), nd);                  // later group: at its start
+                else sb.push_back(nd);                                  // earlier group: at its end
+                ops[b].qmask |= nd.qmask;
+            }
+        }
+        auto &sb = ops[a].subs;
+        for (size_t k = 0; k < sb.size();) {
+            if (sb[k].type == OP_DIAG && sb[k].form.trivial()) sb.erase(sb.begin() + (long)k);
+            else ++k;
+        }
+    }
+}
+
 static void absorb_diagonals(FOp &grp, uint64_t S, int nl) {
     std::vector<FOp> &ops = grp.subs;
     const uint64_t sel_ok = ~0ull;   // global-bit selectors are resolved per rank at encode time
@@ -1167,6 +1236,11 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                 else S = S0;
             }
             pass.S = S;
+            if (!(opt.flags & SV_OPT_NO_VARIANTS)) {
+                bool grouped = !pass.ops.empty();
+                for (FOp &o : pass.ops) grouped &= o.type == OP_GROUP;
+                if (grouped) relocate_v_terms(pass.ops, S);
+            }
             if (!(opt.flags & SV_OPT_NO_VARIANTS))
                 for (FOp &o : pass.ops)
                     if (o.type == OP_GROUP) {

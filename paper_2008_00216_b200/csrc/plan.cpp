@@ -1415,10 +1415,64 @@ static bool half_table(const QForm &f, const std::vector<int> &pos, const int *l
 
 // Split a group's diagonal form into tables of <= STV_MAX_VBITS V-bits each
 // (diagonal terms commute and add, so the split is exact).
+// Several half tables for a diagonal whose every term contains one group bit j but
+// that has more than STV_MAX_VBITS_H V-bits: terms partitioned by their V-bit.
+static bool half_tables_split(const QForm &f, const std::vector<int> &pos, const int *loc,
+                              std::vector<GroupTable> &out) {
+    if (f.cst != 0) return false;
+    auto local = [&](int phys) -> int {
+        if (loc[phys] < 0) return -1;
+        auto it = std::find(pos.begin(), pos.end(), loc[phys]);
+        return it == pos.end() ? -1 : (int)(it - pos.begin());
+    };
+    for (int j = 0; j < 4; ++j) {
+        int pj = -1;
+        for (auto &kv : f.quad)
+            for (int q : {kv.first.first, kv.first.second})
+                if (local(q) == j) pj = q;
+        for (auto &kv : f.lin)
+            if (local(kv.first) == j) pj = kv.first;
+        if (pj < 0) continue;
+        bool ok = true;
+        for (auto &kv : f.lin) ok &= kv.first == pj;
+        for (auto &kv : f.quad) ok &= kv.first.first == pj || kv.first.second == pj;
+        if (!ok) continue;
+        // chunks of terms with <= STV_MAX_VBITS_H distinct V-partners each
+        std::vector<QForm> parts(1);
+        std::vector<std::vector<int>> vs(1);
+        parts[0].lin = f.lin;
+        for (auto &kv : f.quad) {
+            const int o = kv.first.first == pj ? kv.first.second : kv.first.first;
+            const bool v = loc[o] >= 0 && local(o) < 0;
+            size_t t = 0;
+            if (v) {
+                for (; t < parts.size(); ++t) {
+                    const bool has = std::find(vs[t].begin(), vs[t].end(), o) != vs[t].end();
+                    if (has || (int)vs[t].size() < STV_MAX_VBITS_H) {
+                        if (!has) vs[t].push_back(o);
+                        break;
+                    }
+                }
+                if (t == parts.size()) { parts.emplace_back(); vs.push_back({o}); }
+            }
+            parts[t].quad[kv.first] = kv.second;
+        }
+        for (const QForm &q : parts) {
+            GroupTable gt;
+            if (!half_table(q, pos, loc, gt)) return false;
+            out.push_back(gt);
+        }
+        return true;
+    }
+    return false;
+}
+
 static std::vector<GroupTable> split_group_diag(const QForm &f, const std::vector<int> &pos, const int *loc) {
     {
         GroupTable gt;
         if (half_table(f, pos, loc, gt)) return {gt};
+        std::vector<GroupTable> hs;
+        if (half_tables_split(f, pos, loc, hs)) return hs;
     }
     struct Item { int x, y; uint64_t ang; };   // y = -1: linear term on x
     std::vector<Item> items;

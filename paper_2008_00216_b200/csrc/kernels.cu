@@ -809,6 +809,19 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
     }
 }
 
+// two U2 on complementary pairs (A1,B1) then (A2,B2): written as two passes over the
+// quads so the compiler sees both programs at once
+template <int A1, int B1, int A2, int B2, typename C>
+__device__ __forceinline__ void g_u2x2(C (&x)[16], const C (&ma)[16], const C (&mb)[16]) {
+    if constexpr (sizeof(C) == 8) {
+        g_u2p<A1, B1>(*(float2(*)[16]) & x, *(const float2(*)[16]) & ma);
+        g_u2p<A2, B2>(*(float2(*)[16]) & x, *(const float2(*)[16]) & mb);
+    } else {
+        g_u2<A1, B1>(x, ma);
+        g_u2<A2, B2>(x, mb);
+    }
+}
+
 // half-table diagonal: amplitudes with local bit J set times row[l without bit J]
 template <int J, typename C>
 __device__ __forceinline__ void g_diagh(C (&x)[16], const C *__restrict__ row) {
@@ -878,6 +891,33 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
                 } else {
 #pragma unroll
                     for (int l = 0; l < 16; ++l) x[i][l] = cmul(x[i][l], row[l]);
+                }
+            }
+        } else if ((unsigned)(code - SUBC_U2X2) < 3u) {    // two U2 on complementary pairs
+            const uint32_t wa = ca.x >> 8, wb = subs[k].pad;
+            auto vsel = [&](uint32_t w) {
+                return ((tord >> (w & 31u)) & 1u) | (((tord >> ((w >> 5) & 31u)) & 1u) << 1) |
+                       (((tord >> ((w >> 10) & 31u)) & 1u) << 2);
+            };
+            const C *MA = (const C *)(mat + ca.y) + vsel(wa) * 16;
+            const C *MB = (const C *)(mat + subs[k].ctl) + vsel(wb) * 16;
+            C ma[16], mb[16];
+            if constexpr (kPacked) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    *(float2 *)&ma[e] = ld_c64((const float2 *)MA + e);
+                    *(float2 *)&mb[e] = ld_c64((const float2 *)MB + e);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) { ma[e] = MA[e]; mb[e] = MB[e]; }
+            }
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                switch (code - SUBC_U2X2) {
+                case 0: g_u2x2<0, 1, 2, 3>(x[i], ma, mb); break;
+                case 1: g_u2x2<0, 2, 1, 3>(x[i], ma, mb); break;
+                default: g_u2x2<0, 3, 1, 2>(x[i], ma, mb); break;
                 }
             }
         } else if ((unsigned)(code - SUBC_DIAGH) < 4u) {   // half table on local bit j

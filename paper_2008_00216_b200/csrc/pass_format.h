@@ -115,7 +115,10 @@ static constexpr uint32_t kSwzM0 = swz_mask(0), kSwzM1 = swz_mask(1), kSwzM2 = s
 #define SUBC_DIAG 30
 #define SUBC_U2V 31              // + pair index: U2 with per-tile variants (selectors in code bits 8..22)
 #define SUBC_DIAGH 37            // + j: half-table diagonal on local bit j (arg = table index)
-#define SUBC_N 41
+#define SUBC_U2X2 41             // + pairing ({01,23}, {02,13}, {03,12}): two U2 on complementary pairs;
+                                 // arg/code bits 8..22 = first (lower pair) matrix / selectors,
+                                 // ctl/pad = second matrix / selectors (31 = unused selector)
+#define SUBC_N 44
 
 struct alignas(16) StvSub {
     int32_t code;              // bits 0..7: SUBC_*; U2V: bits 8+5i (i < 3) = selector i, a bit index of the

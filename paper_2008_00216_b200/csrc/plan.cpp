@@ -1705,6 +1705,40 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         out.push_back(sub);
                     }
                 }
+                // adjacent 2-qubit sub-ops on complementary pairs run as one sub-op (one dispatch,
+                // interleaved FFMA2 chains); they act on disjoint bits, so order is irrelevant
+                {
+                    std::vector<StvSub> fused;
+                    auto pair_of = [](int code) -> int {
+                        const int c = code & 0xff;
+                        if (c >= SUBC_U2 && c < SUBC_U2 + 6) return c - SUBC_U2;
+                        if (c >= SUBC_U2V && c < SUBC_U2V + 6) return c - SUBC_U2V;
+                        return -1;
+                    };
+                    static const int comp[6] = {5, 4, 3, 2, 1, 0};   // 01<->23, 02<->13, 03<->12
+                    static const int pairing[6] = {0, 1, 2, 2, 1, 0};
+                    for (size_t k = 0; k < out.size(); ++k) {
+                        const int pa = pair_of(out[k].code);
+                        if (pa >= 0 && k + 1 < out.size() && pair_of(out[k + 1].code) == comp[pa]) {
+                            StvSub f;
+                            std::memset(&f, 0, sizeof(f));
+                            const StvSub &A = pa < comp[pa] ? out[k] : out[k + 1];
+                            const StvSub &B = pa < comp[pa] ? out[k + 1] : out[k];
+                            auto sel_bits = [](const StvSub &x) -> uint32_t {   // 3 x 5-bit selectors
+                                const int c = x.code & 0xff;
+                                if (c >= SUBC_U2V) return (uint32_t)x.code >> 8;
+                                return 31u | (31u << 5) | (31u << 10);        // plain: never selects
+                            };
+                            f.code = (int32_t)((SUBC_U2X2 + pairing[pa]) | (sel_bits(A) << 8));
+                            f.arg = A.arg;
+                            f.ctl = B.arg;
+                            f.pad = sel_bits(B);
+                            fused.push_back(f);
+                            ++k;
+                        } else fused.push_back(out[k]);
+                    }
+                    out = fused;
+                }
                 subs[i] = out;
                 StvGroup &g = grecs[i];
                 std::memset(&g, 0, sizeof(g));

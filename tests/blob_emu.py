@@ -193,6 +193,21 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
                 psi = PI._cnot(psi, n, ctl[0], G[t])
             else:
                 psi = psi[np.arange(1 << n) ^ (1 << G[t])]
+        elif 41 <= c < 44:
+            pairs = [((0, 1), (2, 3)), ((0, 2), (1, 3)), ((0, 3), (1, 2))][c - 41]
+            outbits = [b_ for b_ in range(64) if (P.out_mask >> b_) & 1]
+            esz = 16 if c128 else 8
+            jj = np.arange(1 << n)
+            for (a, b), off, w in ((pairs[0], sb.arg, sb.code >> 8), (pairs[1], sb.ctl, sb.pad)):
+                sel = [outbits[(w >> (5 * i)) & 31] for i in range(3) if ((w >> (5 * i)) & 31) != 31]
+                out = np.zeros_like(psi)
+                for v in range(1 << len(sel)):
+                    M = _matrix(blob, po + P.mat_off + off + v * 16 * esz, 4, c128)
+                    m = np.ones(1 << n, dtype=bool)
+                    for i, s_ in enumerate(sel):
+                        m &= ((jj >> s_) & 1) == ((v >> i) & 1)
+                    out[m] = PI._apply_dense(psi, n, [G[a], G[b]], M)[m]
+                psi = out
         elif 37 <= c < 41:
             jb = c - 37                                       # half table on local bit jb
             d = _at(blob, DTab, po + P.tab_off + ct.sizeof(DTab) * sb.arg)

@@ -1157,7 +1157,7 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
     uint32_t loaded = 0;
     auto issue = [&](int s) {
         uint8_t *stile = (uint8_t *)(tiles + (size_t)s * tile_elems);
-        if (loaded < my_tiles)
+        if (loaded < my_tiles && !(dbg_flags & 2))   // bit 1: compute only (microbenchmark)
             tile_copy_fast<true, NT>(gstate, stile, load_tb, hmask, cp, nruns, esz, tid, hash_t, hk);
         cp_async_commit();
         load_tb = masked_add(load_tb, tstep, out_mask);
@@ -1180,7 +1180,8 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
             group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, first + j * stride, tid);
             __syncthreads();
         }
-        tile_copy_fast<false, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
+        if (!(dbg_flags & 2))
+            tile_copy_fast<false, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
         base = masked_add(base, tstep, out_mask);
     }
     cp_async_wait0();

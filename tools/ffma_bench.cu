@@ -120,6 +120,58 @@ __global__ void u2p_smem(float2 *out, const float *g, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+
+__device__ __forceinline__ float2 cmacN(float2 m, float2 x, float2 acc) {
+    acc = __ffma2_rn(x, make_float2(m.x, m.x), acc);
+    return __ffma2_rn(make_float2(-x.y, x.x), make_float2(m.y, m.y), acc);
+}
+__device__ __forceinline__ float2 cmulN(float2 m, float2 x) {
+    return __ffma2_rn(make_float2(-x.y, x.x), make_float2(m.y, m.y), __fmul2_rn(x, make_float2(m.x, m.x)));
+}
+template <int A, int B, bool SPLIT>
+__device__ __forceinline__ void g_u2n(float2 (&x)[16], const float2 (&m)[16]) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & ((1 << A) | (1 << B))) continue;
+        const float2 v[4] = {x[l], x[l | (1 << A)], x[l | (1 << B)], x[l | (1 << A) | (1 << B)]};
+        float2 o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (SPLIT) {
+                float2 a0 = cmulN(m[r * 4], v[0]), a1 = cmulN(m[r * 4 + 1], v[1]);
+                a0 = cmacN(m[r * 4 + 2], v[2], a0);
+                a1 = cmacN(m[r * 4 + 3], v[3], a1);
+                o[r] = make_float2(a0.x + a1.x, a0.y + a1.y);
+            } else {
+                float2 acc = cmulN(m[r * 4], v[0]);
+#pragma unroll
+                for (int c = 1; c < 4; ++c) acc = cmacN(m[r * 4 + c], v[c], acc);
+                o[r] = acc;
+            }
+        }
+        x[l] = o[0]; x[l | (1 << A)] = o[1]; x[l | (1 << B)] = o[2]; x[l | (1 << A) | (1 << B)] = o[3];
+    }
+}
+struct __align__(16) MatsN { float2 u[8][16]; };
+template <bool SPLIT>
+__global__ void u2n_param(float2 *out, const __grid_constant__ MatsN P, int iters) {
+    float2 x[16];
+    for (int l = 0; l < 16; ++l) x[l] = make_float2(threadIdx.x * 1e-3f + l, l * 0.5f);
+    for (int it = 0; it < iters; ++it) {
+        const int k = it & 3;
+        float2 m0[16], m1[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) { m0[e] = P.u[k][e]; m1[e] = P.u[k + 4][e]; }
+        g_u2n<0, 1, SPLIT>(x, m0);
+        g_u2n<2, 3, SPLIT>(x, m1);
+        g_u2n<0, 2, SPLIT>(x, m0);
+        g_u2n<1, 3, SPLIT>(x, m1);
+    }
+    float2 s = make_float2(0, 0);
+    for (int l = 0; l < 16; ++l) { s.x += x[l].x; s.y += x[l].y; }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void u2_const(float2 *out, int iters) {
     float2 x[16];
     for (int l = 0; l < 16; ++l) x[l] = make_float2(threadIdx.x * 1e-3f + l, l * 0.5f);
@@ -194,14 +246,16 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int threads : {128, 256}) {
-        for (int ctas_per_sm : {1, 2, 3, 4}) {
+    for (int threads : {256}) {
+        for (int ctas_per_sm : {1, 2, 3}) {
             const int grid = sms * ctas_per_sm;
             if (threads * ctas_per_sm > 2048) continue;
             // U2: 4 sub-ops x 4 quads x 16 cfma x 4 FFMA = 1024 FFMA per iteration per thread
             const double u2_flops = 2.0 * 1024 * iters * (double)grid * threads;
             const double ffma_flops = 2.0 * 8 * 64 * iters * (double)grid * threads;
-            for (int k = 0; k < 7; ++k) {
+            MatsN PN;
+            for (int u = 0; u < 8; ++u) for (int e = 0; e < 16; ++e) PN.u[u][e] = make_float2(0.1f * ((e * 7 + u) % 5 - 2), 0.05f * (e % 3));
+            for (int k = 0; k < 9; ++k) {
                 float ms = 0;
                 for (int rep = 0; rep < 2; ++rep) {
                     cudaEventRecord(e0);
@@ -212,12 +266,15 @@ int main() {
                     if (k == 4) ffma_imm<<<grid, threads>>>((float *)out, iters);
                     if (k == 5) u2p_smem<1><<<grid, threads>>>(out, (const float *)dg, iters);
                     if (k == 6) u2p_smem<2><<<grid, threads>>>(out, (const float *)dg, iters);
+                    if (k == 7) u2n_param<false><<<grid, threads>>>(out, PN, iters);
+                    if (k == 8) u2n_param<true><<<grid, threads>>>(out, PN, iters);
                     cudaEventRecord(e1);
                     cudaEventSynchronize(e1);
                     cudaEventElapsedTime(&ms, e0, e1);
                 }
-                const char *nm[] = {"u2_smem", "u2_const", "u2_param", "ffma_reg", "ffma_imm", "u2p_nv1", "u2p_nv2"};
-                const double fl = k < 3 ? u2_flops : k == 5 ? u2_flops : k == 6 ? 2 * u2_flops : ffma_flops;
+                const char *nm[] = {"u2_smem", "u2_const", "u2_param", "ffma_reg", "ffma_imm", "u2p_nv1", "u2p_nv2",
+                                    "u2n_ur", "u2n_ur_split"};
+                const double fl = k < 3 ? u2_flops : k == 5 ? u2_flops : k == 6 ? 2 * u2_flops : k >= 7 ? u2_flops : ffma_flops;
                 printf("%-9s threads=%d ctas/sm=%d  %.3f ms  %.1f TFLOP/s  (peak@%d MHz = %.1f)\n", nm[k], threads,
                        ctas_per_sm, ms, fl / ms / 1e9, clk / 1000, sms * 128 * 2.0 * clk * 1e3 / 1e12);
             }

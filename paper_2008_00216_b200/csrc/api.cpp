@@ -369,7 +369,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
             kind = hp->h == 0 ? 1 : 2;
             if (hp->grouped)
                 e = launch_group_pass(s->c128(), s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
-                                      enc_local, hp->rec_bytes, hp->tab_entries, pass_flops_per_amp(ps.ops),
+                                      enc_local, hp->param_bytes, hp->tab_entries, pass_flops_per_amp(ps.ops),
                                       s->stream, &kernels);
             else
                 e = launch_tile_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->rec_bytes,

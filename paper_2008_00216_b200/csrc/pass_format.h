@@ -79,7 +79,9 @@ struct alignas(16) StvPass {
     uint32_t tab_off;          // byte offset of StvDTab[ntab]
     int32_t grouped;           // 1: every op is a gate group (StvGroup[nops] at ops_off), k_group_pass
     uint32_t tab_entries;      // total table entries (amplitudes) in shared memory
-    int32_t pad2;
+    uint32_t param_bytes;      // leading bytes of the record passed as the group-pass kernel
+                               // parameter (the rest -- static table phases -- is read from
+                               // device memory only)
 };
 
 // ---------------------------------------------------------------------------
@@ -150,13 +152,15 @@ struct alignas(16) StvGroup {
 // bank conflicts between lanes with different r).
 struct alignas(16) StvDTab {
     uint32_t stat_off;         // byte offset (pass record) of uint64 stat[(half ? 8 : 16) << m]
+    uint32_t cstat_off;        // byte offset of the same static phases as unit complex numbers
+                               // (state precision, rounded once from fp64): entry = cstat[e] x
+                               // F_low[low index bits] x F_high[V-bit index] built per tile
     uint32_t term_off;         // byte offset of StvTerm[nterm]
     int32_t nterm;
     int32_t m;
     uint32_t ent_off;          // first entry in the shared-memory table area
     int32_t half;              // 0: full table over l (16) x r; 1: half table (below)
     uint16_t vraw[STV_MAX_VBITS_H];   // raw tile offsets of the V-bits (0 for unused)
-    uint16_t pad[2];
 };
 // Half table (code SUBC_DIAGH + j): every term of the diagonal contains local bit j,
 // so amplitudes with l_j = 0 are unchanged; the table is over (the 3 other local

@@ -556,8 +556,7 @@ static size_t diag_table_bytes(const QForm &f, uint64_t vmask, uint64_t T, int a
             if (!ok || m > STV_MAX_VBITS_H) continue;
             *ntab = 1;
             *tab_smem += (size_t)(STV_TAB_STRIDE_H * amp_bytes) << m;
-            return sizeof(StvDTab) + sizeof(StvSub) + ((size_t)64 << m) + 32 +
-                   sizeof(StvTerm) * (f.lin.size() + f.quad.size());
+            return sizeof(StvDTab) + sizeof(StvSub) + 32 + sizeof(StvTerm) * (f.lin.size() + f.quad.size());
         }
     std::vector<uint64_t> sets;
     auto place = [&](uint64_t need) {
@@ -573,7 +572,7 @@ static size_t diag_table_bytes(const QForm &f, uint64_t vmask, uint64_t T, int a
     size_t bytes = sizeof(StvTerm) * terms;
     for (uint64_t u : sets) {
         const int m = __builtin_popcountll(u);
-        bytes += sizeof(StvDTab) + sizeof(StvSub) + ((size_t)128 << m) + 32;
+        bytes += sizeof(StvDTab) + sizeof(StvSub) + 32;
         *tab_smem += (size_t)(STV_TAB_STRIDE * amp_bytes) << m;
     }
     *ntab = (int)sets.size();
@@ -1541,6 +1540,7 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
         e.pass_off.push_back((uint32_t)at);
         StvPass hd;
         std::memset(&hd, 0, sizeof(hd));
+        std::vector<uint8_t> tail;                   // global-only part of the record
         hd.kind = ps.kind;
         hd.n_local = n_local;
         b.resize(at + sizeof(StvPass));
@@ -1689,9 +1689,18 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         d.half = gt.half >= 0 ? 1 : 0;
                         for (int v = 0; v < d.m; ++v) d.vraw[v] = (uint16_t)(1u << gt.vpos[v]);
                         d.nterm = (int)gt.terms.size();
-                        align(b, 16);
-                        d.stat_off = (uint32_t)(b.size() - at);
-                        put(b, gt.stat.data(), gt.stat.size() * sizeof(uint64_t));
+                        // static phases live in the global-only tail of the record (read per lane
+                        // from device memory, never part of the kernel-parameter copy)
+                        align(tail, 16);
+                        d.stat_off = (uint32_t)tail.size();
+                        put(tail, gt.stat.data(), gt.stat.size() * sizeof(uint64_t));
+                        align(tail, 16);
+                        d.cstat_off = (uint32_t)tail.size();
+                        for (uint64_t ph : gt.stat) {
+                            const double a = angle_of_turns(ph);
+                            if (c128) { double v[2] = {std::cos(a), std::sin(a)}; put(tail, v, 16); }
+                            else { float v[2] = {(float)std::cos(a), (float)std::sin(a)}; put(tail, v, 8); }
+                        }
                         align(b, 16);
                         d.term_off = (uint32_t)(b.size() - at);
                         put(b, gt.terms.data(), gt.terms.size() * sizeof(StvTerm));
@@ -1790,6 +1799,17 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
             hd.cnot_t = ps.ops[0].t;
         }
         align(b, 16);
+        hd.param_bytes = (uint32_t)(b.size() - at);
+        if (!tail.empty()) {                         // global-only tail: patch the table offsets
+            const uint32_t base = (uint32_t)(b.size() - at);
+            for (int t = 0; t < hd.ntab; ++t) {
+                StvDTab *d = (StvDTab *)&b[at + hd.tab_off + (size_t)t * sizeof(StvDTab)];
+                d->stat_off += base;
+                d->cstat_off += base;
+            }
+            put(b, tail.data(), tail.size());
+            align(b, 16);
+        }
         hd.rec_bytes = (uint32_t)(b.size() - at);
         std::memcpy(&b[at], &hd, sizeof(hd));
     }

@@ -42,9 +42,9 @@ class Group(ct.Structure):
 
 
 class DTab(ct.Structure):
-    _fields_ = [("stat_off", ct.c_uint32), ("term_off", ct.c_uint32), ("nterm", ct.c_int32), ("m", ct.c_int32),
-                ("ent_off", ct.c_uint32), ("half", ct.c_int32), ("vraw", ct.c_uint16 * 6), ("pad", ct.c_uint16 * 2),
-                ("pad2", ct.c_uint32 * 2)]
+    _fields_ = [("stat_off", ct.c_uint32), ("cstat_off", ct.c_uint32), ("term_off", ct.c_uint32),
+                ("nterm", ct.c_int32), ("m", ct.c_int32), ("ent_off", ct.c_uint32), ("half", ct.c_int32),
+                ("vraw", ct.c_uint16 * 6), ("pad2", ct.c_uint32 * 2)]
 
 
 class Pass(ct.Structure):
@@ -53,7 +53,7 @@ class Pass(ct.Structure):
                 ("n_local", ct.c_int32), ("nops", ct.c_int32), ("ops_off", ct.c_uint32), ("mat_off", ct.c_uint32),
                 ("mat_bytes", ct.c_uint32), ("cnot_c", ct.c_int32), ("cnot_t", ct.c_int32), ("diag_off", ct.c_uint32),
                 ("rec_bytes", ct.c_uint32), ("ntab", ct.c_int32), ("tab_off", ct.c_uint32), ("grouped", ct.c_int32),
-                ("tab_entries", ct.c_uint32), ("pad2", ct.c_int32)]
+                ("tab_entries", ct.c_uint32), ("param_bytes", ct.c_uint32)]
 
 
 assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16

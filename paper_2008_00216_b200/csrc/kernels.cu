@@ -809,6 +809,51 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
     }
 }
 
+// real-matrix U1 / U2: every output is a real combination of complex inputs -- one
+// FMUL2 + FFMA2s with broadcast real coefficients per output (half the work of a
+// complex matrix)
+template <typename C, typename R>
+__device__ __forceinline__ C rmul(R m, C x) {
+    if constexpr (sizeof(C) == 8) return __fmul2_rn(x, make_float2(m, m));
+    else { C r; r.x = m * x.x; r.y = m * x.y; return r; }
+}
+template <typename C, typename R>
+__device__ __forceinline__ C rmac(R m, C x, C acc) {
+    if constexpr (sizeof(C) == 8) return __ffma2_rn(x, make_float2(m, m), acc);
+    else { acc.x = fma(m, x.x, acc.x); acc.y = fma(m, x.y, acc.y); return acc; }
+}
+template <int A, typename C, typename R>
+__device__ __forceinline__ void g_u1r(C (&x)[16], const R *__restrict__ M) {
+    const R m0 = M[0], m1 = M[1], m2 = M[2], m3 = M[3];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & (1 << A)) continue;
+        const C p = x[l], q = x[l | (1 << A)];
+        x[l] = rmac(m1, q, rmul<C, R>(m0, p));
+        x[l | (1 << A)] = rmac(m3, q, rmul<C, R>(m2, p));
+    }
+}
+template <int A, int B, typename C, typename R>
+__device__ __forceinline__ void g_u2r(C (&x)[16], const R (&m)[16]) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+        if (l & ((1 << A) | (1 << B))) continue;
+        const C v[4] = {x[l], x[l | (1 << A)], x[l | (1 << B)], x[l | (1 << A) | (1 << B)]};
+        C o[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            C acc = rmul<C, R>(m[r * 4], v[0]);
+#pragma unroll
+            for (int c = 1; c < 4; ++c) acc = rmac(m[r * 4 + c], v[c], acc);
+            o[r] = acc;
+        }
+        x[l] = o[0];
+        x[l | (1 << A)] = o[1];
+        x[l | (1 << B)] = o[2];
+        x[l | (1 << A) | (1 << B)] = o[3];
+    }
+}
+
 // two U2 on complementary pairs (A1,B1) then (A2,B2): written as two passes over the
 // quads so the compiler sees both programs at once
 template <int A1, int B1, int A2, int B2, typename C>
@@ -891,6 +936,35 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
                 } else {
 #pragma unroll
                     for (int l = 0; l < 16; ++l) x[i][l] = cmul(x[i][l], row[l]);
+                }
+            }
+        } else if ((unsigned)(code - SUBC_U1R) < 10u) {    // real U1 / U2
+            using R = decltype(x[0][0].x);
+            const R *MRl = (const R *)(mat + ca.y);
+            if (code < SUBC_U2R) {
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    switch (code - SUBC_U1R) {
+                    case 0: g_u1r<0>(x[i], MRl); break;
+                    case 1: g_u1r<1>(x[i], MRl); break;
+                    case 2: g_u1r<2>(x[i], MRl); break;
+                    default: g_u1r<3>(x[i], MRl); break;
+                    }
+                }
+            } else {
+                R m[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) m[e] = MRl[e];
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    switch (code - SUBC_U2R) {
+                    case 0: g_u2r<0, 1>(x[i], m); break;
+                    case 1: g_u2r<0, 2>(x[i], m); break;
+                    case 2: g_u2r<0, 3>(x[i], m); break;
+                    case 3: g_u2r<1, 2>(x[i], m); break;
+                    case 4: g_u2r<1, 3>(x[i], m); break;
+                    default: g_u2r<2, 3>(x[i], m); break;
+                    }
                 }
             }
         } else if ((unsigned)(code - SUBC_U2X2) < 3u) {    // two U2 on complementary pairs

@@ -120,7 +120,9 @@ static constexpr uint32_t kSwzM0 = swz_mask(0), kSwzM1 = swz_mask(1), kSwzM2 = s
 #define SUBC_U2X2 41             // + pairing ({01,23}, {02,13}, {03,12}): two U2 on complementary pairs;
                                  // arg/code bits 8..22 = first (lower pair) matrix / selectors,
                                  // ctl/pad = second matrix / selectors (31 = unused selector)
-#define SUBC_N 44
+#define SUBC_U1R 44              // + a: U1 with a real matrix (stored as 4 reals)
+#define SUBC_U2R 48              // + pair index: U2 with a real matrix (stored as 16 reals)
+#define SUBC_N 54
 
 struct alignas(16) StvSub {
     int32_t code;              // bits 0..7: SUBC_*; U2V: bits 8+5i (i < 3) = selector i, a bit index of the

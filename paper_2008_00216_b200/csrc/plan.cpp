@@ -1610,12 +1610,24 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         std::memset(&sub, 0, sizeof(sub));
                         if (so.type == OP_DENSE) {
                             const int x = lbit(so.tg[0]);
-                            if (so.tg.size() == 1) sub.code = SUBC_U1 + x;
-                            else {
-                                static const int pidx[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
-                                sub.code = (so.Mv.empty() ? SUBC_U2 : SUBC_U2V) + pidx[x][lbit(so.tg[1])];
-                            }
-                            if (so.Mv.empty()) sub.arg = put_matrix(so.M);
+                            static const int pidx[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
+                            // a real matrix (Hadamard, CNOT/X factors, real rotations) takes half the
+                            // multiplies: each complex amplitude is scaled by real entries
+                            bool real = so.Mv.empty();
+                            for (const cd &z : so.M) real = real && std::abs(z.imag()) <= 1e-15 * std::max(1.0, std::abs(z.real()));
+                            if (real) {
+                                sub.code = so.tg.size() == 1 ? SUBC_U1R + x : SUBC_U2R + pidx[x][lbit(so.tg[1])];
+                                const uint32_t off = (uint32_t)(b.size() - at - hd.mat_off);
+                                for (const cd &z : so.M) {
+                                    if (c128) { double v = z.real(); put(b, &v, 8); }
+                                    else { float v = (float)z.real(); put(b, &v, 4); }
+                                }
+                                align(b, 16);
+                                sub.arg = off;
+                            } else if (so.tg.size() == 1) sub.code = SUBC_U1 + x;
+                            else sub.code = (so.Mv.empty() ? SUBC_U2 : SUBC_U2V) + pidx[x][lbit(so.tg[1])];
+                            if (real) {}
+                            else if (so.Mv.empty()) sub.arg = put_matrix(so.M);
                             else {
                                 // selectors on local bits become bits of the tile ordinal t (base =
                                 // pdep(t, out_mask)); global-bit selectors are fixed for this rank

@@ -193,6 +193,13 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
                 psi = PI._cnot(psi, n, ctl[0], G[t])
             else:
                 psi = psi[np.arange(1 << n) ^ (1 << G[t])]
+        elif 44 <= c < 54:
+            D_ = 2 if c < 48 else 4
+            dt = np.float64 if c128 else np.float32
+            M = np.frombuffer(blob, dtype=dt, count=D_ * D_, offset=po + P.mat_off + sb.arg).astype(np.float64)
+            M = M.reshape(D_, D_).astype(np.complex128)
+            tg = [G[c - 44]] if c < 48 else [G[q] for q in U2_PAIRS[c - 48]]
+            psi = PI._apply_dense(psi, n, tg, M)
         elif 41 <= c < 44:
             pairs = [((0, 1), (2, 3)), ((0, 2), (1, 3)), ((0, 3), (1, 2))][c - 41]
             outbits = [b_ for b_ in range(64) if (P.out_mask >> b_) & 1]

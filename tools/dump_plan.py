@@ -19,6 +19,8 @@ for pi,po in enumerate(offs):
       c=sb.code&0xff
       if c<4: s.append('U1(%d)'%c)
       elif c<10: s.append('U2(%d%d)'%B.U2_PAIRS[c-4])
+      elif c>=48: s.append('U2R(%d%d)'%B.U2_PAIRS[c-48])
+      elif c>=44: s.append('U1R(%d)'%(c-44))
       elif c>=41: s.append('U2x2%d'%(c-41))
       elif c>=37: s.append('DH%d(m%d)'%(c-37,B._at(blob,B.DTab,po+P.tab_off+48*sb.arg).m))
       elif c>=31: s.append('U2V(%d%d;%d)'%(B.U2_PAIRS[c-31]+(sum(((sb.code>>(8+5*i))&31)!=31 for i in range(3)),)))

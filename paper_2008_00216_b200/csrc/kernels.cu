@@ -1049,17 +1049,25 @@ template <typename C, int NT, int NV>
 __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
                                              const uint8_t *__restrict__ mat,
                                              const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base,
-                                             uint32_t tord, int ctid) {
+                                             uint32_t tord, const uint8_t *__restrict__ grec, int ctid) {
     constexpr int TB = NT == 128 ? 7 : 8;   // log2(NT)
     static_assert((1 << TB) == NT, "NT must be 128 or 256");
     const int nvb = g.nvb;
-    uint32_t braw0 = 0, bsw0 = 0;
+    uint32_t braw0, bsw0;
+    if (NT == 256 && grec) {   // precomputed per-thread bases of the first 8 vector bits (global tail)
+        const uint32_t w = __ldg((const uint32_t *)(grec + g.vtab_off) + ctid);
+        bsw0 = w & 0xffffu;
+        braw0 = w >> 16;
+    } else {
+        braw0 = 0;
+        bsw0 = 0;
 #pragma unroll
-    for (int b = 0; b < TB; ++b) {
-        const uint2 vb = *(const uint2 *)g.vbit[b];
-        if (b < nvb && ((ctid >> b) & 1)) {
-            braw0 |= vb.x;
-            bsw0 ^= vb.y;
+        for (int b = 0; b < TB; ++b) {
+            const uint2 vb = *(const uint2 *)g.vbit[b];
+            if (b < nvb && ((ctid >> b) & 1)) {
+                braw0 |= vb.x;
+                bsw0 ^= vb.y;
+            }
         }
     }
     uint32_t so[16];
@@ -1251,7 +1259,7 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
             __syncthreads();
         }
         for (int o = 0; o < nops; ++o) {
-            group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, first + j * stride, tid);
+            group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, first + j * stride, grec, tid);
             __syncthreads();
         }
         if (!(dbg_flags & 2))

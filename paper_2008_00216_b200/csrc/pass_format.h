@@ -143,6 +143,9 @@ struct alignas(16) StvGroup {
     int32_t tpos[4];
     uint32_t sw_off[16];       // swizzled tile offset (amplitudes) of local index l
     uint32_t vbit[STV_MAX_TILE_BITS - 4][2];   // vector bit b: {raw tile offset 1 << position, swizzled offset}
+    uint32_t vtab_off;         // byte offset (pass record, global-only tail) of uint32 vtab[256]:
+                               // thread t's first vector, (swizzled base) | (raw base << 16)
+    uint32_t pad[3];
 };
 
 // Per-tile phase table of one group DIAG sub-op, over index e = l | (r << 4):

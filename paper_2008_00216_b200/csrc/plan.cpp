@@ -1777,6 +1777,17 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         if ((l >> j) & 1) off |= 1u << pos[j];
                     g.sw_off[l] = swz_amp(off, c128);
                 }
+                {   // per-thread vector bases of the first 8 vector bits (kernel: one load per group)
+                    align(tail, 16);
+                    g.vtab_off = (uint32_t)tail.size();
+                    for (uint32_t t = 0; t < 256; ++t) {
+                        uint32_t raw = 0, sw = 0;
+                        for (int v = 0; v < std::min(g.nvb, 8); ++v)
+                            if ((t >> v) & 1) { raw |= g.vbit[v][0]; sw ^= g.vbit[v][1]; }
+                        const uint32_t w = (sw & 0xffffu) | (raw << 16);
+                        put(tail, &w, 4);
+                    }
+                }
                 align(b, 16);
                 g.nsub = (int)subs[i].size();
                 g.sub_off = (uint32_t)(b.size() - at);
@@ -1812,13 +1823,18 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
         }
         align(b, 16);
         hd.param_bytes = (uint32_t)(b.size() - at);
-        if (!tail.empty()) {                         // global-only tail: patch the table offsets
+        if (!tail.empty()) {                         // global-only tail: patch the offsets into it
             const uint32_t base = (uint32_t)(b.size() - at);
             for (int t = 0; t < hd.ntab; ++t) {
                 StvDTab *d = (StvDTab *)&b[at + hd.tab_off + (size_t)t * sizeof(StvDTab)];
                 d->stat_off += base;
                 d->cstat_off += base;
             }
+            if (hd.grouped)
+                for (int i = 0; i < hd.nops; ++i) {
+                    StvGroup *g = (StvGroup *)&b[at + hd.ops_off + (size_t)i * sizeof(StvGroup)];
+                    g->vtab_off += base;
+                }
             put(b, tail.data(), tail.size());
             align(b, 16);
         }

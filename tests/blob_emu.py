@@ -38,7 +38,8 @@ class Sub(ct.Structure):
 
 class Group(ct.Structure):
     _fields_ = [("nsub", ct.c_int32), ("sub_off", ct.c_uint32), ("nvb", ct.c_int32), ("pair16", ct.c_int32),
-                ("tpos", ct.c_int32 * 4), ("sw_off", ct.c_uint32 * 16), ("vbit", (ct.c_uint32 * 2) * (MAXT - 4))]
+                ("tpos", ct.c_int32 * 4), ("sw_off", ct.c_uint32 * 16), ("vbit", (ct.c_uint32 * 2) * (MAXT - 4)),
+                ("vtab_off", ct.c_uint32), ("pad", ct.c_uint32 * 3)]
 
 
 class DTab(ct.Structure):
@@ -57,7 +58,7 @@ class Pass(ct.Structure):
 
 
 assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
-assert ct.sizeof(Group) == 176 and ct.sizeof(DTab) == 48
+assert ct.sizeof(Group) == 192 and ct.sizeof(DTab) == 48
 
 U2_PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
 

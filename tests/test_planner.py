@@ -246,7 +246,7 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
         if P.kind != 1 or not P.grouped:
             continue
         for gi in range(P.nops):
-            g = BE._at(blob, BE.Group, po + P.ops_off + 176 * gi)
+            g = BE._at(blob, BE.Group, po + P.ops_off + 192 * gi)
             ngroups += 1
             assert g.nvb == P.S - 4
             assert bool(g.pair16) == (not c128 and g.tpos[0] == 0)
@@ -268,6 +268,15 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
                         s ^= g.vbit[b][1]
                 return s ^ g.sw_off[l]
 
+            # precomputed per-thread bases (first 8 vector bits) agree with the bit table
+            vt = np.frombuffer(blob, dtype=np.uint32, count=256, offset=po + g.vtab_off)
+            for t in range(1 << min(g.nvb, 8)):
+                raw = sum(g.vbit[b][0] for b in range(min(g.nvb, 8)) if (t >> b) & 1)
+                sw = 0
+                for b in range(min(g.nvb, 8)):
+                    if (t >> b) & 1:
+                        sw ^= g.vbit[b][1]
+                assert int(vt[t]) == (sw & 0xFFFF) | (raw << 16)
             seen = set()
             for v in range(1 << g.nvb):
                 for l in range(16):

@@ -1596,10 +1596,10 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
                               int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, double flops_per_amp,
                               cudaStream_t st, int *kernels) {
     const size_t esz = c128 ? 16 : 8;
-    static const int cfg0 = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
-    static const double light = getenv("STV_LIGHT") ? atof(getenv("STV_LIGHT")) : 0.0;
-    // light passes (little FP work per amplitude) are HBM-latency-bound: prefetch 2 tiles ahead
-    const int cfg = (cfg0 == 0 && !c128 && flops_per_amp < light) ? 2 : cfg0;
+    // tuning knob STV_GCFG (measured on c2): 0 = 256 threads x 1 vector,
+    // 2 stages (default, best); 1 = 128 threads x 2 vectors; 2 = 3 stages
+    static const int cfg = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
+    (void)flops_per_amp;
     const int ns = cfg == 2 ? 3 : kGStagesDefault;
     const size_t smem = 1024 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)ns * (esz << S);
     const uint64_t ntiles = 1ull << (n_local - S);

@@ -1095,6 +1095,30 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
                     bsw[i] ^= g.vbit[b][1];
                 }
         }
+        // predicated X flips folded into the gather / scatter addresses (pass_format.h)
+        uint32_t bsw_g[NV], bsw_s[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            bsw_g[i] = bsw[i];
+            bsw_s[i] = bsw[i];
+        }
+        if (g.nflip_g | g.nflip_s) {
+            auto flip_delta = [&](int from, int cnt, uint32_t br) {
+                uint32_t dlt = 0;
+                for (int q = 0; q < cnt; ++q) {
+                    const uint32_t f = g.flip[from + q];
+                    const uint32_t a = f >> 17;
+                    const bool on = (f & (1u << 16)) ? ((full_base >> a) & 1) != 0 : (br & a) != 0;
+                    if (on) dlt ^= f & 0xffffu;
+                }
+                return dlt;
+            };
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                bsw_g[i] ^= flip_delta(0, g.nflip_g, braw[i]);
+                bsw_s[i] ^= flip_delta(STV_MAX_FLIPS, g.nflip_s, braw[i]);
+            }
+        }
         C x[NV][16];
         const bool live1 = NV == 1 || v0 + NT < nvec;   // tiny tiles: the second vector may not exist
 #pragma unroll
@@ -1107,12 +1131,12 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
             if (pair16) {
 #pragma unroll
                 for (int l = 0; l < 16; l += 2) {
-                    const float4 q = *(const float4 *)&tile[bsw[i] ^ so[l]];
+                    const float4 q = *(const float4 *)&tile[bsw_g[i] ^ so[l]];
                     x[i][l].x = q.x; x[i][l].y = q.y; x[i][l + 1].x = q.z; x[i][l + 1].y = q.w;
                 }
             } else {
 #pragma unroll
-                for (int l = 0; l < 16; ++l) x[i][l] = tile[bsw[i] ^ so[l]];
+                for (int l = 0; l < 16; ++l) x[i][l] = tile[bsw_g[i] ^ so[l]];
             }
         }
         run_subs<C, NV>(x, braw, subs, nsub, mat, tabs, tables, full_base, tord, P->rank_bits);
@@ -1122,10 +1146,10 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
             if (pair16) {
 #pragma unroll
                 for (int l = 0; l < 16; l += 2)
-                    *(float4 *)&tile[bsw[i] ^ so[l]] = make_float4(x[i][l].x, x[i][l].y, x[i][l + 1].x, x[i][l + 1].y);
+                    *(float4 *)&tile[bsw_s[i] ^ so[l]] = make_float4(x[i][l].x, x[i][l].y, x[i][l + 1].x, x[i][l + 1].y);
             } else {
 #pragma unroll
-                for (int l = 0; l < 16; ++l) tile[bsw[i] ^ so[l]] = x[i][l];
+                for (int l = 0; l < 16; ++l) tile[bsw_s[i] ^ so[l]] = x[i][l];
             }
         }
     }

@@ -23,6 +23,7 @@
 #define STV_MAX_TABLES 32
 #define STV_MAX_VBITS 3          // in-tile bits outside the group a full diag table may index
 #define STV_MAX_VBITS_H 6        // ... a half diag table may index
+#define STV_MAX_FLIPS 8          // predicated X flips per group folded into gather / scatter addresses
 
 #define STV_MAX_TILE_BITS 14
 #define STV_MAX_K 4
@@ -145,7 +146,12 @@ struct alignas(16) StvGroup {
     uint32_t vbit[STV_MAX_TILE_BITS - 4][2];   // vector bit b: {raw tile offset 1 << position, swizzled offset}
     uint32_t vtab_off;         // byte offset (pass record, global-only tail) of uint32 vtab[256]:
                                // thread t's first vector, (swizzled base) | (raw base << 16)
-    uint32_t pad[3];
+    int32_t nflip_g, nflip_s;  // predicated X flips folded into the gather / scatter addresses
+    int32_t pad;
+    uint32_t flip[2 * STV_MAX_FLIPS];   // [0, nflip_g) gather, [STV_MAX_FLIPS, +nflip_s) scatter:
+                                        // bits 0..15 swizzled offset of the flipped tile position,
+                                        // bit 16 control outside the tile, bits 17..31 the raw tile
+                                        // offset of the (vector-bit) control or its physical bit
 };
 
 // Per-tile phase table of one group DIAG sub-op, over index e = l | (r << 4):

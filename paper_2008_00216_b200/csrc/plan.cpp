@@ -1760,6 +1760,65 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                     }
                     out = fused;
                 }
+                // CNOT sub-ops whose control is not a register bit are predicated X flips of a
+                // local bit; at the very start / end of the program (moved past ops that do not
+                // touch the bit; X flips commute with each other) they cost nothing: the gather /
+                // scatter address of local index l becomes that of l xor flips (pass_format.h)
+                std::vector<uint32_t> gflips, sflips;
+                {
+                    auto is_flip = [&](const StvSub &x) {
+                        const int c = x.code & 0xff;
+                        if (!(c >= SUBC_CNOT && c < SUBC_CNOT + 4)) return false;   // in-register control -1
+                        // complex64 pair accesses (16 B) cannot swap the two amplitudes of a pair
+                        return c128 || pos[c - SUBC_CNOT] != 0;
+                    };
+                    auto touches = [&](const StvSub &x, int t) -> bool {  // local bits an op involves
+                        const int c = x.code & 0xff;
+                        if (c < SUBC_U2) return c - SUBC_U1 == t;
+                        if (c < SUBC_CNOT) { const int p = c - SUBC_U2; static const int A[6] = {0,0,0,1,1,2}, Bb[6] = {1,2,3,2,3,3}; return A[p] == t || Bb[p] == t; }
+                        if (c < SUBC_DIAG) { const int cc = (c - SUBC_CNOT) / 4 - 1, tt = (c - SUBC_CNOT) % 4; return tt == t || cc == t; }
+                        if (c >= SUBC_U1R && c < SUBC_U2R) return c - SUBC_U1R == t;
+                        if (c >= SUBC_U2R && c < SUBC_U2R + 6) { const int p = c - SUBC_U2R; static const int A[6] = {0,0,0,1,1,2}, Bb[6] = {1,2,3,2,3,3}; return A[p] == t || Bb[p] == t; }
+                        if (c >= SUBC_U2V && c < SUBC_U2V + 6) { const int p = c - SUBC_U2V; static const int A[6] = {0,0,0,1,1,2}, Bb[6] = {1,2,3,2,3,3}; return A[p] == t || Bb[p] == t; }
+                        return true;                                      // tables, fused pairs: all bits
+                    };
+                    auto encode_flip = [&](const StvSub &x) -> uint32_t {
+                        const int t = ((x.code & 0xff) - SUBC_CNOT) % 4;
+                        const uint32_t dlt = swz_amp(1u << pos[t], c128);
+                        if (x.ctl & 0xffffu) return dlt | ((x.ctl & 0xffffu) << 17);
+                        return dlt | (1u << 16) | (((x.ctl >> 16) - 1) << 17);
+                    };
+                    bool moved = true;
+                    while (moved && (int)gflips.size() < STV_MAX_FLIPS) {
+                        moved = false;
+                        for (size_t k = 0; k < out.size(); ++k) {
+                            if (!is_flip(out[k])) continue;
+                            const int t = ((out[k].code & 0xff) - SUBC_CNOT) % 4;
+                            bool ok = true;
+                            for (size_t q = 0; q < k && ok; ++q) ok = is_flip(out[q]) || !touches(out[q], t);
+                            if (!ok) continue;
+                            gflips.push_back(encode_flip(out[k]));
+                            out.erase(out.begin() + (long)k);
+                            moved = true;
+                            break;
+                        }
+                    }
+                    moved = true;
+                    while (moved && (int)sflips.size() < STV_MAX_FLIPS) {
+                        moved = false;
+                        for (size_t k = out.size(); k-- > 0;) {
+                            if (!is_flip(out[k])) continue;
+                            const int t = ((out[k].code & 0xff) - SUBC_CNOT) % 4;
+                            bool ok = true;
+                            for (size_t q = k + 1; q < out.size() && ok; ++q) ok = is_flip(out[q]) || !touches(out[q], t);
+                            if (!ok) continue;
+                            sflips.push_back(encode_flip(out[k]));
+                            out.erase(out.begin() + (long)k);
+                            moved = true;
+                            break;
+                        }
+                    }
+                }
                 subs[i] = out;
                 StvGroup &g = grecs[i];
                 std::memset(&g, 0, sizeof(g));
@@ -1788,6 +1847,10 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         put(tail, &w, 4);
                     }
                 }
+                g.nflip_g = (int)gflips.size();
+                g.nflip_s = (int)sflips.size();
+                for (size_t q = 0; q < gflips.size(); ++q) g.flip[q] = gflips[q];
+                for (size_t q = 0; q < sflips.size(); ++q) g.flip[STV_MAX_FLIPS + q] = sflips[q];
                 align(b, 16);
                 g.nsub = (int)subs[i].size();
                 g.sub_off = (uint32_t)(b.size() - at);
@@ -1801,7 +1864,32 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
             hd.tab_off = (uint32_t)(b.size() - at);
             put(b, tabs.data(), tabs.size() * sizeof(StvDTab));
             hd.grouped = grouped ? 1 : 0;
-            if (grouped) std::memcpy(&b[ops_at], grecs.data(), grecs.size() * sizeof(StvGroup));
+            if (grouped) {
+                // a group left with no sub-ops (only predicated X flips) folds into the previous
+                // group's scatter: flips commute with nothing in between (they follow all of its
+                // ops), and their controls must be fixed for that group's vectors
+                for (size_t i = 1; i < grecs.size();) {
+                    StvGroup &G2 = grecs[i], &G1 = grecs[i - 1];
+                    bool ok = G2.nsub == 0 && G1.nflip_s + G2.nflip_g + G2.nflip_s <= STV_MAX_FLIPS;
+                    auto ctl_ok = [&](uint32_t f) {
+                        if (f & (1u << 16)) return true;
+                        const uint32_t raw = f >> 17;
+                        for (int j = 0; j < 4; ++j)
+                            if (raw == (1u << G1.tpos[j])) return false;     // varies in G1's vectors
+                        return true;
+                    };
+                    for (int q = 0; q < G2.nflip_g && ok; ++q)
+                        ok = ctl_ok(G2.flip[q]) && !(G1.pair16 && (G2.flip[q] & 1u));
+                    for (int q = 0; q < G2.nflip_s && ok; ++q)
+                        ok = ctl_ok(G2.flip[STV_MAX_FLIPS + q]) && !(G1.pair16 && (G2.flip[STV_MAX_FLIPS + q] & 1u));
+                    if (!ok) { ++i; continue; }
+                    for (int q = 0; q < G2.nflip_g; ++q) G1.flip[STV_MAX_FLIPS + G1.nflip_s++] = G2.flip[q];
+                    for (int q = 0; q < G2.nflip_s; ++q) G1.flip[STV_MAX_FLIPS + G1.nflip_s++] = G2.flip[STV_MAX_FLIPS + q];
+                    grecs.erase(grecs.begin() + (long)i);
+                }
+                hd.nops = (int)grecs.size();
+                std::memcpy(&b[ops_at], grecs.data(), grecs.size() * sizeof(StvGroup));
+            }
             else std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
             (void)esz;
         } else if (ps.kind == PASS_DIAG) {

@@ -39,7 +39,8 @@ class Sub(ct.Structure):
 class Group(ct.Structure):
     _fields_ = [("nsub", ct.c_int32), ("sub_off", ct.c_uint32), ("nvb", ct.c_int32), ("pair16", ct.c_int32),
                 ("tpos", ct.c_int32 * 4), ("sw_off", ct.c_uint32 * 16), ("vbit", (ct.c_uint32 * 2) * (MAXT - 4)),
-                ("vtab_off", ct.c_uint32), ("pad", ct.c_uint32 * 3)]
+                ("vtab_off", ct.c_uint32), ("nflip_g", ct.c_int32), ("nflip_s", ct.c_int32), ("pad", ct.c_int32),
+                ("flip", ct.c_uint32 * 16)]
 
 
 class DTab(ct.Structure):
@@ -58,7 +59,7 @@ class Pass(ct.Structure):
 
 
 assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
-assert ct.sizeof(Group) == 192 and ct.sizeof(DTab) == 48
+assert ct.sizeof(Group) == 256 and ct.sizeof(DTab) == 48
 
 U2_PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
 
@@ -150,6 +151,35 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
     """Apply one encoded gate group: local bit k <-> tile position tpos[k]."""
     G = [pos2phys[g.tpos[i]] for i in range(4)]
     assert len(set(g.sw_off[l] for l in range(16))) == 16
+
+    # inverse of the swizzle on single tile positions: flipped position from its swizzled offset
+    c128_ = c128
+    def swz(i):
+        H = [3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7]
+        def h(x):
+            r, j = 0, 0
+            while x:
+                if x & 1:
+                    r ^= H[j]
+                x >>= 1
+                j += 1
+            return r
+        if c128_:
+            return i ^ h(i >> 3)
+        c = i >> 1
+        return ((c ^ h(c >> 3)) << 1) | (i & 1)
+    pos_of = {swz(1 << q): q for q in range(P.S)}
+
+    def flips(psi, first, cnt):
+        for q in range(cnt):
+            f = g.flip[first + q]
+            tpos, a = pos_of[f & 0xFFFF], f >> 17
+            ctl = a if f & (1 << 16) else pos2phys[a.bit_length() - 1]
+            assert f & (1 << 16) or (a & (a - 1)) == 0
+            psi = PI._cnot(psi, n, ctl, pos2phys[tpos])
+        return psi
+
+    psi = flips(psi, 0, g.nflip_g)
     for k in range(g.nsub):
         sb = _at(blob, Sub, po + g.sub_off + 16 * k)
         c = sb.code & 0xFF
@@ -259,4 +289,4 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
                     on = on * _bits(j, -2 - t.a)
                 ph += on * np.uint64(t.ang)
             psi = _phase_apply(psi, ph)
-    return psi
+    return flips(psi, 8, g.nflip_s)

@@ -246,7 +246,7 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
         if P.kind != 1 or not P.grouped:
             continue
         for gi in range(P.nops):
-            g = BE._at(blob, BE.Group, po + P.ops_off + 192 * gi)
+            g = BE._at(blob, BE.Group, po + P.ops_off + 256 * gi)
             ngroups += 1
             assert g.nvb == P.S - 4
             assert bool(g.pair16) == (not c128 and g.tpos[0] == 0)
@@ -302,3 +302,24 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
                     assert len(banks) == min(want, v0 + lanes if v0 + lanes <= (1 << g.nvb) else (1 << g.nvb) - v0), \
                         (case, gi, l, v0)
     assert ngroups > 0
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_flips_never_split_a_16B_pair(seed):
+    """Predicated X flips folded into gather/scatter addresses (pass_format.h StvGroup.flip) must
+    keep 16-B pair accesses aligned: a complex64 group that reads amplitude pairs never carries a
+    flip of tile position 0; and the emulated blob still reproduces the oracle."""
+    circ = C.qft_circuit(12, tail=200, seed=seed) if seed % 2 else \
+        C.random_circuit(12, 250, seed, kinds=["cnot", "h", "cphase", "x", "cz", "t"])
+    blob, offs = stv.plan_blob(circ.n, circ.gates)
+    for po in offs:
+        P = BE._at(blob, BE.Pass, po)
+        if P.kind != 1 or not P.grouped:
+            continue
+        for i in range(P.nops):
+            g = BE._at(blob, BE.Group, po + P.ops_off + 256 * i)
+            fl = [g.flip[q] for q in range(g.nflip_g)] + [g.flip[8 + q] for q in range(g.nflip_s)]
+            assert not (g.pair16 and any(f & 1 for f in fl))
+    plan = stv.plan_json(circ.n, circ.gates)
+    psi = PI.logical(plan, BE.run(circ.n, blob, offs, x0=circ.x0))
+    assert np.max(np.abs(psi - oracle.run(circ))) < 2e-6

@@ -12,7 +12,7 @@ for pi,po in enumerate(offs):
   print('pass',pi,'kind',P.kind,'S',P.S,'L',P.L,'h',P.h,'hpos',list(P.hpos)[:P.h],'nops',P.nops,'ntab',P.ntab,'rec',P.rec_bytes)
   if not P.grouped: continue
   for i in range(P.nops):
-    op=B._at(blob,B.Group,po+P.ops_off+192*i)
+    op=B._at(blob,B.Group,po+P.ops_off+256*i)
     s=[]
     for k in range(op.nsub):
       sb=B._at(blob,B.Sub,po+op.sub_off+16*k)

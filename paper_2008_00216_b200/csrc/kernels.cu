@@ -774,19 +774,60 @@ struct __align__(16) RecParam {
     uint8_t b[STV_REC_PARAM_BYTES];
 };
 
+// Group diagonal tables.  Half tables (every term on one register bit) have only
+// per-tile CONSTANT terms: their entries are static and built once per CTA
+// (prologue); per tile only the scalar exp(i cst) is refreshed (scal[t], applied
+// with the table).  Full tables carry per-index-bit per-tile coefficients and are
+// rebuilt per tile: lane b < 7 reduces the terms on index bit b, lane 31 the
+// constant; one warp per table.
 template <typename C, int NT>
 __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, const uint8_t *__restrict__ grec,
-                                             uint64_t fb, typename TabEnt<C>::T *__restrict__ tables, int ctid) {
+                                             uint64_t fb, typename TabEnt<C>::T *__restrict__ tables,
+                                             C *__restrict__ scal, int ctid, bool prologue) {
     const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
     const int ntab = P->ntab;
-    const int lane = ctid & 31;
-    for (int t = ctid >> 5; t < ntab; t += NT / 32) {
+    const int lane = ctid & 31, warp = ctid >> 5;
+    if (prologue) {   // static entries: half tables, and full tables without per-tile terms
+        for (int t = warp; t < ntab; t += NT / 32) {
+            const StvDTab &d = tabs[t];
+            if (!d.half && d.nterm) continue;
+            const uint64_t *stat = (const uint64_t *)(grec + d.stat_off);
+            const int lb4 = d.half ? 3 : 4, stride = d.half ? STV_TAB_STRIDE_H : STV_TAB_STRIDE;
+            for (int e = lane; e < ((1 << lb4) << d.m); e += 32)
+                tables[d.ent_off + (uint32_t)(e >> lb4) * stride + (e & ((1 << lb4) - 1))] =
+                    unit_phase<C>(__ldg(stat + e));
+        }
+        return;
+    }
+    // per tile: work items (a half table's scalar, or 32 entries of a full table with
+    // per-tile terms) dealt round-robin to the warps, so one large table does not
+    // serialise the build behind one warp
+    int item = 0;
+    for (int t = 0; t < ntab; ++t) {
         const StvDTab &d = tabs[t];
-        const uint64_t *stat = (const uint64_t *)(grec + d.stat_off);
+        const int nterm = d.nterm;
+        if (!nterm) continue;
         const StvTerm *tm = (const StvTerm *)((const uint8_t *)P + d.term_off);
-        const int lb4 = d.half ? 3 : 4, stride = d.half ? STV_TAB_STRIDE_H : STV_TAB_STRIDE;
-        const int ne = (1 << lb4) << d.m, nterm = d.nterm;
-        // per-tile coefficients: lane b < 4 + m sums the terms on index bit b, lane 31 the constant
+        if (d.half) {
+            if ((item++ & (NT / 32 - 1)) != warp) continue;
+            uint64_t lam = 0;                              // constant terms only
+            for (int i = lane; i < nterm; i += 32) {
+                const StvTerm q = tm[i];
+                if (!((fb >> q.b) & 1)) continue;
+                if (q.a <= -2 && !((fb >> (-2 - q.a)) & 1)) continue;
+                lam += q.ang;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) lam += __shfl_xor_sync(0xffffffffu, lam, o);
+            if (lane == 0) scal[t] = unit_phase<C>(lam);
+            continue;
+        }
+        const int ne = 16 << d.m, nit = (ne + 31) >> 5;
+        const int mine = (warp - item) & (NT / 32 - 1);    // first chunk of this table dealt to this warp
+        item += nit;
+        if (mine >= nit) continue;
+        const uint64_t *stat = (const uint64_t *)(grec + d.stat_off);
+        // lane b < 4 + m sums the terms on index bit b, lane 31 the constant
         uint64_t lam = 0;
         for (int i = 0; i < nterm; ++i) {
             const StvTerm q = tm[i];
@@ -799,12 +840,12 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
         uint64_t lb[7];
 #pragma unroll
         for (int b = 0; b < 7; ++b) lb[b] = __shfl_sync(0xffffffffu, lam, b);
-        for (int e = lane; e < ne; e += 32) {
+        for (int e = (mine << 5) | lane; e < ne; e += NT) {
             uint64_t ph = __ldg(stat + e) + cst;
 #pragma unroll
             for (int b = 0; b < 7; ++b)
                 if ((e >> b) & 1) ph += lb[b];
-            tables[d.ent_off + (uint32_t)(e >> lb4) * stride + (e & ((1 << lb4) - 1))] = unit_phase<C>(ph);
+            tables[d.ent_off + (uint32_t)(e >> 4) * STV_TAB_STRIDE + (e & 15)] = unit_phase<C>(ph);
         }
     }
 }
@@ -869,13 +910,15 @@ __device__ __forceinline__ void g_u2x2(C (&x)[16], const C (&ma)[16], const C (&
 
 // half-table diagonal: amplitudes with local bit J set times row[l without bit J]
 template <int J, typename C>
-__device__ __forceinline__ void g_diagh(C (&x)[16], const C *__restrict__ row) {
+__device__ __forceinline__ void g_diagh(C (&x)[16], const C *__restrict__ row, bool with_scalar, C sc) {
 #pragma unroll
     for (int l = 0; l < 16; ++l) {
         if (!(l & (1 << J))) continue;
         const int c = ((l >> (J + 1)) << J) | (l & ((1 << J) - 1));
-        if constexpr (sizeof(C) == 8) *(float2 *)&x[l] = cmul1(*(const float2 *)&row[c], *(float2 *)&x[l]);
-        else x[l] = cmul(x[l], row[c]);
+        C f = row[c];
+        if (with_scalar) f = cmul(f, sc);
+        if constexpr (sizeof(C) == 8) *(float2 *)&x[l] = cmul1(*(const float2 *)&f, *(float2 *)&x[l]);
+        else x[l] = cmul(x[l], f);
     }
 }
 
@@ -885,7 +928,7 @@ template <typename C, int NV>
 __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[NV], const StvSub *__restrict__ subs,
                                          int nsub, const uint8_t *__restrict__ mat, const StvDTab *__restrict__ tabs,
                                          const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base,
-                                         uint32_t tord, uint64_t rank_bits) {
+                                         uint32_t tord, uint64_t rank_bits, const C *__restrict__ scal) {
     constexpr bool kPacked = sizeof(C) == 8;
     for (int k = 0; k < nsub; ++k) {
         const uint2 ca = *(const uint2 *)&subs[k];         // code, arg: one LDCU.64
@@ -1003,11 +1046,13 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
 #pragma unroll
                 for (int q = 0; q < STV_MAX_VBITS_H; ++q) r |= ((braw[i] & d.vraw[q]) ? 1u : 0u) << q;
                 const typename TabEnt<C>::T *row = tables + eo + r * STV_TAB_STRIDE_H;
+                const bool ws = d.nterm != 0;
+                const C sc = ws ? scal[ca.y] : C();
                 switch (code - SUBC_DIAGH) {
-                case 0: g_diagh<0>(x[i], row); break;
-                case 1: g_diagh<1>(x[i], row); break;
-                case 2: g_diagh<2>(x[i], row); break;
-                default: g_diagh<3>(x[i], row); break;
+                case 0: g_diagh<0>(x[i], row, ws, sc); break;
+                case 1: g_diagh<1>(x[i], row, ws, sc); break;
+                case 2: g_diagh<2>(x[i], row, ws, sc); break;
+                default: g_diagh<3>(x[i], row, ws, sc); break;
                 }
             }
         } else {
@@ -1049,7 +1094,8 @@ template <typename C, int NT, int NV>
 __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
                                              const uint8_t *__restrict__ mat,
                                              const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base,
-                                             uint32_t tord, const uint8_t *__restrict__ grec, int ctid) {
+                                             uint32_t tord, const uint8_t *__restrict__ grec,
+                                             const C *__restrict__ scal, int ctid) {
     constexpr int TB = NT == 128 ? 7 : 8;   // log2(NT)
     static_assert((1 << TB) == NT, "NT must be 128 or 256");
     const int nvb = g.nvb;
@@ -1139,7 +1185,7 @@ __device__ __forceinline__ void group_vec_op(C *__restrict__ tile, const StvGrou
                 for (int l = 0; l < 16; ++l) x[i][l] = tile[bsw_g[i] ^ so[l]];
             }
         }
-        run_subs<C, NV>(x, braw, subs, nsub, mat, tabs, tables, full_base, tord, P->rank_bits);
+        run_subs<C, NV>(x, braw, subs, nsub, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
             if (i > 0 && !live1) continue;
@@ -1242,8 +1288,9 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
     const uint32_t esz = sizeof(C);
     const uint32_t tab_pad = (P->tab_entries * esz + 127u) & ~127u;
     uint8_t *hk = smem;                                                    // 1024 B: chunk hashes
-    typename TabEnt<C>::T *tables = (typename TabEnt<C>::T *)(smem + 1024);
-    C *tiles = (C *)(smem + 1024 + tab_pad);
+    C *scal = (C *)(smem + 1024);                                          // 512 B: half-table scalars
+    typename TabEnt<C>::T *tables = (typename TabEnt<C>::T *)(smem + 1536);
+    C *tiles = (C *)(smem + 1536 + tab_pad);
     const uint32_t tile_elems = 1u << S;
     const uint32_t run_bytes = (1u << L) * esz;
     const uint32_t nruns = 1u << h;
@@ -1253,6 +1300,7 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
     uint64_t hmask = 0;
     for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
     const CopyPlan cp = make_copy_plan<NT>(hmask, run_bytes, nruns, tid);
+    if (ntab && nops) build_tables<C, NT>(P, grec, 0, tables, scal, tid, true);   // static table entries
     __syncthreads();
 
     const uint32_t first = blockIdx.x, stride = gridDim.x;
@@ -1279,11 +1327,11 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t full_base = base | rank_bits;
         if (ntab && nops) {
-            build_tables<C, NT>(P, grec, full_base, tables, tid);
+            build_tables<C, NT>(P, grec, full_base, tables, scal, tid, false);
             __syncthreads();
         }
         for (int o = 0; o < nops; ++o) {
-            group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, first + j * stride, grec, tid);
+            group_vec_op<C, NT, NV>(tile, groups[o], P, mat, tables, full_base, first + j * stride, grec, scal, tid);
             __syncthreads();
         }
         if (!(dbg_flags & 2))
@@ -1625,7 +1673,7 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
     static const int cfg = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
     (void)flops_per_amp;
     const int ns = cfg == 2 ? 3 : kGStagesDefault;
-    const size_t smem = 1024 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)ns * (esz << S);
+    const size_t smem = 1536 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)ns * (esz << S);
     const uint64_t ntiles = 1ull << (n_local - S);
     if (smem > 227 * 1024 || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
     static thread_local RecParam rp;

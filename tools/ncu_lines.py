@@ -29,3 +29,7 @@ top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 print('total', tot, 'samples', ts)
 for l, n in agg.most_common(top):
     print('%6.2f%% %6.2f%%  L%-5s %s' % (100 * n / tot, 100 * samp[l] / ts, l, (src[l - 1].strip()[:80] if l > 0 else ('<crt line %d>' % -l)) if l else ''))
+if len(sys.argv) > 4 and sys.argv[4] == 'samples':
+    print('--- by stall samples')
+    for l, n in samp.most_common(top):
+        print('%6.2f%% %6.2f%%  L%-5s %s' % (100 * agg[l] / tot, 100 * n / ts, l, (src[l - 1].strip()[:80] if l > 0 else ('<crt line %d>' % -l)) if l else ''))

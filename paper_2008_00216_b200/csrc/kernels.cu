@@ -1271,8 +1271,8 @@ __device__ __forceinline__ void tile_copy_fast(uint8_t *gstate, uint8_t *stile, 
     }
 }
 
-template <typename R, int NT, int NV, int kGStages>
-__global__ void __launch_bounds__(NT, sizeof(R) == 4 ? 3 : 2)
+template <typename R, int NT, int NV, int kGStages, int kMinB>
+__global__ void __launch_bounds__(NT, kMinB)
 k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off,
              uint32_t ntiles, int dbg_flags, const __grid_constant__ RecParam rec) {
     using C = typename C2T<R>::T;
@@ -1321,9 +1321,16 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
     uint64_t base = pdep64(first, out_mask);
     for (uint32_t j = 0; j < my_tiles; ++j) {
         const int s = (int)(j % kGStages);
-        cp_async_wait_n<kGStages - 2>();
-        __syncthreads();                                 // tile j visible; stage (j-1)%kGStages free
-        issue((int)((j + kGStages - 1) % kGStages));
+        if constexpr (kGStages == 1) {                   // no ring: other CTAs on the SM overlap the copy
+            if (j) __syncthreads();                      // previous tile's write-back reads are done
+            issue(0);
+            cp_async_wait0();
+            __syncthreads();
+        } else {
+            cp_async_wait_n<kGStages - 2>();
+            __syncthreads();                             // tile j visible; stage (j-1)%kGStages free
+            issue((int)((j + kGStages - 1) % kGStages));
+        }
         C *tile = tiles + (size_t)s * tile_elems;
         const uint64_t full_base = base | rank_bits;
         if (ntab && nops) {
@@ -1645,21 +1652,21 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
     return e;
 }
 
-template <typename R, int NT, int NV, int NS>
+template <typename R, int NT, int NV, int NS, int MB = sizeof(R) == 4 ? 3 : 2>
 static cudaError_t group_launch(void *state, const uint8_t *dblob, uint32_t pass_off, uint32_t ntiles, size_t smem,
                                 const RecParam &rp, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_group_pass<R, NT, NV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_group_pass<R, NT, NV, NS, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_pass<R, NT, NV, NS>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_group_pass<R, NT, NV, NS, MB>, NT, smem);
     if (occ < 1) return cudaErrorInvalidConfiguration;
     uint64_t grid = (uint64_t)num_sms() * occ;
     if (grid > ntiles) grid = ntiles;
     static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
-    k_group_pass<R, NT, NV, NS><<<(unsigned)grid, NT, smem, st>>>((typename C2T<R>::T *)state, dblob, pass_off,
+    k_group_pass<R, NT, NV, NS, MB><<<(unsigned)grid, NT, smem, st>>>((typename C2T<R>::T *)state, dblob, pass_off,
                                                                    ntiles, dbg, rp);
     return cudaGetLastError();
 }
@@ -1669,10 +1676,12 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
                               cudaStream_t st, int *kernels) {
     const size_t esz = c128 ? 16 : 8;
     // tuning knob STV_GCFG (measured on c2): 0 = 256 threads x 1 vector,
-    // 2 stages (default, best); 1 = 128 threads x 2 vectors; 2 = 3 stages
+    // one tile buffer, 4 CTAs/SM at 64 registers (default, best: the other CTAs of the SM hide
+    // each CTA's tile load); 1 = 128 threads x 2 vectors; 2 = 3-stage ring; 3 = 2-stage ring,
+    // 3 CTAs/SM at 80 registers (the previous default)
     static const int cfg = getenv("STV_GCFG") ? atoi(getenv("STV_GCFG")) : 0;
     (void)flops_per_amp;
-    const int ns = cfg == 2 ? 3 : kGStagesDefault;
+    const int ns = c128 ? kGStagesDefault : cfg == 0 ? 1 : cfg == 2 ? 3 : kGStagesDefault;
     const size_t smem = 1536 + (((size_t)tab_entries * esz + 127u) & ~(size_t)127) + (size_t)ns * (esz << S);
     const uint64_t ntiles = 1ull << (n_local - S);
     if (smem > 227 * 1024 || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
@@ -1682,7 +1691,8 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
     if (c128) e = group_launch<double, 128, 1, kGStagesDefault>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
     else if (cfg == 1) e = group_launch<float, 128, 2, kGStagesDefault>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
     else if (cfg == 2) e = group_launch<float, 256, 1, 3>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
-    else e = group_launch<float, 256, 1, kGStagesDefault>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    else if (cfg == 3) e = group_launch<float, 256, 1, 2>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
+    else e = group_launch<float, 256, 1, 1, 4>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
     ++*kernels;
     return e;
 }

@@ -306,7 +306,15 @@ def main():
 
     # e2e: host gate list in, full state vector out (pinned host memory)
     e2e = None
-    if args.e2e_steps > 0:
+    try:   # the full-state read-back needs a pinned host copy of the state: skip it when it cannot fit
+        import psutil
+        host_ok = (esz << n_local) * 1.5 < psutil.virtual_memory().available
+    except Exception:
+        host_ok = True
+    if args.e2e_steps > 0 and not host_ok:
+        e2e = {"value": None, "unit": UNIT, "skipped": "pinned host copy of the %d-GiB state does not fit host RAM"
+               % ((esz << n_local) >> 30)}
+    if args.e2e_steps > 0 and host_ok:
         host = torch.empty((1 << n_local) * esz, dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
         ee0 = torch.cuda.Event(enable_timing=True)

@@ -542,7 +542,7 @@ sv_status sv_sample(sv_state *s, uint64_t seed, size_t shots, uint64_t *out) {
     rmass[(size_t)s->rank] = pre[nch];
     if (s->world > 1) {
         double *d = nullptr;
-        cudaMalloc(&d, s->world * sizeof(double));
+        if (cudaMalloc(&d, s->world * sizeof(double)) != cudaSuccess) { cleanup(); return fail(SV_ERR_OUT_OF_MEMORY, "sample"); }
         cudaMemcpyAsync(d, rmass.data(), s->world * sizeof(double), cudaMemcpyHostToDevice, s->stream);
         int r = g_nccl.allReduce(d, d, (size_t)s->world, ncclFloat64, ncclSum, s->comm, s->stream);
         cudaMemcpyAsync(rmass.data(), d, s->world * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
@@ -599,7 +599,7 @@ sv_status sv_sample(sv_state *s, uint64_t seed, size_t shots, uint64_t *out) {
     }
     if (s->world > 1) {   // every rank returns all samples: sum of the per-rank arrays
         uint64_t *d = nullptr;
-        cudaMalloc(&d, shots * 8);
+        if (cudaMalloc(&d, shots * 8) != cudaSuccess) { cleanup(); return fail(SV_ERR_OUT_OF_MEMORY, "sample"); }
         cudaMemcpyAsync(d, res.data(), shots * 8, cudaMemcpyHostToDevice, s->stream);
         int r = g_nccl.allReduce(d, d, shots, 5 /*ncclUint64*/, ncclSum, s->comm, s->stream);
         cudaMemcpyAsync(res.data(), d, shots * 8, cudaMemcpyDeviceToHost, s->stream);

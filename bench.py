@@ -150,19 +150,41 @@ def roof(gbs, hbm, peak_kind, tflops, fp32_peak, tile_bytes, launches, tile_ms, 
 
 
 # ---------------------------------------------------------------------------
+def oracle_fit(circ):
+    """(n, gates, x0, note) for timing the complex128 oracle on the host: the workload itself
+    when its 16 * 2^n-byte state fits in 40% of the available host RAM, else the same circuit
+    restricted to its lowest n' qubits (gates touching higher qubits dropped) -- the metric is
+    per amplitude, so the rate is comparable."""
+    n = circ.n
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 1 << 62
+    m = n
+    while m > 10 and (16 << m) > 0.4 * avail:
+        m -= 1
+    if m == n:
+        return n, list(circ.gates), circ.x0, ""
+    gates = [g for g in circ.gates if all(q < m for q in g[1])]
+    return m, gates, circ.x0 & ((1 << m) - 1), \
+        f"; the n={n} complex128 state exceeds host RAM, so the circuit restricted to qubits 0..{m - 1}"
+
+
 def oracle_sample(circ, ngates, threads):
     """Time the CPU oracle (as it stands) on the first `ngates` gates of circ."""
     import numpy as np
     import oracle
-    n = circ.n
+    n, gates, x0, note = oracle_fit(circ)
     psi = np.empty(1 << n, dtype=np.complex128)
     lib = oracle.lib()
-    arr, keep = oracle._marshal(circ.gates[:ngates])
+    ngates = min(ngates, len(gates))
+    arr, keep = oracle._marshal(gates[:ngates])
     t0 = time.perf_counter()
-    lib.oracle_run(n, circ.x0, psi.ctypes.data, arr, ngates, threads)
+    lib.oracle_run(n, x0, psi.ctypes.data, arr, ngates, threads)
     t = time.perf_counter() - t0
     del psi
-    return t
+    return t, n, ngates, note
 
 
 def cpu_cores():
@@ -178,18 +200,18 @@ def run_reference(args, circ):
     import numpy as np
     import oracle
     cores = cpu_cores()
-    n = circ.n
+    n, ogates, x0, note = oracle_fit(circ)
     gpp = 4                                  # gates per step (bounded sample)
     psi = np.empty(1 << n, dtype=np.complex128)
     lib = oracle.lib()
     psi[:] = 0
-    psi[circ.x0] = 1
-    G = len(circ.gates)
+    psi[x0] = 1
+    G = len(ogates)
     pos = 0
 
     def step():
         nonlocal pos
-        gs = [circ.gates[(pos + i) % G] for i in range(gpp)]
+        gs = [ogates[(pos + i) % G] for i in range(gpp)]
         pos += gpp
         arr, keep = oracle._marshal(gs)
         lib.oracle_apply(n, psi.ctypes.data, arr, gpp, cores)
@@ -201,18 +223,19 @@ def run_reference(args, circ):
         step()
     t = time.perf_counter() - t0
     per_gate = t / (args.steps * gpp)
-    sec_circ = per_gate * G
-    value = G * 16 * (1 << n) / sec_circ / 1e9
+    value = 16 * (1 << n) / per_gate / 1e9            # per-amplitude rate of the timed sample
+    G = len(circ.gates)
+    sec_circ = G * 16 * (1 << circ.n) / (value * 1e9)  # the whole workload at that rate
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE.json configs[1] circuit)",
-            "config": {"workload": circ.name, "n": n, "gates": G, "state": "complex128 (oracle)",
+            "config": {"workload": circ.name, "n": circ.n, "gates": G, "state": "complex128 (oracle)",
                        "step": f"{gpp} gates of the circuit, gate by gate", "l2": "state 16 GiB >> L2"},
             "sec_per_circuit": sec_circ,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps} steps x {gpp} gates of {circ.name} (n={n}), complex128, "
-                                       f"{cores} OpenMP threads; sec/circuit extrapolated x{G}/gate"},
+                                       f"{cores} OpenMP threads; sec/circuit extrapolated x{G}/gate{note}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -343,11 +366,10 @@ def main():
         return
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        ng = args.oracle_gates
-        t = oracle_sample(circ, ng, cpu_cores())
-        cpu = {"value": ng * 16 * (1 << n) / t / 1e9, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+        t, on, ng, note = oracle_sample(circ, args.oracle_gates, cpu_cores())
+        cpu = {"value": ng * 16 * (1 << on) / t / 1e9, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
                "sample": f"first {ng} of {G} gates of {circ.name} (n={n}), complex128 gate-by-gate, "
-                         f"{cpu_cores()} OpenMP threads, {t:.2f} s",
+                         f"{cpu_cores()} OpenMP threads, {t:.2f} s{note}",
                "sec_per_circuit_extrapolated": t / ng * G}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

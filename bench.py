@@ -370,7 +370,7 @@ def main():
         cpu = {"value": ng * 16 * (1 << on) / t / 1e9, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
                "sample": f"first {ng} of {G} gates of {circ.name} (n={n}), complex128 gate-by-gate, "
                          f"{cpu_cores()} OpenMP threads, {t:.2f} s{note}",
-               "sec_per_circuit_extrapolated": t / ng * G}
+               "sec_per_circuit_extrapolated": t / ng * G * 2.0 ** (n - on)}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -930,41 +930,88 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
                                          const typename TabEnt<C>::T *__restrict__ tables, uint64_t full_base,
                                          uint32_t tord, uint64_t rank_bits, const C *__restrict__ scal) {
     constexpr bool kPacked = sizeof(C) == 8;
+    using R = decltype(x[0][0].x);
+    auto vsel = [&](uint32_t w) {   // 3 x 5-bit selectors: bits of the tile ordinal (31: always 0)
+        return ((tord >> (w & 31u)) & 1u) | (((tord >> ((w >> 5) & 31u)) & 1u) << 1) |
+               (((tord >> ((w >> 10) & 31u)) & 1u) << 2);
+    };
     for (int k = 0; k < nsub; ++k) {
         const uint2 ca = *(const uint2 *)&subs[k];         // code, arg: one LDCU.64
-        const int code = (int)(ca.x & 0xffu);
+        int code = (int)(ca.x & 0xffu);
         const C *M = (const C *)(mat + ca.y);
-        int u2 = code - SUBC_U2;
-        if ((unsigned)(code - SUBC_U2V) < 6u) {             // per-tile variant: selector bits of the tile ordinal
-            const uint32_t w = ca.x >> 8;
-            const uint32_t v = ((tord >> (w & 31u)) & 1u) | (((tord >> ((w >> 5) & 31u)) & 1u) << 1) |
-                               (((tord >> ((w >> 10) & 31u)) & 1u) << 2);
-            M += v * 16;
-            u2 = code - SUBC_U2V;
+        // a per-tile variant op runs the plain U2 case on the variant's matrix
+        if ((unsigned)(code - SUBC_U2V) < 6u) {
+            M += vsel(ca.x >> 8) * 16;
+            code -= SUBC_U2V - SUBC_U2;
         }
-        if ((unsigned)u2 < 6u) {                              // the common case first
-            switch (u2 + SUBC_U2) {
+        // one flat switch over the dense sub-op codes (a single indirect uniform branch)
+        switch (code) {
 #define STV_U2(p, a, b)                                                                     \
     case SUBC_U2 + (p): {                                                                   \
         C m[16];                                                                            \
         if constexpr (kPacked) {                                                            \
             _Pragma("unroll") for (int e = 0; e < 16; ++e)                                  \
                 *(float2 *)&m[e] = ld_c64((const float2 *)M + e);                           \
-        } else {                                                                            \
-            _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = M[e];                     \
-        }                                                                                   \
-        if constexpr (kPacked) {                                                            \
             _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
                 g_u2p<(a), (b)>(*(float2(*)[16]) & x[i], *(const float2(*)[16]) & m);      \
         } else {                                                                            \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = M[e];                     \
             _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u2<(a), (b)>(x[i], m);         \
         }                                                                                   \
         break;                                                                              \
     }
-                STV_U2(0, 0, 1) STV_U2(1, 0, 2) STV_U2(2, 0, 3) STV_U2(3, 1, 2) STV_U2(4, 1, 3) STV_U2(5, 2, 3)
+        STV_U2(0, 0, 1) STV_U2(1, 0, 2) STV_U2(2, 0, 3) STV_U2(3, 1, 2) STV_U2(4, 1, 3) STV_U2(5, 2, 3)
 #undef STV_U2
-            }
-        } else if (code == SUBC_DIAG) {   // per-tile table row of each vector's V-bits
+#define STV_UX2(p, a1, b1, a2, b2)                                                               \
+    case SUBC_U2X2 + (p): {   /* two U2 on complementary pairs */                                \
+        const C *MA = (const C *)(mat + ca.y) + vsel(ca.x >> 8) * 16;                            \
+        const C *MB = (const C *)(mat + subs[k].ctl) + vsel(subs[k].pad) * 16;                   \
+        C m[16];   /* one matrix live at a time (the pair of them exceeds the uniform registers) */ \
+        if constexpr (kPacked) {                                                                 \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) *(float2 *)&m[e] = ld_c64((const float2 *)MA + e); \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                       \
+                g_u2p<a1, b1>(*(float2(*)[16]) & x[i], *(const float2(*)[16]) & m);             \
+            asm volatile("" ::: "memory");                                                       \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) *(float2 *)&m[e] = ld_c64((const float2 *)MB + e); \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                       \
+                g_u2p<a2, b2>(*(float2(*)[16]) & x[i], *(const float2(*)[16]) & m);             \
+        } else {                                                                                 \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = MA[e];                         \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u2<a1, b1>(x[i], m);                \
+            _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = MB[e];                         \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u2<a2, b2>(x[i], m);                \
+        }                                                                                        \
+        break;                                                                                   \
+    }
+        STV_UX2(0, 0, 1, 2, 3) STV_UX2(1, 0, 2, 1, 3) STV_UX2(2, 0, 3, 1, 2)
+#undef STV_UX2
+#define STV_U1(a)                                                                           \
+    case SUBC_U1 + (a): {                                                                   \
+        if constexpr (kPacked) {                                                            \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
+                g_u1p<(a)>(*(float2(*)[16]) & x[i], (const float2 *)M);                     \
+        } else {                                                                            \
+            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u1<(a)>(x[i], M);               \
+        }                                                                                   \
+        break;                                                                              \
+    }
+        STV_U1(0) STV_U1(1) STV_U1(2) STV_U1(3)
+#undef STV_U1
+#define STV_CX(c, t)                                                                             \
+    case SUBC_CNOT + 4 * ((c) + 1) + (t): {                                                      \
+        const uint32_t ctl = subs[k].ctl, raw = ctl & 0xffffu, ph = ctl >> 16;                   \
+        const bool pon = ph == 0 || ((full_base >> (ph - 1)) & 1);                               \
+        _Pragma("unroll") for (int i = 0; i < NV; ++i)                                           \
+            g_cnot<(c), (t)>(x[i], pon && (raw == 0 || (braw[i] & raw) != 0));                   \
+        break;                                                                                   \
+    }
+        STV_CX(-1, 0) STV_CX(-1, 1) STV_CX(-1, 2) STV_CX(-1, 3)
+        STV_CX(0, 1) STV_CX(0, 2) STV_CX(0, 3)
+        STV_CX(1, 0) STV_CX(1, 2) STV_CX(1, 3)
+        STV_CX(2, 0) STV_CX(2, 1) STV_CX(2, 3)
+        STV_CX(3, 0) STV_CX(3, 1) STV_CX(3, 2)
+#undef STV_CX
+        case SUBC_DIAG: {   // per-tile table row of each vector's V-bits
             const StvDTab &d = tabs[ca.y];
             const uint32_t v0 = d.vraw[0], v1 = d.vraw[1], v2 = d.vraw[2];
             const uint32_t eo = d.ent_off;
@@ -981,110 +1028,44 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
                     for (int l = 0; l < 16; ++l) x[i][l] = cmul(x[i][l], row[l]);
                 }
             }
-        } else if ((unsigned)(code - SUBC_U1R) < 10u) {    // real U1 / U2
-            using R = decltype(x[0][0].x);
-            const R *MRl = (const R *)(mat + ca.y);
-            if (code < SUBC_U2R) {
-#pragma unroll
-                for (int i = 0; i < NV; ++i) {
-                    switch (code - SUBC_U1R) {
-                    case 0: g_u1r<0>(x[i], MRl); break;
-                    case 1: g_u1r<1>(x[i], MRl); break;
-                    case 2: g_u1r<2>(x[i], MRl); break;
-                    default: g_u1r<3>(x[i], MRl); break;
-                    }
-                }
-            } else {
-                R m[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) m[e] = MRl[e];
-#pragma unroll
-                for (int i = 0; i < NV; ++i) {
-                    switch (code - SUBC_U2R) {
-                    case 0: g_u2r<0, 1>(x[i], m); break;
-                    case 1: g_u2r<0, 2>(x[i], m); break;
-                    case 2: g_u2r<0, 3>(x[i], m); break;
-                    case 3: g_u2r<1, 2>(x[i], m); break;
-                    case 4: g_u2r<1, 3>(x[i], m); break;
-                    default: g_u2r<2, 3>(x[i], m); break;
-                    }
-                }
-            }
-        } else if ((unsigned)(code - SUBC_U2X2) < 3u) {    // two U2 on complementary pairs
-            const uint32_t wa = ca.x >> 8, wb = subs[k].pad;
-            auto vsel = [&](uint32_t w) {
-                return ((tord >> (w & 31u)) & 1u) | (((tord >> ((w >> 5) & 31u)) & 1u) << 1) |
-                       (((tord >> ((w >> 10) & 31u)) & 1u) << 2);
-            };
-            const C *MA = (const C *)(mat + ca.y) + vsel(wa) * 16;
-            const C *MB = (const C *)(mat + subs[k].ctl) + vsel(wb) * 16;
-            C ma[16], mb[16];
-            if constexpr (kPacked) {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    *(float2 *)&ma[e] = ld_c64((const float2 *)MA + e);
-                    *(float2 *)&mb[e] = ld_c64((const float2 *)MB + e);
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) { ma[e] = MA[e]; mb[e] = MB[e]; }
-            }
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                switch (code - SUBC_U2X2) {
-                case 0: g_u2x2<0, 1, 2, 3>(x[i], ma, mb); break;
-                case 1: g_u2x2<0, 2, 1, 3>(x[i], ma, mb); break;
-                default: g_u2x2<0, 3, 1, 2>(x[i], ma, mb); break;
-                }
-            }
-        } else if ((unsigned)(code - SUBC_DIAGH) < 4u) {   // half table on local bit j
-            const StvDTab &d = tabs[ca.y];
-            const uint32_t eo = d.ent_off;
-#pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                uint32_t r = 0;
-#pragma unroll
-                for (int q = 0; q < STV_MAX_VBITS_H; ++q) r |= ((braw[i] & d.vraw[q]) ? 1u : 0u) << q;
-                const typename TabEnt<C>::T *row = tables + eo + r * STV_TAB_STRIDE_H;
-                const bool ws = d.nterm != 0;
-                const C sc = ws ? scal[ca.y] : C();
-                switch (code - SUBC_DIAGH) {
-                case 0: g_diagh<0>(x[i], row, ws, sc); break;
-                case 1: g_diagh<1>(x[i], row, ws, sc); break;
-                case 2: g_diagh<2>(x[i], row, ws, sc); break;
-                default: g_diagh<3>(x[i], row, ws, sc); break;
-                }
-            }
-        } else {
-            switch (code) {
-#define STV_U1(a)                                                                           \
-    case SUBC_U1 + (a): {                                                                   \
-        if constexpr (kPacked) {                                                            \
-            _Pragma("unroll") for (int i = 0; i < NV; ++i)                                  \
-                g_u1p<(a)>(*(float2(*)[16]) & x[i], (const float2 *)M);                     \
-        } else {                                                                            \
-            _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u1<(a)>(x[i], M);               \
-        }                                                                                   \
-        break;                                                                              \
-    }
-                STV_U1(0) STV_U1(1) STV_U1(2) STV_U1(3)
-#undef STV_U1
-#define STV_CX(c, t)                                                                             \
-    case SUBC_CNOT + 4 * ((c) + 1) + (t): {                                                      \
-        const uint32_t ctl = subs[k].ctl, raw = ctl & 0xffffu, ph = ctl >> 16;                   \
-        const bool pon = ph == 0 || ((full_base >> (ph - 1)) & 1);                               \
-        _Pragma("unroll") for (int i = 0; i < NV; ++i)                                           \
-            g_cnot<(c), (t)>(x[i], pon && (raw == 0 || (braw[i] & raw) != 0));                   \
+            break;
+        }
+#define STV_DH(j)                                                                                \
+    case SUBC_DIAGH + (j): {   /* half table on local bit j */                                   \
+        const StvDTab &d = tabs[ca.y];                                                           \
+        const uint32_t eo = d.ent_off;                                                           \
+        _Pragma("unroll") for (int i = 0; i < NV; ++i) {                                         \
+            uint32_t r = 0;                                                                      \
+            _Pragma("unroll") for (int q = 0; q < STV_MAX_VBITS_H; ++q)                          \
+                r |= ((braw[i] & d.vraw[q]) ? 1u : 0u) << q;                                     \
+            const typename TabEnt<C>::T *row = tables + eo + r * STV_TAB_STRIDE_H;               \
+            const bool ws = d.nterm != 0;                                                        \
+            const C sc = ws ? scal[ca.y] : C();                                                  \
+            g_diagh<(j)>(x[i], row, ws, sc);                                                     \
+        }                                                                                        \
         break;                                                                                   \
     }
-                STV_CX(-1, 0) STV_CX(-1, 1) STV_CX(-1, 2) STV_CX(-1, 3)
-                STV_CX(0, 1) STV_CX(0, 2) STV_CX(0, 3)
-                STV_CX(1, 0) STV_CX(1, 2) STV_CX(1, 3)
-                STV_CX(2, 0) STV_CX(2, 1) STV_CX(2, 3)
-                STV_CX(3, 0) STV_CX(3, 1) STV_CX(3, 2)
-#undef STV_CX
-            default: break;
-            }
+        STV_DH(0) STV_DH(1) STV_DH(2) STV_DH(3)
+#undef STV_DH
+#define STV_U1R(a)                                                                               \
+    case SUBC_U1R + (a): {                                                                       \
+        const R *MRl = (const R *)(mat + ca.y);                                                  \
+        _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u1r<(a)>(x[i], MRl);                    \
+        break;                                                                                   \
+    }
+        STV_U1R(0) STV_U1R(1) STV_U1R(2) STV_U1R(3)
+#undef STV_U1R
+#define STV_U2R(p, a, b)                                                                         \
+    case SUBC_U2R + (p): {                                                                       \
+        const R *MRl = (const R *)(mat + ca.y);                                                  \
+        R m[16];                                                                                 \
+        _Pragma("unroll") for (int e = 0; e < 16; ++e) m[e] = MRl[e];                            \
+        _Pragma("unroll") for (int i = 0; i < NV; ++i) g_u2r<(a), (b)>(x[i], m);                 \
+        break;                                                                                   \
+    }
+        STV_U2R(0, 0, 1) STV_U2R(1, 0, 2) STV_U2R(2, 0, 3) STV_U2R(3, 1, 2) STV_U2R(4, 1, 3) STV_U2R(5, 2, 3)
+#undef STV_U2R
+        default: break;
         }
     }
 }

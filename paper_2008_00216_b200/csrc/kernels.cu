@@ -1035,9 +1035,11 @@ __device__ __forceinline__ void run_subs(C (&x)[NV][16], const uint32_t (&braw)[
         const StvDTab &d = tabs[ca.y];                                                           \
         const uint32_t eo = d.ent_off;                                                           \
         _Pragma("unroll") for (int i = 0; i < NV; ++i) {                                         \
-            uint32_t r = 0;                                                                      \
-            _Pragma("unroll") for (int q = 0; q < STV_MAX_VBITS_H; ++q)                          \
-                r |= ((braw[i] & d.vraw[q]) ? 1u : 0u) << q;                                     \
+            uint32_t r = (braw[i] & d.vraw[0]) ? 1u : 0u;   /* m <= 1: the common case */        \
+            if (d.m > 1) {                                                                       \
+                _Pragma("unroll") for (int q = 1; q < STV_MAX_VBITS_H; ++q)                      \
+                    r |= ((braw[i] & d.vraw[q]) ? 1u : 0u) << q;                                 \
+            }                                                                                    \
             const typename TabEnt<C>::T *row = tables + eo + r * STV_TAB_STRIDE_H;               \
             const bool ws = d.nterm != 0;                                                        \
             const C sc = ws ? scal[ca.y] : C();                                                  \

@@ -916,9 +916,13 @@ __device__ __forceinline__ void g_diagh(C (&x)[16], const C *__restrict__ row, b
         if (!(l & (1 << J))) continue;
         const int c = ((l >> (J + 1)) << J) | (l & ((1 << J) - 1));
         C f = row[c];
-        if (with_scalar) f = cmul(f, sc);
-        if constexpr (sizeof(C) == 8) *(float2 *)&x[l] = cmul1(*(const float2 *)&f, *(float2 *)&x[l]);
-        else x[l] = cmul(x[l], f);
+        if constexpr (sizeof(C) == 8) {   // packed: FMUL2 + FFMA2 per complex product
+            if (with_scalar) *(float2 *)&f = cmul1(*(const float2 *)&sc, *(const float2 *)&f);
+            *(float2 *)&x[l] = cmul1(*(const float2 *)&f, *(float2 *)&x[l]);
+        } else {
+            if (with_scalar) f = cmul(f, sc);
+            x[l] = cmul(x[l], f);
+        }
     }
 }
 

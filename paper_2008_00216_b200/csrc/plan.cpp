@@ -1878,10 +1878,19 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                             if (raw == (1u << G1.tpos[j])) return false;     // varies in G1's vectors
                         return true;
                     };
+                    // the flipped position must be one of G1's register bits: a flip of a vector
+                    // bit would make G1's thread for vector v scatter into vector v^t's slots
+                    // (another thread's, with no barrier between gather and scatter)
+                    auto tgt_ok = [&](uint32_t f) {
+                        for (int j = 0; j < 4; ++j)
+                            if ((f & 0xffffu) == G1.sw_off[1u << j]) return true;
+                        return false;
+                    };
                     for (int q = 0; q < G2.nflip_g && ok; ++q)
-                        ok = ctl_ok(G2.flip[q]) && !(G1.pair16 && (G2.flip[q] & 1u));
+                        ok = ctl_ok(G2.flip[q]) && tgt_ok(G2.flip[q]) && !(G1.pair16 && (G2.flip[q] & 1u));
                     for (int q = 0; q < G2.nflip_s && ok; ++q)
-                        ok = ctl_ok(G2.flip[STV_MAX_FLIPS + q]) && !(G1.pair16 && (G2.flip[STV_MAX_FLIPS + q] & 1u));
+                        ok = ctl_ok(G2.flip[STV_MAX_FLIPS + q]) && tgt_ok(G2.flip[STV_MAX_FLIPS + q]) &&
+                             !(G1.pair16 && (G2.flip[STV_MAX_FLIPS + q] & 1u));
                     if (!ok) { ++i; continue; }
                     for (int q = 0; q < G2.nflip_g; ++q) G1.flip[STV_MAX_FLIPS + G1.nflip_s++] = G2.flip[q];
                     for (int q = 0; q < G2.nflip_s; ++q) G1.flip[STV_MAX_FLIPS + G1.nflip_s++] = G2.flip[STV_MAX_FLIPS + q];

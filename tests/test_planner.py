@@ -323,3 +323,26 @@ def test_flips_never_split_a_16B_pair(seed):
     plan = stv.plan_json(circ.n, circ.gates)
     psi = PI.logical(plan, BE.run(circ.n, blob, offs, x0=circ.x0))
     assert np.max(np.abs(psi - oracle.run(circ))) < 2e-6
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("tile_bits", [0, 13])
+def test_flip_targets_are_register_bits(seed, tile_bits):
+    """Every predicated X flip folded into a group's gather or scatter addresses targets one of
+    that group's 4 register bits (tpos): a flip of a vector bit would make the thread owning
+    vector v read or write vector v^t's slots, and the group pass has no barrier between gather
+    and scatter.  Covers flip-only groups merged into the previous group's scatter."""
+    circ = C.random_circuit(22, 400, seed, kinds=["cnot", "x", "h", "cz", "t", "sx"])
+    blob, offs = stv.plan_blob(circ.n, circ.gates, tile_bits=tile_bits)
+    seen = 0
+    for po in offs:
+        P = BE._at(blob, BE.Pass, po)
+        if P.kind != 1 or not P.grouped:
+            continue
+        for i in range(P.nops):
+            g = BE._at(blob, BE.Group, po + P.ops_off + 256 * i)
+            regs = {g.sw_off[1 << j] for j in range(4)}
+            fl = [g.flip[q] for q in range(g.nflip_g)] + [g.flip[8 + q] for q in range(g.nflip_s)]
+            seen += len(fl)
+            assert all((f & 0xFFFF) in regs for f in fl), (po, i)
+    assert seen > 0

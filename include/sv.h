@@ -159,15 +159,20 @@ sv_status sv_norm(sv_state *s, double *out);
 /* Measurement sampling ("Simulating
  * measurements is then straightforward"; SPEC S:L286-292 sample_measurement).
  *   out[s] (s < shots) = logical basis index j drawn with probability |a_j|^2 / sum |a|^2.
- * Draws: u_s = (splitmix64(seed + s) >> 11) * 2^-53 (counter-based, so the result is
- * deterministic given seed); the sample is the first index, in the state's STORAGE order
- * (physical order through the frame, rank-major across GPUs), at which the fp64 inclusive
- * cumulative sum of |a|^2 exceeds u_s * total; it is returned as a logical index.
- * Cumulative sums: 4096-amplitude chunks, each summed as 32 lanes x 128 consecutive
- * amplitudes then a fixed warp tree, chunk totals prefix-summed on the host in order.
+ * Definition, in LOGICAL index order (independent of the internal frame and of the
+ * partition): u_s = (splitmix64 output s+1 for `seed`, >> 11) * 2^-53 (counter-based,
+ * so the result is deterministic given seed); the sample is the first logical index j
+ * at which the cumulative sum of |a_0|^2 + ... + |a_j|^2 exceeds u_s * total.
+ * Evaluation: fp64 |a|^2 read through the frame; 4096-index chunks of 32 lanes x 128
+ * consecutive indices; chunk masses as a fixed warp tree, prefix-summed on the host in
+ * order; per shot the lane and then the index inside the lane by sequential scans (a
+ * rounding miss at a boundary falls back to the last index with mass).  The result can
+ * differ from the exact definition only where u_s * total lies within summation rounding
+ * of a cumulative-sum boundary.
  * out: caller host memory of `shots` uint64.  shots == 0 is a no-op.
  * Errors: SV_ERR_INVALID_ARG (NULL out with shots > 0, total mass <= 0 or not finite).
- * Distributed: collective; every rank returns all samples. */
+ * Distributed: collective (per-rank partial sums are all-reduced); every rank returns
+ * all samples. */
 sv_status sv_sample(sv_state *s, uint64_t seed, size_t shots, uint64_t *out);
 
 typedef struct {

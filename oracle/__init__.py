@@ -204,8 +204,8 @@ def timed_run(circuit, nthreads: int = 0, gates=None):
 # Measurement sampling ("Simulating
 # measurements is then straightforward").  The definition,
 # written out: the s-th draw takes u_s from the (s+1)-th output of splitmix64
-# seeded with `seed`, u_s = (out >> 11) * 2^-53, and returns the first index j, in
-# the given storage order, at which the fp64 cumulative sum of |a|^2 exceeds
+# seeded with `seed`, u_s = (out >> 11) * 2^-53, and returns the first LOGICAL index j
+# at which the fp64 cumulative sum of |a|^2 (in logical order) exceeds
 # u_s * total (inverse-CDF sampling; Born rule).  Plain numpy, no blocking.
 # ---------------------------------------------------------------------------
 _GAMMA = 0x9E3779B97F4A7C15
@@ -224,25 +224,12 @@ def uniforms(seed: int, shots: int) -> np.ndarray:
     return np.array([(splitmix64(seed, s) >> 11) * 2.0 ** -53 for s in range(shots)], dtype=np.float64)
 
 
-def storage_order(n: int, perm, xmask: int) -> np.ndarray:
-    """logical index of the amplitude stored at physical index p (frame: stored index
-    = P(j) xor xmask, P moving logical bit q to physical bit perm[q])."""
-    p = np.arange(1 << n, dtype=np.int64) ^ np.int64(xmask)
-    j = np.zeros(1 << n, dtype=np.int64)
-    for q in range(n):
-        j |= ((p >> perm[q]) & 1) << q
-    return j
-
-
-def sample(psi: np.ndarray, seed: int, shots: int, order=None) -> np.ndarray:
-    """Inverse-CDF samples of |psi|^2 (logical indices); `order[p]` = logical index of
-    the p-th amplitude in storage order (identity if None)."""
+def sample(psi: np.ndarray, seed: int, shots: int) -> np.ndarray:
+    """Inverse-CDF samples of |psi|^2 in logical index order (Born rule)."""
     prob = np.abs(np.asarray(psi, dtype=np.complex128)) ** 2
-    if order is not None:
-        prob = prob[order]
-    cdf = np.cumsum(prob)                      # sequential, storage order
+    cdf = np.cumsum(prob)                      # sequential, logical order
     total = cdf[-1]
     u = uniforms(seed, shots) * total
-    idx = np.searchsorted(cdf, u, side="right")  # first p with cdf[p] > u
+    idx = np.searchsorted(cdf, u, side="right")  # first j with cdf[j] > u
     idx = np.minimum(idx, prob.size - 1)
-    return (order[idx] if order is not None else idx).astype(np.uint64)
+    return idx.astype(np.uint64)

@@ -26,10 +26,10 @@ cudaError_t launch_tile_pass(bool c128, void *state, const uint8_t *dblob, uint3
                              uint32_t rec_bytes, int ntab, cudaStream_t st, int *kernels);
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,
                              cudaStream_t st, int *kernels);
-cudaError_t launch_sample_mass(bool c128, const void *state, uint64_t N, double *mass, uint64_t nchunks,
-                               cudaStream_t st, int *kernels);
-cudaError_t launch_sample_find(bool c128, const void *state, uint64_t N, const uint64_t *chunk, const double *res,
-                               uint64_t nshots, uint64_t *out, cudaStream_t st, int *kernels);
+cudaError_t launch_sample(int phase, bool c128, const void *state, const int32_t *perm, uint64_t xmask, int n,
+                          int n_local, uint64_t rank_bits, uint64_t count, const uint64_t *chunk, const double *res,
+                          double *a, int32_t *pick_lane, double *res2, double *vals, uint64_t *out, cudaStream_t st,
+                          int *kernels);
 cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off,
                               int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, double flops_per_amp,
                               cudaStream_t st, int *kernels);
@@ -242,6 +242,7 @@ sv_status sv_wrap(int n, sv_dtype dt, void *dev_buf, size_t bytes, void *stream,
 
 sv_status sv_create_virtual(int n, sv_dtype dt, int g, sv_state **out) {
     if (g < 0 || g > 3) return fail(SV_ERR_INVALID_ARG, "virtual shards: g in [0, 3]");
+    if (n - g < 4) return fail(SV_ERR_INVALID_ARG, "virtual shards: need at least 4 local qubits per shard (n - g >= 4)");
     sv_status st = sv_create(n, dt, out);
     if (st) return st;
     (*out)->n_global = g;
@@ -254,6 +255,8 @@ sv_status sv_create_dist(int n, sv_dtype dt, const void *uid, int rank, int worl
                          void *stream, sv_state **out) {
     if (world < 1 || (world & (world - 1)) || rank < 0 || rank >= world)
         return fail(SV_ERR_INVALID_ARG, "world must be a power of two, 0 <= rank < world");
+    if (world > 256)   // the remap swaps at most 8 bits at once (dist_remap's chunk tables)
+        return fail(SV_ERR_INVALID_ARG, "world must be <= 256");
     int g = 0;
     while ((1 << g) < world) ++g;
     sv_status st = make_state(n, dt, g, out);
@@ -522,90 +525,73 @@ sv_status sv_sample(sv_state *s, uint64_t seed, size_t shots, uint64_t *out) {
     if (st) return st;
     if (!shots) return SV_OK;
     if (!out) return fail(SV_ERR_INVALID_ARG, "out is NULL");
-    const uint64_t N = s->nloc_amps();
-    const uint64_t nch = (N + 4095) / 4096;
-    double *dmass = nullptr, *dres = nullptr;
+    // logical order: chunk c = logical indices [4096 c, 4096 (c + 1)) of all 2^n
+    const uint64_t NL = 1ull << s->n;
+    const uint64_t nch = (NL + 4095) / 4096;
+    const int nl = s->virt ? s->n : s->n_local;
+    const uint64_t rb = rank_value(s);
+    const uint64_t batch = std::min<uint64_t>(shots, 1ull << 16);
+    double *dmass = nullptr, *dres = nullptr, *dlanes = nullptr, *dres2 = nullptr, *dvals = nullptr;
     uint64_t *dchunk = nullptr, *dout = nullptr;
+    int32_t *dlane = nullptr;
     auto cleanup = [&]() {
-        cudaFree(dmass); cudaFree(dres); cudaFree(dchunk); cudaFree(dout);
+        cudaFree(dmass); cudaFree(dres); cudaFree(dlanes); cudaFree(dres2); cudaFree(dvals);
+        cudaFree(dchunk); cudaFree(dout); cudaFree(dlane);
     };
-    if (cudaMalloc(&dmass, nch * sizeof(double)) != cudaSuccess) { cleanup(); return fail(SV_ERR_OUT_OF_MEMORY, "sample"); }
+    auto allreduce = [&](double *d, size_t cnt) -> bool {   // distributed: sum the per-rank arrays
+        if (s->world < 2) return true;
+        return g_nccl.allReduce(d, d, cnt, ncclFloat64, ncclSum, s->comm, s->stream) == 0;
+    };
+    if (cudaMalloc(&dmass, nch * 8) || cudaMalloc(&dres, batch * 8) || cudaMalloc(&dlanes, batch * 32 * 8) ||
+        cudaMalloc(&dres2, batch * 8) || cudaMalloc(&dvals, batch * 128 * 8) || cudaMalloc(&dchunk, batch * 8) ||
+        cudaMalloc(&dout, batch * 8) || cudaMalloc(&dlane, batch * 4)) {
+        cleanup();
+        return fail(SV_ERR_OUT_OF_MEMORY, "sample scratch");
+    }
     int k = 0;
-    cudaError_t e = launch_sample_mass(s->c128(), s->buf, N, dmass, nch, s->stream, &k);
+    cudaError_t e = launch_sample(0, s->c128(), s->buf, s->perm, s->xmask, s->n, nl, rb, nch, nullptr, nullptr, dmass,
+                                  nullptr, nullptr, nullptr, nullptr, s->stream, &k);
+    if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample mass"); }
+    if (!allreduce(dmass, nch)) { cleanup(); s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (sample mass)"); }
     std::vector<double> mass(nch), pre(nch + 1, 0.0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(mass.data(), dmass, nch * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
+    e = cudaMemcpyAsync(mass.data(), dmass, nch * 8, cudaMemcpyDeviceToHost, s->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
     if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample mass"); }
-    for (uint64_t c = 0; c < nch; ++c) pre[c + 1] = pre[c] + mass[c];
-    // per-rank masses (distributed: every rank needs all of them)
-    std::vector<double> rmass((size_t)s->world, 0.0);
-    rmass[(size_t)s->rank] = pre[nch];
-    if (s->world > 1) {
-        double *d = nullptr;
-        if (cudaMalloc(&d, s->world * sizeof(double)) != cudaSuccess) { cleanup(); return fail(SV_ERR_OUT_OF_MEMORY, "sample"); }
-        cudaMemcpyAsync(d, rmass.data(), s->world * sizeof(double), cudaMemcpyHostToDevice, s->stream);
-        int r = g_nccl.allReduce(d, d, (size_t)s->world, ncclFloat64, ncclSum, s->comm, s->stream);
-        cudaMemcpyAsync(rmass.data(), d, s->world * sizeof(double), cudaMemcpyDeviceToHost, s->stream);
-        cudaStreamSynchronize(s->stream);
-        cudaFree(d);
-        if (r) { cleanup(); s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (sample mass)"); }
-    }
-    std::vector<double> rpre((size_t)s->world + 1, 0.0);
-    for (int r = 0; r < s->world; ++r) rpre[(size_t)r + 1] = rpre[(size_t)r] + rmass[(size_t)r];
-    const double total = rpre[(size_t)s->world];
+    for (uint64_t c = 0; c < nch; ++c) pre[c + 1] = pre[c] + mass[c];   // fp64, sequential, logical order
+    const double total = pre[nch];
     if (!(total > 0) || !std::isfinite(total)) { cleanup(); return fail(SV_ERR_INVALID_ARG, "state has no probability mass"); }
-    // route the shots: owner rank, chunk, residual
-    std::vector<uint64_t> mine, hchunk;
-    std::vector<double> hres;
-    for (size_t sh = 0; sh < shots; ++sh) {
-        const double u = (double)(splitmix_out(seed, sh) >> 11) * 0x1.0p-53;
-        const double target = u * total;
-        int owner = s->world - 1;
-        for (int r = 0; r < s->world; ++r)
-            if (target < rpre[(size_t)r + 1] && rmass[(size_t)r] > 0) { owner = r; break; }
-        while (owner > 0 && rmass[(size_t)owner] <= 0) --owner;
-        if (owner != s->rank) continue;
-        const double t = target - rpre[(size_t)owner];
-        // first chunk whose inclusive prefix exceeds t (clamped to the last chunk with mass)
-        uint64_t c = (uint64_t)(std::upper_bound(pre.begin() + 1, pre.end(), t) - (pre.begin() + 1));
-        if (c >= nch) c = nch - 1;
-        while (c > 0 && mass[c] <= 0) --c;
-        mine.push_back(sh);
-        hchunk.push_back(c);
-        hres.push_back(t - pre[c]);
-    }
-    std::vector<uint64_t> phys(mine.size());
-    if (!mine.empty()) {
-        const size_t m = mine.size();
-        if (cudaMalloc(&dchunk, m * 8) || cudaMalloc(&dres, m * 8) || cudaMalloc(&dout, m * 8)) {
-            cleanup();
-            return fail(SV_ERR_OUT_OF_MEMORY, "sample");
+    uint64_t last_nz = nch - 1;
+    while (last_nz > 0 && mass[last_nz] <= 0) --last_nz;
+    std::vector<uint64_t> hchunk(batch), res(shots);
+    std::vector<double> hres(batch);
+    for (size_t b0 = 0; b0 < shots; b0 += batch) {
+        const uint64_t m = std::min<uint64_t>(batch, shots - b0);
+        for (uint64_t i = 0; i < m; ++i) {
+            const double u = (double)(splitmix_out(seed, b0 + i) >> 11) * 0x1.0p-53;
+            const double target = u * total;
+            // first chunk whose inclusive prefix exceeds the target (clamped to the last chunk with mass)
+            uint64_t c = (uint64_t)(std::upper_bound(pre.begin() + 1, pre.end(), target) - (pre.begin() + 1));
+            if (c > last_nz) c = last_nz;
+            while (c > 0 && mass[c] <= 0) --c;
+            hchunk[i] = c;
+            hres[i] = target - pre[c];
         }
         e = cudaMemcpyAsync(dchunk, hchunk.data(), m * 8, cudaMemcpyHostToDevice, s->stream);
         if (e == cudaSuccess) e = cudaMemcpyAsync(dres, hres.data(), m * 8, cudaMemcpyHostToDevice, s->stream);
-        if (e == cudaSuccess) e = launch_sample_find(s->c128(), s->buf, N, dchunk, dres, m, dout, s->stream, &k);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(phys.data(), dout, m * 8, cudaMemcpyDeviceToHost, s->stream);
+        if (e == cudaSuccess)
+            e = launch_sample(1, s->c128(), s->buf, s->perm, s->xmask, s->n, nl, rb, m, dchunk, nullptr, dlanes,
+                              nullptr, nullptr, nullptr, nullptr, s->stream, &k);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample lanes"); }
+        if (!allreduce(dlanes, m * 32)) { cleanup(); s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (sample lanes)"); }
+        e = launch_sample(2, s->c128(), s->buf, s->perm, s->xmask, s->n, nl, rb, m, dchunk, dres, dlanes, dlane, dres2,
+                          dvals, nullptr, s->stream, &k);
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample values"); }
+        if (!allreduce(dvals, m * 128)) { cleanup(); s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (sample values)"); }
+        e = launch_sample(3, s->c128(), s->buf, s->perm, s->xmask, s->n, nl, rb, m, dchunk, nullptr, nullptr, dlane,
+                          dres2, dvals, dout, s->stream, &k);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(res.data() + b0, dout, m * 8, cudaMemcpyDeviceToHost, s->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
-        if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample find"); }
-    }
-    // physical -> logical through the frame
-    std::vector<uint64_t> res(shots, 0);
-    const uint64_t rb = s->virt ? 0 : (uint64_t)s->rank << s->n_local;
-    for (size_t i = 0; i < mine.size(); ++i) {
-        const uint64_t Q = (phys[i] | rb) ^ s->xmask;
-        uint64_t j = 0;
-        for (int q = 0; q < s->n; ++q) j |= ((Q >> s->perm[q]) & 1ull) << q;
-        res[mine[i]] = j;
-    }
-    if (s->world > 1) {   // every rank returns all samples: sum of the per-rank arrays
-        uint64_t *d = nullptr;
-        if (cudaMalloc(&d, shots * 8) != cudaSuccess) { cleanup(); return fail(SV_ERR_OUT_OF_MEMORY, "sample"); }
-        cudaMemcpyAsync(d, res.data(), shots * 8, cudaMemcpyHostToDevice, s->stream);
-        int r = g_nccl.allReduce(d, d, shots, 5 /*ncclUint64*/, ncclSum, s->comm, s->stream);
-        cudaMemcpyAsync(res.data(), d, shots * 8, cudaMemcpyDeviceToHost, s->stream);
-        cudaStreamSynchronize(s->stream);
-        cudaFree(d);
-        if (r) { cleanup(); s->poisoned = true; return fail(SV_ERR_NCCL, "ncclAllReduce (samples)"); }
+        if (e != cudaSuccess) { cleanup(); return cuda_fail(s, e, "sample pick"); }
     }
     std::memcpy(out, res.data(), shots * 8);
     cleanup();
@@ -737,6 +723,7 @@ namespace {
 sv_status dist_remap(sv_state *s, const std::vector<std::pair<int, int>> &swaps, int *kernels) {
     if (s->world < 2) return SV_OK;
     const int m = (int)swaps.size();
+    if (m < 1 || m > 8 || m > s->n_global) return fail(SV_ERR_INVALID_ARG, "remap: 1..min(8, g) swapped bits");
     uint32_t gbits = 0;
     int lbits[8];
     // pairs sorted by global bit so chunk value bit i <-> global bit i-th

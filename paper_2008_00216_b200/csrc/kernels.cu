@@ -1459,30 +1459,59 @@ __global__ void __launch_bounds__(STV_THREADS) k_norm_final(const double *part, 
 }
 
 // ---------------------------------------------------------------------------
-// measurement sampling (NEXT #3): chunk masses, then one warp per shot finds the
-// first index whose cumulative |a|^2 exceeds the shot's residual in its chunk.
-// Both kernels sum a chunk in the same order (lane-contiguous 128 amplitudes, then
-// a fixed shuffle tree), so chunk totals and in-chunk scans agree bit for bit.
+// measurement sampling (NEXT #3), over LOGICAL index order (include/sv.h):
+// logical chunk c = indices [4096 c, 4096 (c+1)); lane i of a warp owns the 128
+// consecutive logical indices 4096 c + 128 i + k.  Every |a_j|^2 is read through
+// the frame (physical p = P(j) xor xmask; P moves logical bit q to physical bit
+// perm[q]); amplitudes another rank owns count 0 (distributed: the per-rank
+// arrays are summed).  Lane sums are sequential over k in every kernel, so the
+// chunk masses, the per-shot lane sums and the in-lane scan add the same values
+// in the same order.
 // ---------------------------------------------------------------------------
 constexpr int kSampChunk = 4096;
 static int num_sms();
 
+struct SampMap {
+    uint64_t plo[128];     // P(k) for the low 7 logical bits (k < 128)
+    int32_t perm[64];      // logical qubit -> physical bit
+    uint64_t xmask;
+    uint64_t N;            // 2^n logical amplitudes
+    uint64_t lmask;        // local physical bits
+    uint64_t rank_bits;    // this rank's value of the physical bits >= n_local
+    int32_t n, n_local;
+};
+
+// physical index (xmask applied) of logical j with its low 7 bits cleared
+__device__ __forceinline__ uint64_t samp_base(const SampMap &m, uint64_t j) {
+    uint64_t p = m.xmask;
+    for (int q = 7; q < m.n; ++q) p ^= ((j >> q) & 1ull) << m.perm[q];
+    return p;
+}
+// |a_j|^2 of logical j = (base index) + k; 0 if j >= N or another rank owns it
 template <typename C>
-__device__ __forceinline__ double amp2(const C *__restrict__ st, uint64_t i, uint64_t N) {
-    if (i >= N) return 0.0;
-    const C a = st[i];
+__device__ __forceinline__ double samp_p(const C *__restrict__ st, const SampMap &m, uint64_t base, uint64_t j, int k) {
+    if (j >= m.N) return 0.0;
+    const uint64_t p = base ^ m.plo[k];
+    if ((p >> m.n_local) != m.rank_bits) return 0.0;
+    const C a = st[p & m.lmask];
     return (double)a.x * (double)a.x + (double)a.y * (double)a.y;
+}
+// sequential sum of the 128 values of (chunk c, lane)
+template <typename C>
+__device__ __forceinline__ double samp_lane_sum(const C *__restrict__ st, const SampMap &m, uint64_t c, int lane) {
+    const uint64_t j0 = c * kSampChunk + (uint64_t)lane * 128;
+    const uint64_t base = samp_base(m, j0);
+    double acc = 0;
+    for (int k = 0; k < 128; ++k) acc += samp_p(st, m, base, j0 + k, k);
+    return acc;
 }
 
 template <typename C>
-__global__ void __launch_bounds__(256) k_sample_mass(const C *__restrict__ st, uint64_t N, uint64_t nchunks,
-                                                     double *__restrict__ mass) {
+__global__ void __launch_bounds__(256) k_sample_mass(const C *__restrict__ st, const __grid_constant__ SampMap m,
+                                                     uint64_t nchunks, double *__restrict__ mass) {
     const int lane = threadIdx.x & 31;
-    const uint64_t per = kSampChunk / 32;
     for (uint64_t c = blockIdx.x * 8ull + (threadIdx.x >> 5); c < nchunks; c += gridDim.x * 8ull) {
-        const uint64_t b = c * kSampChunk + lane * per;
-        double acc = 0;
-        for (uint64_t k = 0; k < per; ++k) acc += amp2(st, b + k, N);
+        double acc = samp_lane_sum(st, m, c, lane);
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {                 // fixed tree
             const double v = __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1492,57 +1521,136 @@ __global__ void __launch_bounds__(256) k_sample_mass(const C *__restrict__ st, u
     }
 }
 
-// shot s: chunk[s], residual res[s] (u * total - prefix before the chunk) -> out[s] = physical index
+// per shot s: the 32 lane sums of its chunk
 template <typename C>
-__global__ void __launch_bounds__(256) k_sample_find(const C *__restrict__ st, uint64_t N, const uint64_t *chunk,
-                                                     const double *res, uint64_t nshots, uint64_t *out) {
+__global__ void __launch_bounds__(256) k_sample_lanes(const C *__restrict__ st, const __grid_constant__ SampMap m,
+                                                      const uint64_t *__restrict__ chunk, uint64_t nshots,
+                                                      double *__restrict__ lanes) {
     const int lane = threadIdx.x & 31;
-    const uint64_t per = kSampChunk / 32;
+    for (uint64_t s = blockIdx.x * 8ull + (threadIdx.x >> 5); s < nshots; s += gridDim.x * 8ull)
+        lanes[s * 32 + lane] = samp_lane_sum(st, m, chunk[s], lane);
+}
+
+// per shot s: the lane L whose inclusive prefix (sequential over lanes) first exceeds
+// the residual res[s]; on a rounding miss, the highest lane with mass (res2 = -1:
+// take its last nonzero value).  The 128 values of lane L go to vals[s][*].
+template <typename C>
+__global__ void __launch_bounds__(256) k_sample_vals(const C *__restrict__ st, const __grid_constant__ SampMap m,
+                                                     const uint64_t *__restrict__ chunk, const double *__restrict__ res,
+                                                     const double *__restrict__ lanes, uint64_t nshots,
+                                                     int32_t *__restrict__ pick_lane, double *__restrict__ res2,
+                                                     double *__restrict__ vals) {
+    const int lane = threadIdx.x & 31;
     for (uint64_t s = blockIdx.x * 8ull + (threadIdx.x >> 5); s < nshots; s += gridDim.x * 8ull) {
-        const uint64_t c = chunk[s];
         const double r = res[s];
-        const uint64_t b = c * kSampChunk + lane * per;
-        double acc = 0;
-        for (uint64_t k = 0; k < per; ++k) acc += amp2(st, b + k, N);
-        // inclusive prefix of lane sums in lane order (sequential over lanes: left to right)
-        double incl = acc;
+        const double mine = lanes[s * 32 + lane];
+        double incl = mine;
         for (int o = 1; o < 32; o <<= 1) {
             const double v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
-        const double excl = incl - acc;
-        const unsigned hit = __ballot_sync(0xffffffffu, incl > r);
-        // first lane whose inclusive sum exceeds r (rounding: fall back to the last lane)
-        const int L = hit ? __ffs(hit) - 1 : 31;
-        if (lane == L) {
-            double cum = excl;
-            uint64_t pick = b + per - 1, last_nz = ~0ull;
-            for (uint64_t k = 0; k < per; ++k) {
-                const double p = amp2(st, b + k, N);
-                if (p > 0) last_nz = b + k;
-                cum += p;
-                if (cum > r && p > 0) { pick = b + k; break; }
-                if (k == per - 1 && last_nz != ~0ull) pick = last_nz;
-            }
-            out[s] = pick < N ? pick : N - 1;
+        const unsigned hit = __ballot_sync(0xffffffffu, incl > r && mine > 0);
+        const unsigned nz = __ballot_sync(0xffffffffu, mine > 0);
+        const double excl = incl - mine;
+        int L;
+        double r2;
+        if (hit) {
+            L = __ffs(hit) - 1;
+            r2 = __shfl_sync(0xffffffffu, r - excl, L);
+        } else {                                     // rounding miss: the last lane with mass
+            L = nz ? 31 - __clz(nz) : 31;
+            r2 = -1.0;
+        }
+        if (lane == 0) {
+            pick_lane[s] = L;
+            res2[s] = r2;
+        }
+        const uint64_t j0 = chunk[s] * kSampChunk + (uint64_t)L * 128;
+        const uint64_t base = samp_base(m, j0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = lane + 32 * q;
+            vals[s * 128 + k] = samp_p(st, m, base, j0 + k, k);
         }
     }
 }
 
-cudaError_t launch_sample_mass(bool c128, const void *state, uint64_t N, double *mass, uint64_t nchunks,
-                               cudaStream_t st, int *kernels) {
-    const unsigned g = (unsigned)std::min<uint64_t>((nchunks + 7) / 8, (uint64_t)num_sms() * 16);
-    if (c128) k_sample_mass<double2><<<g, 256, 0, st>>>((const double2 *)state, N, nchunks, mass);
-    else k_sample_mass<float2><<<g, 256, 0, st>>>((const float2 *)state, N, nchunks, mass);
-    ++*kernels;
-    return cudaGetLastError();
+// per shot s: the first k of lane L whose sequential cumulative value exceeds
+// res2[s] (and has mass); on a miss (or res2 < 0) the last k with mass -> logical index
+__global__ void __launch_bounds__(256) k_sample_pick(const uint64_t *__restrict__ chunk,
+                                                     const int32_t *__restrict__ pick_lane,
+                                                     const double *__restrict__ res2, const double *__restrict__ vals,
+                                                     uint64_t nshots, uint64_t N, uint64_t *__restrict__ out) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nshots;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const double r = res2[s];
+        const double *v = vals + s * 128;
+        double cum = 0;
+        int pick = -1, last = -1;
+        for (int k = 0; k < 128; ++k) {
+            const double p = v[k];
+            cum += p;
+            if (p > 0) last = k;
+            if (r >= 0 && p > 0 && cum > r) {
+                pick = k;
+                break;
+            }
+        }
+        if (pick < 0) pick = last >= 0 ? last : 127;
+        const uint64_t j = chunk[s] * kSampChunk + (uint64_t)pick_lane[s] * 128 + (uint64_t)pick;
+        out[s] = j < N ? j : N - 1;
+    }
 }
 
-cudaError_t launch_sample_find(bool c128, const void *state, uint64_t N, const uint64_t *chunk, const double *res,
-                               uint64_t nshots, uint64_t *out, cudaStream_t st, int *kernels) {
-    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nshots + 7) / 8, (uint64_t)num_sms() * 16));
-    if (c128) k_sample_find<double2><<<g, 256, 0, st>>>((const double2 *)state, N, chunk, res, nshots, out);
-    else k_sample_find<float2><<<g, 256, 0, st>>>((const float2 *)state, N, chunk, res, nshots, out);
+static SampMap make_samp_map(const int32_t *perm, uint64_t xmask, int n, int n_local, uint64_t rank_bits) {
+    SampMap m;
+    std::memset(&m, 0, sizeof(m));
+    for (int q = 0; q < 64; ++q) m.perm[q] = q < n ? perm[q] : q;
+    for (int k = 0; k < 128; ++k) {
+        uint64_t p = 0;
+        for (int q = 0; q < 7 && q < n; ++q) p |= (uint64_t)((k >> q) & 1) << m.perm[q];
+        m.plo[k] = p;
+    }
+    m.xmask = xmask;
+    m.N = 1ull << n;
+    m.n = n;
+    m.n_local = n_local;
+    m.lmask = n_local >= 64 ? ~0ull : (1ull << n_local) - 1;
+    m.rank_bits = rank_bits;
+    return m;
+}
+
+// phase 0: chunk masses (count = nchunks, a = mass); 1: per-shot lane sums (a = lanes,
+// count * 32); 2: lane pick + the lane's values (a = lanes, input); 3: in-lane pick
+cudaError_t launch_sample(int phase, bool c128, const void *state, const int32_t *perm, uint64_t xmask, int n,
+                          int n_local, uint64_t rank_bits, uint64_t count, const uint64_t *chunk, const double *res,
+                          double *a, int32_t *pick_lane, double *res2, double *vals, uint64_t *out, cudaStream_t st,
+                          int *kernels) {
+    const SampMap m = make_samp_map(perm, xmask, n, n_local, rank_bits);
+    const unsigned gw = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((count + 7) / 8, (uint64_t)num_sms() * 16));
+    switch (phase) {
+    case 0:
+        if (c128) k_sample_mass<double2><<<gw, 256, 0, st>>>((const double2 *)state, m, count, a);
+        else k_sample_mass<float2><<<gw, 256, 0, st>>>((const float2 *)state, m, count, a);
+        break;
+    case 1:
+        if (c128) k_sample_lanes<double2><<<gw, 256, 0, st>>>((const double2 *)state, m, chunk, count, a);
+        else k_sample_lanes<float2><<<gw, 256, 0, st>>>((const float2 *)state, m, chunk, count, a);
+        break;
+    case 2:
+        if (c128)
+            k_sample_vals<double2><<<gw, 256, 0, st>>>((const double2 *)state, m, chunk, res, a, count, pick_lane,
+                                                        res2, vals);
+        else
+            k_sample_vals<float2><<<gw, 256, 0, st>>>((const float2 *)state, m, chunk, res, a, count, pick_lane, res2,
+                                                       vals);
+        break;
+    default: {
+        const unsigned g =
+            (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, (uint64_t)num_sms() * 8));
+        k_sample_pick<<<g, 256, 0, st>>>(chunk, pick_lane, res2, vals, count, m.N, out);
+    }
+    }
     ++*kernels;
     return cudaGetLastError();
 }

@@ -1,10 +1,13 @@
 """Measurement sampling.
 
 CPU (-m "not gpu"): the oracle sampler pinned to the published splitmix64 outputs,
-to basis states, to the Born rule (chi-square) and to the storage-order mapping.
-GPU (-m gpu): sv_sample through the C ABI against the oracle sampler run on the
-same amplitudes in the same storage order (exact index agreement), plus basis
-states, virtual shards and a Born-rule check against the oracle's own state.
+to basis states and to the Born rule (chi-square).
+GPU (-m gpu): sv_sample through the C ABI against the ORACLE's own state
+(oracle.run): every sample must bracket the oracle's logical-order CDF within the
+bound implied by the per-amplitude bar, and agree index for index with the oracle
+sampler except within rounding of a CDF boundary; plus basis states, virtual
+shards and a Born-rule chi-square.  No GPU-produced value (amplitudes, frame) is
+passed to any oracle call.
 """
 import numpy as np
 import pytest
@@ -57,22 +60,6 @@ def test_sample_two_outcomes_half_half():
     assert abs(np.mean(s == 0) - 0.5) < 0.01
 
 
-def test_storage_order_maps_back_to_logical():
-    n = 5
-    perm = [3, 0, 4, 1, 2]
-    xm = 0b10110
-    order = oracle.storage_order(n, perm, xm)
-    assert sorted(order.tolist()) == list(range(1 << n))
-    for j in range(1 << n):            # stored index of logical j: P(j) xor xmask
-        p = 0
-        for q in range(n):
-            p |= ((j >> q) & 1) << perm[q]
-        assert order[p ^ xm] == j
-    psi = np.zeros(1 << n, dtype=np.complex128)
-    psi[19] = 1
-    assert np.all(oracle.sample(psi, 2, 50, order=order) == 19)
-
-
 # --------------------------- GPU: sv_sample ---------------------------
 @pytest.fixture(scope="module")
 def stv():
@@ -84,28 +71,45 @@ def stv():
     return m
 
 
-def _storage_order(stv, st, n):
-    perm, xm = st.frame()
-    return oracle.storage_order(n, perm, xm)
+def _bracket_check(got, ref, seed, eps):
+    """Every GPU sample j must satisfy cdf(j-1) - eps <= u * total <= cdf(j) + eps for the
+    ORACLE's state (oracle.run), with u the oracle's own counter-based uniforms: the
+    definition in include/sv.h, evaluated on independent amplitudes."""
+    p = np.abs(ref) ** 2
+    cdf = np.cumsum(p)
+    total = cdf[-1]
+    t = oracle.uniforms(seed, got.size) * total
+    j = got.astype(np.int64)
+    assert np.all((j >= 0) & (j < ref.size))
+    lo = np.where(j > 0, cdf[np.maximum(j - 1, 0)], 0.0)
+    hi = cdf[j]
+    bad = np.nonzero((t < lo - eps) | (t > hi + eps) | (p[j] == 0))[0]
+    assert bad.size == 0, (bad[:5], t[bad[:5]], lo[bad[:5]], hi[bad[:5]])
+
+
+def _eps(ref, bar):
+    # per-amplitude bar |d| <= bar  =>  | |a+d|^2 - |a|^2 | <= 2 |a| bar + bar^2: summed over
+    # all indices it bounds the CDF shift; doubled for the u * total term
+    return 2.0 * (2.0 * bar * float(np.sum(np.abs(ref))) + ref.size * bar * bar) + 1e-15
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("n,seed", [(5, 1), (12, 2), (16, 3)])
-def test_gpu_sample_matches_oracle_sampler(stv, n, seed, dtype):
+def test_gpu_sample_matches_oracle_cdf(stv, n, seed, dtype):
     circ = C.random_circuit(n, 12 * n, seed)
+    ref = oracle.run(circ)
     st = stv.State(n, dtype)
     st.set_basis(circ.x0)
     st.apply(circ.gates)
-    psi = st.amplitudes()                      # the GPU's own amplitudes (exact widening)
-    order = _storage_order(stv, st, n)
     shots = 20000
     got = st.sample(shots, seed=seed + 100)
     st.close()
-    want = oracle.sample(psi, seed + 100, shots, order=order)
-    # same probabilities, same order, same draws: only the summation association
-    # differs (chunk trees vs a sequential cumsum) -> identical indices
-    assert np.count_nonzero(got != want) == 0
+    _bracket_check(got, ref, seed + 100, _eps(ref, 2e-6 if dtype == "c64" else 1e-12))
+    want = oracle.sample(ref, seed + 100, shots)
+    same = int(np.count_nonzero(got == want))
+    # only draws within rounding of a CDF boundary may differ
+    assert same >= shots - (1 if dtype == "c128" else shots // 100), same
 
 
 @pytest.mark.gpu
@@ -139,17 +143,16 @@ def test_gpu_sample_basis(stv, x):
 
 
 @pytest.mark.gpu
-def test_gpu_sample_virtual_shards(stv):
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_gpu_sample_virtual_shards(stv, g):
     circ = C.random_circuit(14, 150, 5)
-    st = stv.State(14, "c64", virtual_g=2)
+    ref = oracle.run(circ)
+    st = stv.State(14, "c64", virtual_g=g)
     st.set_basis(circ.x0)
     st.apply(circ.gates)
-    psi = st.amplitudes()
-    order = _storage_order(stv, st, 14)
     got = st.sample(5000, seed=8)
     st.close()
-    want = oracle.sample(psi, 8, 5000, order=order)
-    assert np.count_nonzero(got != want) == 0
+    _bracket_check(got, ref, 8, _eps(ref, 2e-6))
 
 
 @pytest.mark.gpu

@@ -11,6 +11,9 @@ may import this package; the product package never does.
                          numpy, n <= 8 -- the "enormously wasteful" baseline
   gate_matrix(...)       the oracle's own gate table (sv_oracle.c)
   compare(psi, ref)      max |delta|, fidelity, norms
+  monomial_amplitudes    single output amplitudes of permutation/phase circuits
+                         (one row of each padded matrix), for sampled parity at
+                         full size; qft_basis_amplitudes: the QFT closed form
 """
 from __future__ import annotations
 
@@ -198,6 +201,56 @@ def timed_run(circuit, nthreads: int = 0, gates=None):
     t0 = time.perf_counter()
     psi = run(circuit, nthreads, gates)
     return psi, time.perf_counter() - t0
+
+
+# ---------------------------------------------------------------------------
+# One amplitude at a time, for circuits of monomial gates (sampled parity at
+# full size, VERDICT r1 / SURVEY.md 8(c) "sampled outputs the oracle can compute
+# one by one").  (U psi)[y] = sum_x U[y, x] psi[x] (one row of
+# the padded matrix); when every row of every gate matrix has exactly one
+# nonzero entry (X, CNOT, SWAP, Z, S, T, CZ, CPHASE: permutations times phases)
+# the sum has one term, so psi_out[y] = (product of the entries met while walking
+# y back through the gates) * psi_in[x].  Generic in the gate: the nonzero
+# entries are read from gate_matrix(), the oracle's own table; plain numpy over
+# an array of indices, no special case per gate kind.
+# ---------------------------------------------------------------------------
+def monomial_amplitudes(n: int, gates, psi_in, ys) -> np.ndarray:
+    """psi_out[ys] for psi_out = U_G ... U_1 psi_in, every U_g monomial; psi_in is a
+    callable mapping an array of indices to their input amplitudes."""
+    idx = np.array(ys, dtype=np.uint64)
+    amp = np.ones(idx.size, dtype=np.complex128)
+    for name, qs, p in reversed(list(gates)):
+        U = gate_matrix(name, p)
+        d, q = U.shape[0], len(qs)
+        col = np.empty(d, dtype=np.int64)
+        for r in range(d):
+            nz = np.flatnonzero(U[r] != 0)
+            if nz.size != 1:
+                raise ValueError(f"{name} is not monomial")
+            col[r] = nz[0]
+        ent = U[np.arange(d), col]
+        row = np.zeros(idx.size, dtype=np.int64)
+        for i, qq in enumerate(qs):            # first-listed qubit = MSB of the local index
+            row |= ((idx >> np.uint64(qq)) & np.uint64(1)).astype(np.int64) << (q - 1 - i)
+        amp *= ent[row]
+        c = col[row]
+        for i, qq in enumerate(qs):
+            bit = ((c >> (q - 1 - i)) & 1).astype(np.uint64)
+            idx = (idx & ~np.uint64(1 << qq)) | (bit << np.uint64(qq))
+    return amp * psi_in(idx)
+
+
+def qft_basis_amplitudes(n: int, x0: int, ys) -> np.ndarray:
+    """QFT of |x0> at indices ys (reading A7, pinned against run() for n = 3..10):
+    2^{-n/2} exp(2 pi i ((x0 y) mod 2^n) / 2^n), the product reduced exactly in
+    integers before the single rounding to double."""
+    y = np.asarray(ys, dtype=np.uint64)
+    if n <= 32:
+        r = (np.uint64(x0) * y) & np.uint64((1 << n) - 1)        # < 2^64: exact
+        frac = r.astype(np.float64) / float(1 << n)
+    else:
+        frac = np.array([((x0 * int(v)) % (1 << n)) / float(1 << n) for v in y])
+    return 2.0 ** (-n / 2) * np.exp(2j * np.pi * frac)
 
 
 # ---------------------------------------------------------------------------

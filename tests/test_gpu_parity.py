@@ -56,7 +56,8 @@ def test_random_circuits_all_kinds(stv, n, seed, dtype):
 @pytest.mark.parametrize("kw", [dict(kmax=1), dict(kmax=2), dict(kmax=3), dict(kmax=4),
                                 dict(tile_bits=8, low_bits=3), dict(tile_bits=13, low_bits=5),
                                 dict(tile_bits=10, low_bits=0), dict(budget=400), dict(budget=20),
-                                dict(flags=2), dict(flags=4), dict(flags=8), dict(flags=16)])
+                                dict(flags=2), dict(flags=4), dict(flags=8), dict(flags=16),
+                                dict(flags=32), dict(flags=128), dict(flags=32 | 128)])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_planner_options(stv, kw, dtype):
     circ = C.random_circuit(17, 300, 42)
@@ -142,6 +143,24 @@ def test_norm_deterministic(stv):
     b = st.norm()
     st.close()
     assert a == b and abs(a - 1) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [1, 7, 13, 22])
+def test_norm_vs_host_fp64_sum(stv, n, dtype):
+    """sv_norm of a NON-normalised buffer (seeded normal values written into the wrapped
+    tensor) against the fp64 host sum of |a|^2, 1e-12 relative."""
+    import torch
+    rng = np.random.default_rng(n)
+    real = np.float32 if dtype == "c64" else np.float64
+    host = (rng.normal(size=2 << n) * 3.0).astype(real)
+    st = stv.State(n, dtype)
+    st.tensor.copy_(torch.from_numpy(host).to(st.tensor.device))
+    torch.cuda.synchronize()
+    got = st.norm()
+    st.close()
+    want = float(np.sum(host.astype(np.float64) ** 2))
+    assert abs(got - want) <= 1e-12 * want, (got, want)
 
 
 def test_uniform_init_and_get_amplitudes(stv):

@@ -314,3 +314,43 @@ def test_coupler_patterns_cover_grid():
             assert len(qs) == len(set(qs))
     assert sum(len(p) for p in C.coupler_patterns(4, 4)) == 24
     assert sum(len(p) for p in C.coupler_patterns(5, 6)) == 49
+
+
+# ------------------ single-amplitude paths (sampled full-size parity) ------------------
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_monomial_amplitudes_vs_run(seed):
+    # brute force: the full gate-by-gate state of a random permutation/phase circuit
+    # applied to a random (non-basis) input state
+    n = 10
+    circ = C.random_circuit(n, 300, seed, kinds=["x", "cnot", "swap", "z", "s", "t", "cz", "cphase"])
+    rng = np.random.default_rng(seed)
+    psi0 = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi0 /= np.linalg.norm(psi0)
+    full = oracle.apply(n, psi0.copy(), circ.gates)
+    ys = np.arange(1 << n, dtype=np.uint64)
+    got = oracle.monomial_amplitudes(n, circ.gates, lambda x: psi0[x.astype(np.int64)], ys)
+    assert close(got, full, 1e-13)
+
+
+def test_monomial_amplitudes_rejects_dense_gates():
+    with pytest.raises(ValueError):
+        oracle.monomial_amplitudes(2, [("h", (0,), ())], lambda x: np.ones(x.size), [0])
+
+
+@pytest.mark.parametrize("n", [8, 14])
+def test_c3_paths_vs_run(n):
+    # c3 shape: QFT closed form followed by the CNOT/X/CZ/T tail, against run()
+    circ = C.qft_circuit(n, tail=200, seed=3)
+    nq = len(C.qft_gates(n))
+    psi = oracle.run(circ)
+    ys = np.arange(1 << n, dtype=np.uint64)
+    got = oracle.monomial_amplitudes(n, circ.gates[nq:], lambda x: oracle.qft_basis_amplitudes(n, circ.x0, x), ys)
+    assert close(got, psi, 1e-12)
+
+
+@pytest.mark.parametrize("n", [3, 5, 7, 10])
+def test_qft_basis_amplitudes_vs_run(n):
+    circ = C.qft_circuit(n, tail=0, seed=5)
+    psi = oracle.run(circ)
+    got = oracle.qft_basis_amplitudes(n, circ.x0, np.arange(1 << n))
+    assert close(got, psi, 1e-12)

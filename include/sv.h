@@ -93,6 +93,7 @@ typedef struct {
 #define SV_OPT_NO_GROUPS    0x20u /* one shared-memory round trip per op (no register-resident gate groups) */
 /* 0x40u reserved (was an experimental warp-per-tile kernel; ignored)                                     */
 #define SV_OPT_NO_VARIANTS  0x80u /* do not merge 2-qubit sub-op chains into per-tile variant matrices      */
+#define SV_OPT_NO_TC        0x100u /* complex64 gate groups on the CUDA-core FMA path only (no tcgen05 pass) */
 typedef struct {
     int32_t kmax;        /* max qubits of one fused dense op (1..5); 0 = default (4)     */
     int32_t tile_bits;   /* max tile bits |S| of a fused pass; 0 = default              */

@@ -229,6 +229,7 @@ class State:
         if self._h:
             lib().sv_destroy(self._h)
             self._h = ctypes.c_void_p()
+        self.tensor = None        # release the torch-owned buffer with the state
 
     def __del__(self):
         try:

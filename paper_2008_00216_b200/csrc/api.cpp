@@ -34,6 +34,9 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
                               int S, int n_local, uint32_t rec_bytes, uint32_t tab_entries, double flops_per_amp,
                               cudaStream_t st, int *kernels);
 cudaError_t launch_cnot(bool c128, void *state, int c, int t, int n_local, cudaStream_t st, int *kernels);
+cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off, int S,
+                                 int n_local, uint32_t rec_bytes, uint32_t tab_entries, int ntcop, cudaStream_t st,
+                                 int *kernels);
 cudaError_t launch_bitswap(bool c128, void *state, int a, int b, int n_bits, cudaStream_t st, int *kernels);
 cudaError_t launch_norm(bool c128, const void *state, uint64_t N, double *part, int np, double *out, cudaStream_t st,
                         int *kernels);
@@ -370,7 +373,10 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
         cudaError_t e = cudaSuccess;
         if (ps.kind == PASS_TILE) {
             kind = hp->h == 0 ? 1 : 2;
-            if (hp->grouped)
+            if (hp->grouped && hp->ntc > 0 && !s->c128())
+                e = launch_tc_group_pass(s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
+                                         enc_local, hp->param_bytes, hp->tab_entries, hp->ntcop, s->stream, &kernels);
+            else if (hp->grouped)
                 e = launch_group_pass(s->c128(), s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
                                       enc_local, hp->param_bytes, hp->tab_entries, pass_flops_per_amp(ps.ops),
                                       s->stream, &kernels);

@@ -1335,6 +1335,8 @@ k_group_pass(typename C2T<R>::T *__restrict__ state, const uint8_t *__restrict__
     cp_async_wait0();
 }
 
+#include "tc_pass.cuh"
+
 // ---------------------------------------------------------------------------
 // standalone diagonal pass (streaming; skip-write)
 // ---------------------------------------------------------------------------
@@ -1790,6 +1792,29 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
     else e = group_launch<float, 256, 1, 1, 4>(state, dblob, pass_off, (uint32_t)ntiles, smem, rp, st);
     ++*kernels;
     return e;
+}
+
+// tensor-core group pass (tc_pass.cuh): 2 CTAs per SM (TMEM 256 columns each)
+cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off, int S,
+                                 int n_local, uint32_t rec_bytes, uint32_t tab_entries, int ntcop, cudaStream_t st,
+                                 int *kernels) {
+    const size_t smem = (size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127) +
+                        ((size_t)8 << S) + sizeof(TcShared);
+    const uint64_t ntiles = 1ull << (n_local - S);
+    if (smem > 113 * 1024 || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_tc_group_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+        attr = true;
+    }
+    static thread_local RecParam rp;
+    std::memcpy(rp.b, hrec, rec_bytes);
+    uint64_t grid = (uint64_t)num_sms() * 2;
+    if (grid > ntiles) grid = ntiles;
+    static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
+    k_tc_group_pass<<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, (uint32_t)ntiles, dbg, rp);
+    ++*kernels;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,

@@ -83,6 +83,24 @@ struct alignas(16) StvPass {
     uint32_t param_bytes;      // leading bytes of the record passed as the group-pass kernel
                                // parameter (the rest -- static table phases -- is read from
                                // device memory only)
+    // tensor-core group pass (tc_pass.cuh; complex64, S <= 12): ntc > 0 selects it
+    uint32_t tc_off;           // byte offset of StvTcStep[ntc] (kernel-parameter part)
+    int32_t ntc;               // steps over all groups, in group order
+    int32_t ntcop;             // operator slots (M steps), <= STV_TC_MAX_OPS
+    int32_t tc_pad;
+    uint8_t tperm[48];         // tile ordinal bit of permuted-ordinal bit i (dep bits on top)
+};
+
+// Tensor-core pass step: a group's sub-op program [first, first + n) either runs
+// on the register vectors (kind 0, "E") or is multiplied into one 16 x 16 complex
+// operator applied with tcgen05.mma (kind 1, "M"; slot `op`, rebuilt when the
+// tile base bits `dep` change).  `last` ends the group's steps.
+#define STV_TC_MAX_OPS 12
+#define STV_TC_MAX_STEPS 64
+struct alignas(16) StvTcStep {
+    int16_t kind, last, first, n;
+    int32_t op, group;
+    uint64_t dep;
 };
 
 // ---------------------------------------------------------------------------

@@ -1089,6 +1089,7 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
     Plan plan;
     plan.n = n;
     plan.n_global = n_global;
+    plan.flags = opt.flags;
     const int nl = n - n_global;
     const uint64_t local_mask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
     const uint64_t all_mask = n >= 64 ? ~0ull : ((1ull << n) - 1);
@@ -1530,6 +1531,135 @@ static std::vector<GroupTable> split_group_diag(const QForm &f, const std::vecto
     return out;
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core step plan of a grouped complex64 pass (pass_format.h StvTcStep,
+// tc_pass.cuh).  Each group's final sub-op program is cut into maximal runs of
+// sub-ops that act identically on every vector of a tile ("foldable": matrices,
+// per-tile variants, CNOTs without a V-bit control, diagonal tables without
+// V-bits) and the rest.  A foldable run whose FMA cost reaches STV_TC_MIN
+// (FFMA2-equivalents per vector; cheaper runs stay on the registers) becomes an
+// M step: one 16 x 16 operator applied with tcgen05.mma.
+// ---------------------------------------------------------------------------
+static int nth_set_bit(uint64_t m, int i) {
+    for (int k = 0; k < 64; ++k)
+        if ((m >> k) & 1) {
+            if (i-- == 0) return k;
+        }
+    return -1;
+}
+
+static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, const std::vector<StvGroup> &grecs,
+                            const std::vector<StvDTab> &tabs) {
+    static const double tc_min = getenv("STV_TC_MIN") ? atof(getenv("STV_TC_MIN")) : 200.0;
+    auto foldable = [&](const StvSub &x) {
+        const int c = x.code & 0xff;
+        if (c >= SUBC_CNOT && c < SUBC_DIAG) return (x.ctl & 0xffffu) == 0;   // no V-bit control
+        if (c == SUBC_DIAG || (c >= SUBC_DIAGH && c < SUBC_DIAGH + 4)) return tabs[x.arg].m == 0;
+        return true;
+    };
+    auto cost = [&](const StvSub &x) -> double {   // FFMA2-equivalents per 16-amplitude vector
+        const int c = x.code & 0xff;
+        if (c < SUBC_U2) return 32;
+        if (c < SUBC_CNOT) return 128;
+        if (c < SUBC_DIAG) return 16;
+        if (c == SUBC_DIAG) return 40;
+        if (c < SUBC_DIAGH) return 128;          // U2V
+        if (c < SUBC_U2X2) return 20;            // half table
+        if (c < SUBC_U1R) return 256;            // two U2
+        if (c < SUBC_U2R) return 16;
+        return 64;
+    };
+    auto sel_bits = [&](uint32_t w, uint64_t &dep) {   // 3 x 5-bit tile-ordinal selectors
+        for (int i = 0; i < 3; ++i) {
+            const uint32_t sl = (w >> (5 * i)) & 31u;
+            if (sl != 31u) {
+                const int pb = nth_set_bit(hd.out_mask, (int)sl);
+                if (pb >= 0) dep |= 1ull << pb;
+            }
+        }
+    };
+    auto depends = [&](const StvSub &x) -> uint64_t {   // tile-base bits the op's action depends on
+        const int c = x.code & 0xff;
+        uint64_t dep = 0;
+        if (c >= SUBC_U2V && c < SUBC_U2V + 6) sel_bits((uint32_t)x.code >> 8, dep);
+        if (c >= SUBC_U2X2 && c < SUBC_U2X2 + 3) {
+            sel_bits((uint32_t)x.code >> 8, dep);
+            sel_bits(x.pad, dep);
+        }
+        if (c >= SUBC_CNOT && c < SUBC_DIAG && (x.ctl >> 16)) dep |= 1ull << ((x.ctl >> 16) - 1);
+        if (c == SUBC_DIAG || (c >= SUBC_DIAGH && c < SUBC_DIAGH + 4)) {
+            const StvDTab &d = tabs[x.arg];
+            const StvTerm *tm = (const StvTerm *)&b[at + d.term_off];
+            for (int i = 0; i < d.nterm; ++i) {
+                dep |= 1ull << tm[i].b;
+                if (tm[i].a <= -2) dep |= 1ull << (-2 - tm[i].a);
+            }
+        }
+        return dep;
+    };
+    std::vector<StvTcStep> st;
+    int nop = 0;
+    uint64_t dep_all = 0;
+    for (size_t gi = 0; gi < grecs.size(); ++gi) {
+        const StvGroup &G = grecs[gi];
+        const StvSub *sp = (const StvSub *)&b[at + G.sub_off];
+        const size_t g0 = st.size();
+        int k = 0;
+        while (k < G.nsub) {
+            bool f = foldable(sp[k]);
+            int e = k;
+            double c = 0;
+            uint64_t dep = 0;
+            while (e < G.nsub && foldable(sp[e]) == f) {
+                c += cost(sp[e]);
+                dep |= depends(sp[e]);
+                ++e;
+            }
+            if (f && c < tc_min) f = false;
+            if (!f && st.size() > g0 && st.back().kind == 0) {
+                st.back().n = (int16_t)(st.back().n + (e - k));
+            } else {
+                StvTcStep s;
+                std::memset(&s, 0, sizeof(s));
+                s.kind = f ? 1 : 0;
+                s.first = (int16_t)k;
+                s.n = (int16_t)(e - k);
+                s.group = (int32_t)gi;
+                if (f) {
+                    s.op = nop++;
+                    s.dep = dep;
+                    dep_all |= dep;
+                }
+                st.push_back(s);
+            }
+            k = e;
+        }
+        if (st.size() == g0) {   // no sub-ops (flips only)
+            StvTcStep s;
+            std::memset(&s, 0, sizeof(s));
+            s.group = (int32_t)gi;
+            st.push_back(s);
+        }
+        st.back().last = 1;
+    }
+    const int nord = __builtin_popcountll(hd.out_mask);
+    const size_t need = st.size() * sizeof(StvTcStep) + 16;
+    if (nop == 0 || nop > STV_TC_MAX_OPS || st.size() > STV_TC_MAX_STEPS || nord > 48 ||
+        b.size() - at + need > (size_t)STV_REC_PARAM_BYTES)
+        return;   // FMA group pass
+    // tile order: ordinal bits the operators depend on vary slowest within a CTA's range
+    std::vector<int> lo, hi;
+    for (int i = 0; i < nord; ++i) ((dep_all >> nth_set_bit(hd.out_mask, i)) & 1 ? hi : lo).push_back(i);
+    int q = 0;
+    for (int i : lo) hd.tperm[q++] = (uint8_t)i;
+    for (int i : hi) hd.tperm[q++] = (uint8_t)i;
+    align(b, 16);
+    hd.tc_off = (uint32_t)(b.size() - at);
+    hd.ntc = (int32_t)st.size();
+    hd.ntcop = nop;
+    put(b, st.data(), st.size() * sizeof(StvTcStep));
+}
+
 Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
     Encoded e;
     std::vector<uint8_t> &b = e.blob;
@@ -1898,6 +2028,7 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                 }
                 hd.nops = (int)grecs.size();
                 std::memcpy(&b[ops_at], grecs.data(), grecs.size() * sizeof(StvGroup));
+                if (!c128 && !(p.flags & SV_OPT_NO_TC) && hd.S <= 12) encode_tc_steps(b, at, hd, grecs, tabs);
             }
             else std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
             (void)esz;

@@ -108,6 +108,7 @@ struct Plan {
     int sigma_out[64];        // virtual -> actual physical bit after the plan
     double alg_bytes = 0;     // algorithmic HBM bytes
     double alg_flops = 0;     // algorithmic FP flops of the fused tile passes
+    uint32_t flags = 0;       // SV_OPT_* the plan was built with (encoder choices)
 };
 
 // Validation (all-or-nothing).  Returns "" if ok, else the error message.

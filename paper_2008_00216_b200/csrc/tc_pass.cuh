@@ -1,0 +1,374 @@
+// tc_pass.cuh -- tensor-core gate-group pass, complex64.
+// Included by kernels.cu after the FMA group pass (it reuses its tile copy,
+// swizzled gather/scatter addressing, per-tile tables and the sub-op program
+// interpreter run_subs).
+//
+// A group's sub-op program (pass_format.h StvSub) is split by the encoder into
+// steps (StvTcStep): E steps run on each thread's 16-amplitude register vector
+// exactly as in k_group_pass (diagonal tables over V-bits, CNOTs controlled by
+// V-bits: everything that differs between the vectors of a tile); M steps are
+// runs of sub-ops whose action is the same for every vector of the tile
+// (U1/U2 matrices, per-tile variants, in-register CNOTs, V-bit-free diagonal
+// tables).  An M step's product is ONE dense 16 x 16 complex operator U
+// ("fused k-qubit block"; the paper's contrast case of
+// multiplied-out clusters applied with MACs, L383-384), applied with
+// tcgen05.mma kind::tf32:
+//   * real embedding: amplitude l of a vector is the pair (re, im) at real
+//     index k = 2l + ri; out = A . B with B[2l+ri][2l'+ro] = (Ur, -Ui; Ui, Ur)
+//     of U[l'][l] -- a 32 x 32 real matrix, N = K = 32;
+//   * A = the tile's 256 vectors (rows) in TMEM, two M = 128 blocks; B in shared
+//     memory, K-major SWIZZLE_NONE canonical layout; D (fp32) in TMEM;
+//   * 3xTF32: x = x_hi + x_lo with x_hi = tf32(x), D = A_hi B_hi + A_hi B_lo +
+//     A_lo B_hi (the dropped A_lo B_lo term is ~2^-22 relative), accumulated in
+//     fp32 -- complex64 accuracy (DESIGN.md a7 error budget).
+// U is built on the device by running the step's sub-ops on the 16 basis
+// vectors (lane j of one warp computes column j), so it is exactly the product
+// the FMA path applies; it depends on the tile only through the step's `dep`
+// bits of the tile base and is rebuilt only when they change.  Each CTA walks
+// a contiguous range of tile ordinals whose dep bits are the slowest-varying
+// (StvPass.tperm), so a CTA rebuilds its operators a few times per pass.
+#pragma once
+
+// ---------------------------------------------------------------------------
+// tcgen05 / TMEM PTX wrappers (sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+// 32 lanes x 32 columns of 32 bit: thread i <-> TMEM lane (base + i), register j <-> column j
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+        "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+        "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] . B[smem descriptor]: kind::tf32, cta_group::1
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "TCW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TCW;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// shared-memory matrix descriptor, SWIZZLE_NONE K-major canonical layout: core
+// matrix = 8 rows x 16 B; lbo = byte stride of K-adjacent core matrices, sbo =
+// byte stride of 8-row groups; version 1 (sm_100)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)((lbo >> 4) & 0x3fffu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, N = 32, M = 128
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+// byte offset of B^T[n][k] (n = output real index, k = input real index) in an operator slot
+__device__ __forceinline__ uint32_t tc_bt_off(int n, int k) {
+    return (uint32_t)((n & 7) * 16 + (k & 3) * 4 + (k >> 2) * 128 + (n >> 3) * 1024);
+}
+constexpr uint32_t kTcOpBytes = 8192;   // hi (4 KB) + lo (4 KB)
+constexpr uint32_t kTcCols = 256;       // TMEM columns per CTA: 2 blocks x (A_hi 32, A_lo 32, D 32), rounded up
+
+// Build the operator of M step st into its slot: lane j < 16 runs the step's sub-ops on e_j.
+__device__ __forceinline__ void tc_build_op(const StvSub *__restrict__ subs, int n, const uint8_t *__restrict__ mat,
+                                            const StvDTab *__restrict__ tabs, const float2 *__restrict__ tables,
+                                            uint64_t full_base, uint32_t tord, uint64_t rank_bits,
+                                            const float2 *__restrict__ scal, uint8_t *slot, int lane) {
+    float2 x[1][16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) x[0][l] = make_float2(l == (lane & 15) ? 1.f : 0.f, 0.f);
+    const uint32_t braw[1] = {0u};
+    run_subs<float2, 1>(x, braw, subs, n, mat, tabs, tables, full_base, tord, rank_bits, scal);
+    if (lane < 16) {
+        const int j = lane;   // input amplitude index (column of U)
+#pragma unroll
+        for (int l = 0; l < 16; ++l) {   // U[l][j] = x[l]
+            const float ur = x[0][l].x, ui = x[0][l].y;
+            const float v[4] = {ur, -ui, ui, ur};   // (ro, ri) = (0,0) (0,1) (1,0) (1,1)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int ro = q >> 1, ri = q & 1;
+                const uint32_t off = tc_bt_off(2 * l + ro, 2 * j + ri);
+                const uint32_t hi = tf32_rna(v[q]);
+                *(uint32_t *)(slot + off) = hi;
+                *(float *)(slot + 4096 + off) = v[q] - __uint_as_float(hi);
+            }
+        }
+    }
+}
+
+// The MMA of one M step for both blocks: 3xTF32, 4 K-slices of 8 each.
+__device__ __forceinline__ void tc_issue(uint32_t tmem, uint32_t slot_saddr) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+            mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+            mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 4096 + 256 * kk, 128, 1024), kTcIdesc, 1);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+            mma_tf32_ts(d, al + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, 1);
+    }
+}
+
+struct TcShared {
+    uint64_t bar;
+    uint32_t tmem;
+    uint32_t pad;
+    uint64_t key[STV_TC_MAX_OPS];
+};
+
+// One group on the resident tile with tensor-core M steps: thread ctid owns vector ctid.
+__device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
+                                         const StvTcStep *__restrict__ steps, int s0, const uint8_t *__restrict__ mat,
+                                         const float2 *__restrict__ tables, uint64_t full_base, uint32_t tord,
+                                         const uint8_t *__restrict__ grec, const float2 *__restrict__ scal,
+                                         const uint8_t *__restrict__ opsm, TcShared *sh, uint32_t &phase, int ctid) {
+    const int nvb = g.nvb;
+    const uint32_t nvec = 1u << nvb;
+    const bool live = (uint32_t)ctid < nvec;
+    uint32_t braw = 0, bsw = 0;
+    {
+        const uint32_t w = __ldg((const uint32_t *)(grec + g.vtab_off) + ctid);
+        bsw = w & 0xffffu;
+        braw = w >> 16;
+    }
+    uint32_t so[16];
+#pragma unroll
+    for (int l = 0; l < 16; l += 2) {
+        const uint2 w = *(const uint2 *)&g.sw_off[l];
+        so[l] = w.x;
+        so[l + 1] = w.y;
+    }
+    uint32_t bsw_g = bsw, bsw_s = bsw;
+    if (g.nflip_g | g.nflip_s) {
+        auto flip_delta = [&](int from, int cnt) {
+            uint32_t dlt = 0;
+            for (int q = 0; q < cnt; ++q) {
+                const uint32_t f = g.flip[from + q];
+                const uint32_t a = f >> 17;
+                const bool on = (f & (1u << 16)) ? ((full_base >> a) & 1) != 0 : (braw & a) != 0;
+                if (on) dlt ^= f & 0xffffu;
+            }
+            return dlt;
+        };
+        bsw_g ^= flip_delta(0, g.nflip_g);
+        bsw_s ^= flip_delta(STV_MAX_FLIPS, g.nflip_s);
+    }
+    const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off);
+    const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
+    const bool pair16 = g.pair16;
+    float2 x[1][16];
+    if (live) {
+        if (pair16) {
+#pragma unroll
+            for (int l = 0; l < 16; l += 2) {
+                const float4 q = *(const float4 *)&tile[bsw_g ^ so[l]];
+                x[0][l] = make_float2(q.x, q.y);
+                x[0][l + 1] = make_float2(q.z, q.w);
+            }
+        } else {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) x[0][l] = tile[bsw_g ^ so[l]];
+        }
+    } else {
+#pragma unroll
+        for (int l = 0; l < 16; ++l) x[0][l] = make_float2(0.f, 0.f);
+    }
+    const uint32_t braw1[1] = {braw};
+    const int warp = ctid >> 5;
+    const uint32_t trow = sh->tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 96);
+    for (int s = s0;; ++s) {
+        const StvTcStep st = steps[s];
+        if (st.kind == 0) {
+            run_subs<float2, 1>(x, braw1, subs + st.first, st.n, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
+        } else {
+            {   // A_hi, A_lo of this vector into TMEM (row = this thread's lane, block = warp / 4)
+                uint32_t v[32];
+#pragma unroll
+                for (int l = 0; l < 16; ++l) {
+                    v[2 * l] = tf32_rna(x[0][l].x);
+                    v[2 * l + 1] = tf32_rna(x[0][l].y);
+                }
+                tmem_st32(trow, v);
+#pragma unroll
+                for (int l = 0; l < 16; ++l) {
+                    v[2 * l] = __float_as_uint(x[0][l].x - __uint_as_float(v[2 * l]));
+                    v[2 * l + 1] = __float_as_uint(x[0][l].y - __uint_as_float(v[2 * l + 1]));
+                }
+                tmem_st32(trow + 32, v);
+            }
+            tc_wait_st();
+            tc_fence_before();
+            __syncthreads();
+            if (ctid == 0) {
+                tc_fence_after();
+                tc_issue(sh->tmem, smem_u32(opsm + (size_t)st.op * kTcOpBytes));
+                mma_commit(&sh->bar);
+            }
+            __syncwarp();
+            mbar_wait_spin(&sh->bar, phase);
+            phase ^= 1u;
+            tc_fence_after();
+            {
+                uint32_t v[32];
+                tmem_ld32(trow + 64, v);
+                tc_wait_ld();
+#pragma unroll
+                for (int l = 0; l < 16; ++l) x[0][l] = make_float2(__uint_as_float(v[2 * l]), __uint_as_float(v[2 * l + 1]));
+            }
+        }
+        if (st.last) break;
+    }
+    if (live) {
+        if (pair16) {
+#pragma unroll
+            for (int l = 0; l < 16; l += 2)
+                *(float4 *)&tile[bsw_s ^ so[l]] = make_float4(x[0][l].x, x[0][l].y, x[0][l + 1].x, x[0][l + 1].y);
+        } else {
+#pragma unroll
+            for (int l = 0; l < 16; ++l) tile[bsw_s ^ so[l]] = x[0][l];
+        }
+    }
+}
+
+// Tensor-core group pass: persistent CTAs (2 per SM, 256 threads, one tile buffer
+// each), tile ordinals in the permuted order of StvPass.tperm, contiguous per CTA.
+__global__ void __launch_bounds__(256, 2)
+k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off, uint32_t ntiles,
+                int dbg_flags, const __grid_constant__ RecParam rec) {
+    constexpr int NT = 256;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const StvPass *P = (const StvPass *)rec.b;
+    const uint8_t *grec = blob + pass_off;
+    const int S = P->S, L = P->L, h = P->h;
+    const uint64_t out_mask = P->out_mask, rank_bits = P->rank_bits;
+    const int nops = P->nops;
+    const int ntab = P->ntab;
+    const StvGroup *groups = (const StvGroup *)(rec.b + P->ops_off);
+    const StvTcStep *steps = (const StvTcStep *)(rec.b + P->tc_off);
+    const int ntc = P->ntc, nmop = P->ntcop;
+    const uint8_t *mat = rec.b + P->mat_off;
+    const uint32_t esz = 8;
+    // shared memory: operator slots (1024-aligned) | hashes | scalars | tables | tile | TcShared
+    uint8_t *opsm = smem;
+    uint8_t *hk = smem + (size_t)nmop * kTcOpBytes;
+    float2 *scal = (float2 *)(hk + 1024);
+    float2 *tables = (float2 *)(hk + 1536);
+    const uint32_t tab_pad = (P->tab_entries * esz + 127u) & ~127u;
+    float2 *tile = (float2 *)(hk + 1536 + tab_pad);
+    const uint32_t tile_elems = 1u << S;
+    TcShared *sh = (TcShared *)((uint8_t *)tile + (size_t)tile_elems * esz);
+    const uint32_t run_bytes = (1u << L) * esz;
+    const uint32_t nruns = 1u << h;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t hash_t = swz_hash_d((uint32_t)tid >> 3);
+    for (int k = tid; k < 1024; k += NT) hk[k] = (uint8_t)swz_hash_d(((uint32_t)NT * (uint32_t)k) >> 3);
+    uint64_t hmask = 0;
+    for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
+    const CopyPlan cp = make_copy_plan<NT>(hmask, run_bytes, nruns, tid);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh->tmem)),
+                     "n"(kTcCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&sh->bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < STV_TC_MAX_OPS) sh->key[tid] = ~0ull;
+    if (ntab) build_tables<float2, NT>(P, grec, 0, tables, scal, tid, true);   // static table entries
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    uint32_t phase = 0;
+
+    // contiguous range of permuted ordinals t' for this CTA
+    const uint64_t G = gridDim.x;
+    const uint32_t t_begin = (uint32_t)(((uint64_t)blockIdx.x * ntiles) / G);
+    const uint32_t t_end = (uint32_t)(((uint64_t)(blockIdx.x + 1) * ntiles) / G);
+    const int nord = __popcll(out_mask);
+    uint8_t *gstate = (uint8_t *)state;
+    for (uint32_t tp = t_begin; tp < t_end; ++tp) {
+        uint32_t tord = 0;   // t = tperm(t')
+        for (int i = 0; i < nord; ++i) tord |= ((tp >> i) & 1u) << P->tperm[i];
+        const uint64_t base = pdep64(tord, out_mask);
+        const uint64_t full_base = base | rank_bits;
+        if (!(dbg_flags & 2))
+            tile_copy_fast<true, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
+        cp_async_commit();
+        if (ntab) build_tables<float2, NT>(P, grec, full_base, tables, scal, tid, false);
+        __syncthreads();   // tables visible (the operator build reads them)
+        // operators whose dependency bits changed: one warp per M step
+        for (int s = warp; s < ntc; s += NT / 32) {
+            const StvTcStep st = steps[s];
+            if (st.kind != 1) continue;
+            const uint64_t key = full_base & st.dep;
+            if (key == sh->key[st.op]) continue;
+            const StvGroup &g = groups[st.group];
+            const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off) + st.first;
+            tc_build_op(subs, st.n, mat, (const StvDTab *)((const uint8_t *)P + P->tab_off), tables, full_base, tord,
+                        rank_bits, scal, opsm + (size_t)st.op * kTcOpBytes, lane);
+            __syncwarp();
+            if (lane == 0) sh->key[st.op] = key;
+        }
+        fence_proxy_async();   // operator slots (generic-proxy stores) -> tensor-core reads
+        cp_async_wait0();
+        __syncthreads();
+        if (!(dbg_flags & 1)) {
+            int s0 = 0;
+            for (int o = 0; o < nops; ++o) {
+                tc_group(tile, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh, phase, tid);
+                while (!steps[s0].last) ++s0;
+                ++s0;
+                __syncthreads();
+            }
+        }
+        if (!(dbg_flags & 2))
+            tile_copy_fast<false, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
+        __syncthreads();   // tile reads of the write-back done before the next load
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sh->tmem), "n"(kTcCols) : "memory");
+    }
+}

@@ -55,11 +55,18 @@ class Pass(ct.Structure):
                 ("n_local", ct.c_int32), ("nops", ct.c_int32), ("ops_off", ct.c_uint32), ("mat_off", ct.c_uint32),
                 ("mat_bytes", ct.c_uint32), ("cnot_c", ct.c_int32), ("cnot_t", ct.c_int32), ("diag_off", ct.c_uint32),
                 ("rec_bytes", ct.c_uint32), ("ntab", ct.c_int32), ("tab_off", ct.c_uint32), ("grouped", ct.c_int32),
-                ("tab_entries", ct.c_uint32), ("param_bytes", ct.c_uint32)]
+                ("tab_entries", ct.c_uint32), ("param_bytes", ct.c_uint32),
+                ("tc_off", ct.c_uint32), ("ntc", ct.c_int32), ("ntcop", ct.c_int32), ("tc_pad", ct.c_int32),
+                ("tperm", ct.c_uint8 * 48)]
 
 
-assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 144 and ct.sizeof(Term) == 16
-assert ct.sizeof(Group) == 256 and ct.sizeof(DTab) == 48
+class TcStep(ct.Structure):
+    _fields_ = [("kind", ct.c_int16), ("last", ct.c_int16), ("first", ct.c_int16), ("n", ct.c_int16),
+                ("op", ct.c_int32), ("group", ct.c_int32), ("dep", ct.c_uint64), ("pad", ct.c_uint64)]
+
+
+assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 208 and ct.sizeof(Term) == 16
+assert ct.sizeof(Group) == 256 and ct.sizeof(DTab) == 48 and ct.sizeof(TcStep) == 32
 
 U2_PAIRS = [(0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)]
 

@@ -154,6 +154,7 @@ def test_c4_shards_agree_mirror_norm(stv):
             st.apply(C.inverse_gates(circ.gates))
             a0 = st.amplitudes(np.array([0, 1, (1 << n) - 1], dtype=np.uint64))
         st.close()
+        del st
         _free()
     base = res[0][0]
     for g in (1, 2):

@@ -9,15 +9,19 @@ C ABI: sv_set_basis(|0..0>) + sv_apply_circuit(all gates of the workload)
 Workload at N=1: BASELINE.json configs[1] = c2, the 30-qubit 5x6-grid random
 circuit (20 cycles, sqrt X/Y/W + fSim(pi/2, pi/6)), complex64 state (8 GiB,
 far larger than the 126 MB L2, so no flush is needed between steps).
+N > 1 (torchrun, one rank per GPU): the weak-scaling ladder of BASELINE.json
+configs[4] (n = 34 + log2 N, 128 GiB per GPU; --config ladder, the default) or
+c4 strong scaling (--config c4).
 
-metric/value: BASELINE.json's metric "fused-gate state-vector update GB/s".
-value is GATE-EQUIVALENT GB/s = gates x 16 B x 2^n / (sec per circuit), the
-bandwidth a one-pass-per-gate complex64 simulator would need to match this
-time (BASELINE.md "Derived context" defines the same quantity for the
-paper's CPU numbers).  It is whole-job (all ranks) and inversely
-proportional to sec/circuit, also reported.  The per-pass HBM fraction of
-peak is the `roofline` object (dominant kernel: the fused gate-group tile
-pass k_group_pass).
+metric/value: BASELINE.json's metric "fused-gate state-vector update GB/s (% of
+HBM peak); sec/circuit".  value = the state-update bandwidth the fused passes
+achieve over the whole circuit: algorithmic HBM bytes of all passes (2 x 8 B
+per amplitude per fused pass) / sec per circuit, summed
+over ranks.  pct_of_hbm_peak = value per GPU / the measured HBM copy peak;
+sec_per_circuit and gate_equiv_gbs (gates x 16 B x 2^n / sec, the bandwidth a
+one-pass-per-gate simulator would need) are reported beside it.  The
+`roofline` object is the dominant kernel (the fused gate-group pass: the
+tcgen05 tensor-core kernel when it ran, else the CUDA-core FMA kernel).
 """
 import argparse
 import json
@@ -33,7 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fused-gate state-vector update GB/s (% of HBM peak); sec/circuit at n=30–37"
-UNIT = "GB/s (gate-equivalent)"
+UNIT = "GB/s"
 
 
 def parse():
@@ -42,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="", help="c1..c5, ladder (weak, N>1 default) or a ladder n (34..37)")
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--kmax", type=int, default=0)
     ap.add_argument("--budget", type=int, default=0)
@@ -58,16 +62,16 @@ def parse():
 
 # ---------------------------------------------------------------------------
 def workload(cfg, world):
+    """N=1: c2 by default.  N>1: the weak-scaling ladder n = 34 + log2(N) (BASELINE.json
+    configs[4]) unless --config names a config (c4: strong scaling)."""
     from inputs import circuits as C
-    if world == 1:
-        if cfg.startswith("c"):
-            return C.config(int(cfg[1:]))
-        return C.weak_ladder(int(cfg))
-    # weak scaling: 2^30 amplitudes per GPU, same circuit family as c2
-    g = world.bit_length() - 1
-    shapes = {30: (5, 6, 0), 31: (5, 7, 4), 32: (4, 8, 0), 33: (5, 7, 2)}
-    R, Cc, rm = shapes[30 + g]
-    return C.grid_circuit(f"weak{30 + g}", R, Cc, rm, 20, "fsim", 2)
+    if not cfg:
+        cfg = "c2" if world == 1 else "ladder"
+    if cfg == "ladder":
+        return C.weak_ladder(34 + world.bit_length() - 1)
+    if cfg.startswith("c"):
+        return C.config(int(cfg[1:]))
+    return C.weak_ladder(int(cfg))
 
 
 class ClockSampler:
@@ -121,29 +125,53 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the tile pass from the committed ncu --set full summary."""
-    p = os.path.join(ROOT, "profiles", "tile_pass_traffic.json")
+def ncu_traffic(tc=False):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of the dominant
+    kernel from the committed ncu --set full summary (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "tc_pass_traffic.json" if tc else "tile_pass_traffic.json")
     try:
         return json.load(open(p)).get("dram_bytes_per_launch")
     except Exception:
         return None
 
 
-def roof(gbs, hbm, peak_kind, tflops, fp32_peak, tile_bytes, launches, tile_ms, flops_per_step):
-    """Roofline of the dominant kernel (k_group_pass) against the resource that
-    binds it: HBM (algorithmic R+W bytes / time vs the measured copy peak) or
-    the FP32 FMA pipe (algorithmic flops / time vs 148 x 128 x 2 x clock)."""
+def tensor_peak():
+    """tf32 dense peak: the measured sustained bf16 GEMM rate (MEASURED_PEAKS.json; the
+    passes run inside a long step) x the nominal tf32/bf16 ratio 1.1/2.25 (B200_PROFILING.md)."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp.get("bf16_tflops_sustained") or mp["bf16_tflops"]) * 1.1 / 2.25, \
+            "measured bf16 sustained x nominal tf32/bf16 (1.1/2.25)"
+    except Exception:
+        return 1400.0 * 1.1 / 2.25, "fallback 1.4 PF bf16 sustained x 1.1/2.25"
+
+
+def roof(tc, gbs, hbm, peak_kind, tflops, fp32_peak, tile_bytes, launches, tile_ms, flops_per_step, tc_tflops,
+         tc_flops_per_step):
+    """Roofline of the dominant kernel, the fused gate-group pass.  Tensor-core kernel
+    (k_tc_group_pass): bound = HBM (the operator MMAs are far from the tensor peak), with
+    the tensor pipe's fraction beside it.  CUDA-core kernel (k_group_pass): HBM or the FP32
+    FMA pipe, whichever fraction is higher."""
     if gbs is None:
         return None
     f_hbm = gbs / hbm
     f_alu = tflops / fp32_peak if tflops else 0.0
-    common = {"kernel": "k_group_pass (fused gate-group tile pass)", "bytes_per_launch": tile_bytes, "launches": launches,
-              "avg_launch_ms": tile_ms / max(1, launches), "traffic": ncu_traffic(),
+    tpk, tpk_kind = tensor_peak()
+    common = {"kernel": "k_tc_group_pass (tcgen05 3xTF32 gate-group pass)" if tc else
+              "k_group_pass (CUDA-core FMA gate-group pass)",
+              "bytes_per_launch": tile_bytes, "launches": launches,
+              "avg_launch_ms": tile_ms / max(1, launches), "traffic": ncu_traffic(tc),
               "hbm": {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_hbm, "peak_kind": peak_kind},
               "alu": {"achieved": tflops, "peak": fp32_peak, "unit": "TFLOP/s", "frac": f_alu,
                       "flops_per_step": flops_per_step,
+                      "what": "algorithmic complex flops of the fused programs (8 x 2^k per k-qubit matrix)",
                       "peak_kind": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz"}}
+    if tc:
+        common["tensor"] = {"achieved": tc_tflops, "peak": tpk, "unit": "TFLOP/s",
+                            "frac": (tc_tflops / tpk) if tc_tflops else 0.0, "flops_per_step": tc_flops_per_step,
+                            "what": "tcgen05 kind::tf32 flops issued (3 products per operator step)",
+                            "peak_kind": tpk_kind}
+        return dict(bound="hbm", achieved=gbs, peak=hbm, unit="GB/s", frac=f_hbm, **common)
     if f_alu > f_hbm:
         return dict(bound="alu", achieved=tflops, peak=fp32_peak, unit="TFLOP/s", frac=f_alu, **common)
     return dict(bound="hbm", achieved=gbs, peak=hbm, unit="GB/s", frac=f_hbm, **common)
@@ -223,15 +251,16 @@ def run_reference(args, circ):
         step()
     t = time.perf_counter() - t0
     per_gate = t / (args.steps * gpp)
-    value = 16 * (1 << n) / per_gate / 1e9            # per-amplitude rate of the timed sample
+    value = 2 * 16 * (1 << n) / per_gate / 1e9        # state-update GB/s: each gate reads + writes the c128 state
     G = len(circ.gates)
-    sec_circ = G * 16 * (1 << circ.n) / (value * 1e9)  # the whole workload at that rate
+    sec_circ = per_gate * G * 2.0 ** (circ.n - n)      # the whole workload at that per-amplitude rate
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE.json configs[1] circuit)",
             "config": {"workload": circ.name, "n": circ.n, "gates": G, "state": "complex128 (oracle)",
-                       "step": f"{gpp} gates of the circuit, gate by gate", "l2": "state 16 GiB >> L2"},
+                       "step": f"{gpp} gates of the circuit, gate by gate (one full read + write of the state per gate)",
+                       "l2": "state >> L2"},
             "sec_per_circuit": sec_circ,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps} steps x {gpp} gates of {circ.name} (n={n}), complex128, "
@@ -249,7 +278,7 @@ def main():
     circ = workload(args.config, world)
     if args.impl == "reference":
         if rank == 0:
-            run_reference(args, workload(args.config, 1))
+            run_reference(args, circ)
         return
 
     import numpy as np
@@ -287,6 +316,9 @@ def main():
     tile_ms = 0.0
     flops_total = 0.0
     tile_launches = 0
+    tc_flops_total = 0.0
+    remap_ms = 0.0
+    remap_bytes = 0.0
     launches = 0
     plan_ms = []
     kinds = {}
@@ -301,6 +333,9 @@ def main():
             tile_launches += s["n_pass"]["tile_low"] + s["n_pass"]["tile_high"]
             launches += s["n_kernels"] + 1           # + the init kernel of set_basis
             flops_total += s["alg_flops"]
+            tc_flops_total += s["tc_flops"]
+            remap_ms += s["pass_ms"]["remap"]
+            remap_bytes += s["remap_bytes"]
             plan_ms.append(s["plan_ms"])
             kinds = s
         e1.record(stream)
@@ -312,11 +347,13 @@ def main():
         ms = float(t.item())
     sec = ms / 1e3
     G = len(circ.gates)
-    value = G * 16 * (1 << n) / sec / 1e9        # gate-equivalent GB/s, whole job
     esz = 8 if args.dtype == "c64" else 16
     n_local = n - (world.bit_length() - 1)
-    tile_bytes = 2 * esz * (1 << n_local)        # algorithmic R+W bytes per tile-pass launch
     hbm, peak_kind = peaks()
+    alg_bytes = kinds["alg_bytes"]               # per rank and circuit: 2 x esz x 2^n_local per pass
+    value = alg_bytes * world / sec / 1e9        # fused-gate state-update GB/s, whole job
+    gate_equiv = G * 16 * (1 << n) / sec / 1e9
+    tile_bytes = 2 * esz * (1 << n_local)        # algorithmic R+W bytes per tile-pass launch
     achieved = tile_bytes / (tile_ms / max(1, tile_launches) / 1e3) / 1e9 if tile_launches else None
     # FP32 CUDA-core peak: 148 SMs x 128 FMA lanes x 2 flop x max SM clock (B200_PROFILING.md
     # unit counts; MEASURED_PEAKS.json sm_max_mhz), the ceiling of an FMA-bound tile pass
@@ -326,6 +363,8 @@ def main():
         smhz = 1965.0
     fp32_peak = 148 * 128 * 2 * smhz * 1e6 / 1e12 if args.dtype == "c64" else 148 * 64 * 2 * smhz * 1e6 / 1e12
     flops_ach = (flops_total / (tile_ms / 1e3) / 1e12) if tile_ms > 0 else None
+    tc_ach = (tc_flops_total / (tile_ms / 1e3) / 1e12) if tile_ms > 0 and tc_flops_total else None
+    used_tc = kinds.get("n_tc_pass", 0) > 0
 
     # e2e: host gate list in, full state vector out (pinned host memory)
     e2e = None
@@ -354,7 +393,7 @@ def main():
         barrier()
         ems = ee0.elapsed_time(ee1) / args.e2e_steps
         h2d = int(st.stats().get("h2d_bytes", 0)) or None
-        e2e = {"value": G * 16 * (1 << n) / (ems / 1e3) / 1e9, "unit": UNIT,
+        e2e = {"value": alg_bytes * world / (ems / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d if h2d is not None else 0,
                "d2h_bytes_per_step": (esz << n) if world == 1 else 0,
                "ms_per_step": ems,
@@ -367,26 +406,36 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         t, on, ng, note = oracle_sample(circ, args.oracle_gates, cpu_cores())
-        cpu = {"value": ng * 16 * (1 << on) / t / 1e9, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+        cpu = {"value": ng * 2 * 16 * (1 << on) / t / 1e9, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
                "sample": f"first {ng} of {G} gates of {circ.name} (n={n}), complex128 gate-by-gate, "
-                         f"{cpu_cores()} OpenMP threads, {t:.2f} s{note}",
+                         f"{cpu_cores()} OpenMP threads, {t:.2f} s{note}; value = its state-update GB/s "
+                         f"(each gate reads + writes the 16-B complex128 state)",
                "sec_per_circuit_extrapolated": t / ng * G * 2.0 ** (n - on)}
+    remap = None
+    if world > 1 or remap_bytes > 0:
+        remap = {"bytes_per_rank_per_step": remap_bytes / max(1, args.steps), "ms_per_step": remap_ms / max(1, args.steps),
+                 "nvlink_gbs": (remap_bytes / (remap_ms / 1e3) / 1e9) if remap_ms > 0 else None}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak" if (world == 1 or (args.config or "ladder") == "ladder") else "strong",
         "vs_baseline": None, "dtype": "f32" if args.dtype == "c64" else "f64",
         "data": "synthetic (seeded BASELINE.json circuit; no dataset)",
         "config": {"workload": circ.name, "n": n, "gates": G, "state": args.dtype,
                    "state_bytes_per_gpu": esz << n_local, "l2": "state >> 126 MB L2 (no flush needed)",
-                   "kmax": args.kmax or 4, "budget": args.budget or 1000, "tile_bits": args.tile_bits or None},
+                   "kmax": args.kmax or 4, "budget": args.budget or 1000, "tile_bits": args.tile_bits or None,
+                   "flags": args.flags, "gate_kernel": "tcgen05 tensor-core" if used_tc else "CUDA-core FMA"},
         "sec_per_circuit": sec,
+        "pct_of_hbm_peak": 100.0 * value / world / hbm,
+        "gate_equiv_gbs": gate_equiv,
         "passes": {k: v for k, v in kinds["n_pass"].items() if v},
+        "tc_passes": kinds.get("n_tc_pass", 0), "tc_steps": kinds.get("n_tc_steps", 0),
         "ops": kinds["n_ops"],
         "plan_ms": statistics.median(plan_ms),
-        "hbm_effective_gbs": kinds["alg_bytes"] / sec / 1e9,
         "gpu_launches": launches,
-        "roofline": roof(achieved, hbm, peak_kind, flops_ach, fp32_peak, tile_bytes, tile_launches, tile_ms,
-                         flops_total / max(1, args.steps)),
+        "roofline": roof(used_tc, achieved, hbm, peak_kind, flops_ach, fp32_peak, tile_bytes, tile_launches, tile_ms,
+                         flops_total / max(1, args.steps), tc_ach, tc_flops_total / max(1, args.steps)),
+        "remap": remap,
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,

@@ -188,6 +188,11 @@ typedef struct {
     int32_t n_kernels;     /* kernels launched by the last call                    */
     double h2d_bytes;      /* host->device bytes copied by the last call (plan)    */
     double alg_flops;      /* algorithmic flops of the fused tile passes */
+    double tc_flops;       /* tensor-core flops issued by the tcgen05 group passes
+                              (3xTF32: 3 real 32x32 products per 16-amplitude vector and
+                              operator step = 384 flop per amplitude per step)     */
+    int32_t n_tc_pass;     /* group passes that ran on the tensor-core kernel       */
+    int32_t n_tc_steps;    /* their operator (MMA) steps                            */
 } sv_stats;
 sv_status sv_last_run_stats(const sv_state *s, sv_stats *out);
 

@@ -60,7 +60,8 @@ class Stats(ctypes.Structure):
                 ("n_pass", ctypes.c_int32 * 8), ("pass_ms", ctypes.c_double * 8),
                 ("alg_bytes", ctypes.c_double), ("remap_bytes", ctypes.c_double),
                 ("n_ops", ctypes.c_int32 * 4), ("n_kernels", ctypes.c_int32), ("h2d_bytes", ctypes.c_double),
-                ("alg_flops", ctypes.c_double)]
+                ("alg_flops", ctypes.c_double), ("tc_flops", ctypes.c_double),
+                ("n_tc_pass", ctypes.c_int32), ("n_tc_steps", ctypes.c_int32)]
 
 
 _lib = None
@@ -297,7 +298,8 @@ class State:
                 "pass_ms": dict(zip(PASS_KINDS, list(s.pass_ms))),
                 "alg_bytes": s.alg_bytes, "remap_bytes": s.remap_bytes,
                 "n_ops": dict(zip(["dense", "diag", "cnot", "group"], list(s.n_ops))),
-                "n_kernels": s.n_kernels, "h2d_bytes": s.h2d_bytes, "alg_flops": s.alg_flops}
+                "n_kernels": s.n_kernels, "h2d_bytes": s.h2d_bytes, "alg_flops": s.alg_flops,
+                "tc_flops": s.tc_flops, "n_tc_pass": s.n_tc_pass, "n_tc_steps": s.n_tc_steps}
 
     def frame(self):
         perm = (ctypes.c_int32 * 64)()

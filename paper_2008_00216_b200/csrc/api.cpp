@@ -373,9 +373,16 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
         cudaError_t e = cudaSuccess;
         if (ps.kind == PASS_TILE) {
             kind = hp->h == 0 ? 1 : 2;
-            if (hp->grouped && hp->ntc > 0 && !s->c128())
+            if (hp->grouped && hp->ntc > 0 && !s->c128()) {
                 e = launch_tc_group_pass(s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
                                          enc_local, hp->param_bytes, hp->tab_entries, hp->ntcop, s->stream, &kernels);
+                const StvTcStep *tcs = (const StvTcStep *)((const uint8_t *)hp + hp->tc_off);
+                int ms = 0;
+                for (int k = 0; k < hp->ntc; ++k) ms += tcs[k].kind == 1;
+                s->stats.n_tc_pass++;
+                s->stats.n_tc_steps += ms;
+                s->stats.tc_flops += 384.0 * ms * std::ldexp(1.0, enc_local);
+            }
             else if (hp->grouped)
                 e = launch_group_pass(s->c128(), s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
                                       enc_local, hp->param_bytes, hp->tab_entries, pass_flops_per_amp(ps.ops),
@@ -419,11 +426,27 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
     CK(s, cudaEventElapsedTime(&ms, s->ev0, s->ev1));
     s->stats.run_ms = ms;
     if (prof) {
+        // STV_PASS_LOG=<file>: one line per pass (tuning / profiles; not part of the ABI)
+        const char *plog = getenv("STV_PASS_LOG");
+        FILE *pf = plog ? fopen(plog, "a") : nullptr;
         for (size_t i = 0; i < plan.passes.size(); ++i) {
             float pm = 0;
             CK(s, cudaEventElapsedTime(&pm, s->pev[i], s->pev[i + 1]));
             s->stats.pass_ms[kind_of[i]] += pm;
+            if (pf) {
+                const StvPass *hp = (const StvPass *)&enc.blob[enc.pass_off[i]];
+                int msteps = 0;
+                if (hp->ntc > 0) {
+                    const StvTcStep *tcs = (const StvTcStep *)((const uint8_t *)hp + hp->tc_off);
+                    for (int k = 0; k < hp->ntc; ++k) msteps += tcs[k].kind == 1;
+                }
+                fprintf(pf, "{\"pass\": %zu, \"kind\": %d, \"S\": %d, \"L\": %d, \"h\": %d, \"groups\": %d, "
+                            "\"ntc\": %d, \"msteps\": %d, \"flops_per_amp\": %.1f, \"ms\": %.4f}\n",
+                        i, hp->kind, hp->S, hp->L, hp->h, hp->nops, hp->ntc, msteps,
+                        plan.passes[i].kind == PASS_TILE ? pass_flops_per_amp(plan.passes[i].ops) : 0.0, pm);
+            }
         }
+        if (pf) fclose(pf);
     }
     s->stats.n_kernels = kernels;
     // new frame: logical -> actual

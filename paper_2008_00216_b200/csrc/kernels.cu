@@ -1794,27 +1794,40 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
     return e;
 }
 
-// tensor-core group pass (tc_pass.cuh): 2 CTAs per SM (TMEM 256 columns each)
-cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off, int S,
-                                 int n_local, uint32_t rec_bytes, uint32_t tab_entries, int ntcop, cudaStream_t st,
-                                 int *kernels) {
-    const size_t smem = (size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127) +
-                        ((size_t)8 << S) + sizeof(TcShared);
-    const uint64_t ntiles = 1ull << (n_local - S);
-    if (smem > 113 * 1024 || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
+// tensor-core group pass (tc_pass.cuh): 2 CTAs per SM (TMEM 256 columns each); a
+// double-buffered tile ring when it fits the shared memory of 2 CTAs, else one buffer
+template <int NS>
+static cudaError_t tc_launch(void *state, const uint8_t *dblob, uint32_t pass_off, uint32_t ntiles, size_t smem,
+                             const RecParam &rp, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_tc_group_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+        cudaFuncSetAttribute(k_tc_group_pass<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
         attr = true;
     }
-    static thread_local RecParam rp;
-    std::memcpy(rp.b, hrec, rec_bytes);
     uint64_t grid = (uint64_t)num_sms() * 2;
     if (grid > ntiles) grid = ntiles;
     static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
-    k_tc_group_pass<<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, (uint32_t)ntiles, dbg, rp);
-    ++*kernels;
+    k_tc_group_pass<NS><<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, ntiles, dbg, rp);
     return cudaGetLastError();
+}
+
+cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off, int S,
+                                 int n_local, uint32_t rec_bytes, uint32_t tab_entries, int ntcop, cudaStream_t st,
+                                 int *kernels) {
+    const size_t fixed = (size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127) +
+                         sizeof(TcShared);
+    const size_t tile = (size_t)8 << S;
+    const uint64_t ntiles = 1ull << (n_local - S);
+    const size_t cap = 113 * 1024;   // 2 CTAs per SM
+    if (fixed + tile > cap || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
+    static thread_local RecParam rp;
+    std::memcpy(rp.b, hrec, rec_bytes);
+    static const int ns_env = getenv("STV_TC_NS") ? atoi(getenv("STV_TC_NS")) : 2;
+    cudaError_t e = (ns_env >= 2 && fixed + 2 * tile <= cap)
+                        ? tc_launch<2>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, rp, st)
+                        : tc_launch<1>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, rp, st);
+    ++*kernels;
+    return e;
 }
 
 cudaError_t launch_diag_pass(bool c128, void *state, const uint8_t *dblob, uint32_t pass_off, int S, int n_local,

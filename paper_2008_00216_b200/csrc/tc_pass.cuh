@@ -130,28 +130,27 @@ __device__ __forceinline__ void tc_build_op(const StvSub *__restrict__ subs, int
     }
 }
 
-// The MMA of one M step for both blocks: 3xTF32, 4 K-slices of 8 each.
-__device__ __forceinline__ void tc_issue(uint32_t tmem, uint32_t slot_saddr) {
+// The MMA of one M step for block b (128 rows): 3xTF32, 4 K-slices of 8 each.
+__device__ __forceinline__ void tc_issue_block(uint32_t tmem, int b, uint32_t slot_saddr) {
+    const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
-        const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
+    for (int kk = 0; kk < 4; ++kk)
+        mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-            mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, kk > 0);
+    for (int kk = 0; kk < 4; ++kk)
+        mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 4096 + 256 * kk, 128, 1024), kTcIdesc, 1);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-            mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 4096 + 256 * kk, 128, 1024), kTcIdesc, 1);
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-            mma_tf32_ts(d, al + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, 1);
-    }
+    for (int kk = 0; kk < 4; ++kk)
+        mma_tf32_ts(d, al + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, 1);
 }
 
 struct TcShared {
-    uint64_t bar;
+    uint64_t bar[2];
     uint32_t tmem;
     uint32_t pad;
     uint64_t key[STV_TC_MAX_OPS];
+    uint64_t cm[48];    // base xor-mask when the permuted ordinal's trailing-ones count is j
+    uint32_t tm[48];    // ordinal xor-mask for the same carry
 };
 
 // One group on the resident tile with tensor-core M steps: thread ctid owns vector ctid.
@@ -169,12 +168,12 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         bsw = w & 0xffffu;
         braw = w >> 16;
     }
-    uint32_t so[16];
+    uint32_t so[16];   // byte offsets of the 16 register amplitudes (swizzled)
 #pragma unroll
     for (int l = 0; l < 16; l += 2) {
         const uint2 w = *(const uint2 *)&g.sw_off[l];
-        so[l] = w.x;
-        so[l + 1] = w.y;
+        so[l] = w.x << 3;
+        so[l + 1] = w.y << 3;
     }
     uint32_t bsw_g = bsw, bsw_s = bsw;
     if (g.nflip_g | g.nflip_s) {
@@ -191,6 +190,9 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         bsw_g ^= flip_delta(0, g.nflip_g);
         bsw_s ^= flip_delta(STV_MAX_FLIPS, g.nflip_s);
     }
+    bsw_g <<= 3;   // bytes
+    bsw_s <<= 3;
+    uint8_t *tb = (uint8_t *)tile;
     const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off);
     const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
     const bool pair16 = g.pair16;
@@ -199,13 +201,13 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         if (pair16) {
 #pragma unroll
             for (int l = 0; l < 16; l += 2) {
-                const float4 q = *(const float4 *)&tile[bsw_g ^ so[l]];
+                const float4 q = *(const float4 *)(tb + (bsw_g ^ so[l]));
                 x[0][l] = make_float2(q.x, q.y);
                 x[0][l + 1] = make_float2(q.z, q.w);
             }
         } else {
 #pragma unroll
-            for (int l = 0; l < 16; ++l) x[0][l] = tile[bsw_g ^ so[l]];
+            for (int l = 0; l < 16; ++l) x[0][l] = *(const float2 *)(tb + (bsw_g ^ so[l]));
         }
     } else {
 #pragma unroll
@@ -219,31 +221,37 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         if (st.kind == 0) {
             run_subs<float2, 1>(x, braw1, subs + st.first, st.n, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
         } else {
-            {   // A_hi, A_lo of this vector into TMEM (row = this thread's lane, block = warp / 4)
+            {   // A_hi = x itself (the tensor core reads the top 19 bits: tf32 truncation of x),
+                // A_lo = x - trunc_tf32(x) (exact in fp32) -> TMEM row of this thread, block warp / 4
                 uint32_t v[32];
 #pragma unroll
                 for (int l = 0; l < 16; ++l) {
-                    v[2 * l] = tf32_rna(x[0][l].x);
-                    v[2 * l + 1] = tf32_rna(x[0][l].y);
+                    v[2 * l] = __float_as_uint(x[0][l].x);
+                    v[2 * l + 1] = __float_as_uint(x[0][l].y);
                 }
                 tmem_st32(trow, v);
 #pragma unroll
                 for (int l = 0; l < 16; ++l) {
-                    v[2 * l] = __float_as_uint(x[0][l].x - __uint_as_float(v[2 * l]));
-                    v[2 * l + 1] = __float_as_uint(x[0][l].y - __uint_as_float(v[2 * l + 1]));
+                    const float2 t = make_float2(__uint_as_float(v[2 * l] & 0xffffe000u),
+                                                 __uint_as_float(v[2 * l + 1] & 0xffffe000u));
+                    const float2 lo = __fadd2_rn(x[0][l], make_float2(-t.x, -t.y));
+                    v[2 * l] = __float_as_uint(lo.x);
+                    v[2 * l + 1] = __float_as_uint(lo.y);
                 }
                 tmem_st32(trow + 32, v);
             }
             tc_wait_st();
             tc_fence_before();
-            __syncthreads();
-            if (ctid == 0) {
+            // each half of the CTA (warps 0-3: block 0, warps 4-7: block 1) syncs and issues its own MMAs
+            const int half = ctid >> 7;
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
+            if ((ctid & 127) == 0) {
                 tc_fence_after();
-                tc_issue(sh->tmem, smem_u32(opsm + (size_t)st.op * kTcOpBytes));
-                mma_commit(&sh->bar);
+                tc_issue_block(sh->tmem, half, smem_u32(opsm + (size_t)st.op * kTcOpBytes));
+                mma_commit(&sh->bar[half]);
             }
             __syncwarp();
-            mbar_wait_spin(&sh->bar, phase);
+            mbar_wait_spin(&sh->bar[half], phase);
             phase ^= 1u;
             tc_fence_after();
             {
@@ -260,16 +268,33 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         if (pair16) {
 #pragma unroll
             for (int l = 0; l < 16; l += 2)
-                *(float4 *)&tile[bsw_s ^ so[l]] = make_float4(x[0][l].x, x[0][l].y, x[0][l + 1].x, x[0][l + 1].y);
+                *(float4 *)(tb + (bsw_s ^ so[l])) = make_float4(x[0][l].x, x[0][l].y, x[0][l + 1].x, x[0][l + 1].y);
         } else {
 #pragma unroll
-            for (int l = 0; l < 16; ++l) tile[bsw_s ^ so[l]] = x[0][l];
+            for (int l = 0; l < 16; ++l) *(float2 *)(tb + (bsw_s ^ so[l])) = x[0][l];
         }
     }
 }
 
-// Tensor-core group pass: persistent CTAs (2 per SM, 256 threads, one tile buffer
-// each), tile ordinals in the permuted order of StvPass.tperm, contiguous per CTA.
+// Tile copy with per-thread offsets precomputed once per CTA: thread t moves the
+// 16-B chunks c = t + 256 k (k < kTcChunks) between global (tile base + goff[k])
+// and its swizzled shared-memory slot soff[k] = 16 (c ^ H(c >> 3)) (see tile_copy_swz).
+constexpr int kTcChunks = 8;   // 2^12 complex64 amplitudes = 2048 chunks over 256 threads
+template <bool kLoad>
+__device__ __forceinline__ void tc_tile_copy(uint8_t *gtile, uint8_t *stile, const uint64_t (&goff)[kTcChunks],
+                                             const uint32_t (&soff)[kTcChunks], int nk) {
+#pragma unroll
+    for (int k = 0; k < kTcChunks; ++k) {
+        if (k >= nk) break;
+        if (kLoad) cp_async16(stile + soff[k], gtile + goff[k]);
+        else *(uint4 *)(gtile + goff[k]) = *(const uint4 *)(stile + soff[k]);
+    }
+}
+
+// Tensor-core group pass: persistent CTAs (2 per SM, 256 threads), tile ordinals in
+// the permuted order of StvPass.tperm, a contiguous range per CTA; NS = 2: the next
+// tile's load overlaps this tile's work (1: single buffer when shared memory is short).
+template <int NS>
 __global__ void __launch_bounds__(256, 2)
 k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off, uint32_t ntiles,
                 int dbg_flags, const __grid_constant__ RecParam rec) {
@@ -286,34 +311,57 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     const int ntc = P->ntc, nmop = P->ntcop;
     const uint8_t *mat = rec.b + P->mat_off;
     const uint32_t esz = 8;
-    // shared memory: operator slots (1024-aligned) | hashes | scalars | tables | tile | TcShared
+    // shared memory: operator slots (1024-aligned) | hashes | scalars | tables | NS tiles | TcShared
     uint8_t *opsm = smem;
     uint8_t *hk = smem + (size_t)nmop * kTcOpBytes;
     float2 *scal = (float2 *)(hk + 1024);
     float2 *tables = (float2 *)(hk + 1536);
     const uint32_t tab_pad = (P->tab_entries * esz + 127u) & ~127u;
-    float2 *tile = (float2 *)(hk + 1536 + tab_pad);
+    float2 *tiles = (float2 *)(hk + 1536 + tab_pad);
     const uint32_t tile_elems = 1u << S;
-    TcShared *sh = (TcShared *)((uint8_t *)tile + (size_t)tile_elems * esz);
+    TcShared *sh = (TcShared *)((uint8_t *)tiles + (size_t)NS * tile_elems * esz);
     const uint32_t run_bytes = (1u << L) * esz;
     const uint32_t nruns = 1u << h;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t hash_t = swz_hash_d((uint32_t)tid >> 3);
-    for (int k = tid; k < 1024; k += NT) hk[k] = (uint8_t)swz_hash_d(((uint32_t)NT * (uint32_t)k) >> 3);
     uint64_t hmask = 0;
     for (int r = 0; r < h; ++r) hmask |= 1ull << P->hpos[r];
-    const CopyPlan cp = make_copy_plan<NT>(hmask, run_bytes, nruns, tid);
+    (void)run_bytes;
+    (void)nruns;
+    // this thread's chunks of a tile: global byte offset from the tile base, shared slot
+    const int nchunk = (int)(tile_elems >> 1);
+    const int nk = (nchunk - tid + NT - 1) / NT;
+    uint64_t goff[kTcChunks];
+    uint32_t soff[kTcChunks];
+#pragma unroll
+    for (int k = 0; k < kTcChunks; ++k) {
+        const uint32_t c = (uint32_t)tid + NT * (uint32_t)k;
+        const uint32_t i = 2 * c;   // first tile-local amplitude of the chunk
+        goff[k] = (pdep64(i >> L, hmask) + (i & ((1u << L) - 1))) * esz;
+        soff[k] = 16u * (c ^ swz_hash_d(c >> 3));
+    }
+    const int nord = __popcll(out_mask);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh->tmem)),
                      "n"(kTcCols)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    if (tid == 0) {
-        mbar_init(&sh->bar, 1);
+    if (tid == 32) {
+        mbar_init(&sh->bar[0], 1);
+        mbar_init(&sh->bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < STV_TC_MAX_OPS) sh->key[tid] = ~0ull;
+    if (tid < 48) {   // carry masks of the permuted ordinal: bits 0..tid flip together
+        uint64_t cm = 0;
+        uint32_t tm = 0;
+        for (int i = 0; i <= tid && i < nord; ++i) {
+            tm |= 1u << P->tperm[i];
+            cm |= pdep64(1ull << P->tperm[i], out_mask);
+        }
+        sh->cm[tid] = cm;
+        sh->tm[tid] = tm;
+    }
     if (ntab) build_tables<float2, NT>(P, grec, 0, tables, scal, tid, true);   // static table entries
     tc_fence_before();
     __syncthreads();
@@ -324,16 +372,23 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     const uint64_t G = gridDim.x;
     const uint32_t t_begin = (uint32_t)(((uint64_t)blockIdx.x * ntiles) / G);
     const uint32_t t_end = (uint32_t)(((uint64_t)(blockIdx.x + 1) * ntiles) / G);
-    const int nord = __popcll(out_mask);
+    uint32_t tord = 0;   // t = tperm(t'), advanced by carry masks
+    for (int i = 0; i < nord; ++i) tord |= ((t_begin >> i) & 1u) << P->tperm[i];
+    uint64_t base = pdep64(tord, out_mask);
+    uint64_t lbase = base;   // next tile to load
     uint8_t *gstate = (uint8_t *)state;
-    for (uint32_t tp = t_begin; tp < t_end; ++tp) {
-        uint32_t tord = 0;   // t = tperm(t')
-        for (int i = 0; i < nord; ++i) tord |= ((tp >> i) & 1u) << P->tperm[i];
-        const uint64_t base = pdep64(tord, out_mask);
-        const uint64_t full_base = base | rank_bits;
-        if (!(dbg_flags & 2))
-            tile_copy_fast<true, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
+    auto issue = [&](uint32_t tp, int slot) {   // load tile tp (if in range) into ring slot
+        if (tp < t_end && !(dbg_flags & 2))
+            tc_tile_copy<true>(gstate + lbase * esz, (uint8_t *)(tiles + (size_t)slot * tile_elems), goff, soff, nk);
         cp_async_commit();
+        if (tp + 1 < t_end) lbase ^= sh->cm[__ffs(~tp) - 1];
+    };
+    if (NS == 2) issue(t_begin, 0);
+    for (uint32_t tp = t_begin; tp < t_end; ++tp) {
+        const int slot = NS == 2 ? (int)((tp - t_begin) & 1u) : 0;
+        float2 *tile = tiles + (size_t)slot * tile_elems;
+        const uint64_t full_base = base | rank_bits;
+        if (NS == 1) issue(tp, 0);
         if (ntab) build_tables<float2, NT>(P, grec, full_base, tables, scal, tid, false);
         __syncthreads();   // tables visible (the operator build reads them)
         // operators whose dependency bits changed: one warp per M step
@@ -350,7 +405,12 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
             if (lane == 0) sh->key[st.op] = key;
         }
         fence_proxy_async();   // operator slots (generic-proxy stores) -> tensor-core reads
-        cp_async_wait0();
+        if (NS == 2) {
+            issue(tp + 1, slot ^ 1);   // the other slot was freed by the previous iteration's last barrier
+            cp_async_wait1();
+        } else {
+            cp_async_wait0();
+        }
         __syncthreads();
         if (!(dbg_flags & 1)) {
             int s0 = 0;
@@ -361,10 +421,15 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
                 __syncthreads();
             }
         }
-        if (!(dbg_flags & 2))
-            tile_copy_fast<false, NT>(gstate, (uint8_t *)tile, base, hmask, cp, nruns, esz, tid, hash_t, hk);
-        __syncthreads();   // tile reads of the write-back done before the next load
+        if (!(dbg_flags & 2)) tc_tile_copy<false>(gstate + base * esz, (uint8_t *)tile, goff, soff, nk);
+        if (tp + 1 < t_end) {
+            const int j = __ffs(~tp) - 1;
+            base ^= sh->cm[j];
+            tord ^= sh->tm[j];
+        }
+        __syncthreads();   // write-back reads of this slot done before it is reloaded
     }
+    cp_async_wait0();
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {

@@ -37,7 +37,6 @@ cudaError_t launch_cnot(bool c128, void *state, int c, int t, int n_local, cudaS
 cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off, int S,
                                  int n_local, uint32_t rec_bytes, uint32_t tab_entries, int ntcop, cudaStream_t st,
                                  int *kernels);
-cudaError_t launch_bitswap(bool c128, void *state, int a, int b, int n_bits, cudaStream_t st, int *kernels);
 cudaError_t launch_norm(bool c128, const void *state, uint64_t N, double *part, int np, double *out, cudaStream_t st,
                         int *kernels);
 cudaError_t launch_fill(bool c128, void *state, uint64_t N, double val, int64_t one_at, cudaStream_t st, int *kernels);
@@ -124,6 +123,11 @@ struct sv_state {
     bool c128() const { return dt == SV_C128; }
     size_t esz() const { return dt == SV_C128 ? 16 : 8; }
     uint64_t nloc_amps() const { return 1ull << n_local; }
+    // amplitudes held by this process's buffer (virtual shards: all 2^n, shard r at r * 2^n_local)
+    uint64_t buf_amps() const { return virt ? 1ull << n : 1ull << n_local; }
+    int nshards() const { return virt ? 1 << n_global : 1; }
+    void *shard(int r) const { return (uint8_t *)buf + (virt ? ((size_t)r * esz()) << n_local : 0); }
+    uint64_t shard_rank(int r) const { return virt ? (uint64_t)r : (uint64_t)rank; }
 };
 
 namespace {
@@ -164,7 +168,7 @@ uint64_t rank_value(const sv_state *s) { return s->virt ? 0 : (uint64_t)s->rank;
 
 sv_status fill(sv_state *s, double val, int64_t one_at) {
     int k = 0;
-    CK(s, launch_fill(s->c128(), s->buf, s->nloc_amps(), val, one_at, s->stream, &k));
+    CK(s, launch_fill(s->c128(), s->buf, s->buf_amps(), val, one_at, s->stream, &k));
     CK(s, cudaStreamSynchronize(s->stream));
     return SV_OK;
 }
@@ -248,8 +252,11 @@ sv_status sv_create_virtual(int n, sv_dtype dt, int g, sv_state **out) {
     if (n - g < 4) return fail(SV_ERR_INVALID_ARG, "virtual shards: need at least 4 local qubits per shard (n - g >= 4)");
     sv_status st = sv_create(n, dt, out);
     if (st) return st;
+    // one buffer holds the 2^g shards back to back (shard r = the amplitudes whose top g
+    // physical bits equal r, i.e. a real rank's buffer); every pass runs per shard with that
+    // rank's encoding, remaps go through the distributed pack -> exchange -> unpack path
     (*out)->n_global = g;
-    (*out)->n_local = n;     // one buffer holds all shards; the planner keeps the top g bits global
+    (*out)->n_local = n - g;
     (*out)->virt = true;
     return SV_OK;
 }
@@ -328,7 +335,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
     fr.xmask = s->xmask;
     const uint32_t flags = opt ? opt->flags : 0;
     std::vector<PGate> pg = to_physical(s->n, gates, ng, fr, flags);
-    PlanOptions po = resolve_options(opt, (int)s->esz(), s->virt ? s->n - s->n_global : s->n_local);
+    PlanOptions po = resolve_options(opt, (int)s->esz(), s->n_local);
     int sigma[64];
     for (int v = 0; v < 64; ++v) sigma[v] = v;
     Plan plan;
@@ -337,24 +344,33 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
     } catch (const std::exception &ex) {
         return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
     }
-    const int enc_local = s->n_local;   // virtual: the whole buffer is addressed directly
-    Encoded enc = encode(plan, enc_local, s->c128(), s->virt ? 0 : (uint64_t)s->rank << s->n_local);
-    // rank bits into every pass header
-    for (uint32_t off : enc.pass_off) {
-        StvPass *hp = (StvPass *)&enc.blob[off];
-        hp->rank_bits = s->virt ? 0 : (uint64_t)s->rank << s->n_local;
+    // one encoding per shard this process holds (rank bits, selectors on global bits)
+    const int nsh = s->nshards();
+    std::vector<uint8_t> blob;
+    std::vector<std::vector<uint32_t>> poff(nsh);
+    for (int r = 0; r < nsh; ++r) {
+        const uint64_t rb = s->shard_rank(r) << s->n_local;
+        Encoded enc = encode(plan, s->n_local, s->c128(), rb);
+        while (blob.size() & 255) blob.push_back(0);
+        const uint32_t at = (uint32_t)blob.size();
+        for (uint32_t off : enc.pass_off) {
+            StvPass *hp = (StvPass *)&enc.blob[off];
+            hp->rank_bits = rb;
+            poff[r].push_back(at + off);
+        }
+        blob.insert(blob.end(), enc.blob.begin(), enc.blob.end());
     }
     auto t1 = std::chrono::steady_clock::now();
     std::memset(&s->stats, 0, sizeof(s->stats));
     s->stats.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-    s->stats.alg_bytes = plan.alg_bytes;
-    s->stats.alg_flops = plan.alg_flops;
-    s->stats.h2d_bytes = (double)enc.blob.size();
-    if ((st = ensure(s, (void **)&s->hblob, &s->hblob_cap, enc.blob.size(), true))) return st;
-    if ((st = ensure(s, (void **)&s->dblob, &s->dblob_cap, enc.blob.size(), false))) return st;
-    std::memcpy(s->hblob, enc.blob.data(), enc.blob.size());
+    s->stats.alg_bytes = plan.alg_bytes * nsh;
+    s->stats.alg_flops = plan.alg_flops * nsh;
+    s->stats.h2d_bytes = (double)blob.size();
+    if ((st = ensure(s, (void **)&s->hblob, &s->hblob_cap, blob.size(), true))) return st;
+    if ((st = ensure(s, (void **)&s->dblob, &s->dblob_cap, blob.size(), false))) return st;
+    std::memcpy(s->hblob, blob.data(), blob.size());
     CK(s, cudaEventRecord(s->ev0, s->stream));
-    CK(s, cudaMemcpyAsync(s->dblob, s->hblob, enc.blob.size(), cudaMemcpyHostToDevice, s->stream));
+    CK(s, cudaMemcpyAsync(s->dblob, s->hblob, blob.size(), cudaMemcpyHostToDevice, s->stream));
     const bool prof = flags & SV_OPT_PROFILE;
     if (prof && s->pev.size() < plan.passes.size() + 1) {
         for (size_t i = s->pev.size(); i < plan.passes.size() + 1; ++i) {
@@ -368,51 +384,50 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
     if (prof) CK(s, cudaEventRecord(s->pev[0], s->stream));
     for (size_t i = 0; i < plan.passes.size(); ++i) {
         const PPass &ps = plan.passes[i];
-        const StvPass *hp = (const StvPass *)&enc.blob[enc.pass_off[i]];
         int kind = 7;
         cudaError_t e = cudaSuccess;
-        if (ps.kind == PASS_TILE) {
-            kind = hp->h == 0 ? 1 : 2;
-            if (hp->grouped && hp->ntc > 0 && !s->c128()) {
-                e = launch_tc_group_pass(s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
-                                         enc_local, hp->param_bytes, hp->tab_entries, hp->ntcop, s->stream, &kernels);
-                const StvTcStep *tcs = (const StvTcStep *)((const uint8_t *)hp + hp->tc_off);
-                int ms = 0;
-                for (int k = 0; k < hp->ntc; ++k) ms += tcs[k].kind == 1;
-                s->stats.n_tc_pass++;
-                s->stats.n_tc_steps += ms;
-                s->stats.tc_flops += 384.0 * ms * std::ldexp(1.0, enc_local);
-            }
-            else if (hp->grouped)
-                e = launch_group_pass(s->c128(), s->buf, s->dblob, &enc.blob[enc.pass_off[i]], enc.pass_off[i], hp->S,
-                                      enc_local, hp->param_bytes, hp->tab_entries, pass_flops_per_amp(ps.ops),
-                                      s->stream, &kernels);
-            else
-                e = launch_tile_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, hp->rec_bytes,
-                                     hp->ntab, s->stream, &kernels);
-            for (auto &o : ps.ops) s->stats.n_ops[o.type == OP_DENSE ? 0 : o.type == OP_DIAG ? 1 : o.type == OP_CNOT ? 2 : 3]++;
-        } else if (ps.kind == PASS_DIAG) {
-            kind = 3;
-            e = launch_diag_pass(s->c128(), s->buf, s->dblob, enc.pass_off[i], hp->S, enc_local, s->stream, &kernels);
-        } else if (ps.kind == PASS_CNOT) {
-            kind = 4;
-            int c = hp->cnot_c, t = hp->cnot_t;
-            bool run = true;
-            if (!s->virt && c >= s->n_local) {   // control on a global bit: per-rank predicate
-                run = (s->rank >> (c - s->n_local)) & 1;
-                c = -1;
-            }
-            if (run) e = launch_cnot(s->c128(), s->buf, c, t, enc_local, s->stream, &kernels);
-        } else if (ps.kind == PASS_REMAP) {
+        if (ps.kind == PASS_REMAP) {
             kind = 5;
-            if (s->virt) {
-                for (auto &sw : ps.swaps) {
-                    e = launch_bitswap(s->c128(), s->buf, sw.first, sw.second, s->n, s->stream, &kernels);
-                    if (e != cudaSuccess) break;
-                    s->stats.remap_bytes += (double)s->esz() * std::ldexp(1.0, s->n - 1) / (1 << s->n_global);
+            if ((st = dist_remap(s, ps.swaps, &kernels))) return st;
+        }
+        for (int r = 0; r < nsh && ps.kind != PASS_REMAP && e == cudaSuccess; ++r) {
+            void *sbuf = s->shard(r);
+            const uint32_t po_r = poff[r][i];
+            const StvPass *hp = (const StvPass *)&blob[po_r];
+            if (ps.kind == PASS_TILE) {
+                kind = hp->h == 0 ? 1 : 2;
+                if (hp->grouped && hp->ntc > 0 && !s->c128()) {
+                    e = launch_tc_group_pass(sbuf, s->dblob, &blob[po_r], po_r, hp->S, s->n_local, hp->param_bytes,
+                                             hp->tab_entries, hp->ntcop, s->stream, &kernels);
+                    const StvTcStep *tcs = (const StvTcStep *)((const uint8_t *)hp + hp->tc_off);
+                    int ms = 0;
+                    for (int k = 0; k < hp->ntc; ++k) ms += tcs[k].kind == 1;
+                    if (r == 0) s->stats.n_tc_pass++;
+                    if (r == 0) s->stats.n_tc_steps += ms;
+                    s->stats.tc_flops += 384.0 * ms * std::ldexp(1.0, s->n_local);
+                } else if (hp->grouped) {
+                    e = launch_group_pass(s->c128(), sbuf, s->dblob, &blob[po_r], po_r, hp->S, s->n_local,
+                                          hp->param_bytes, hp->tab_entries, pass_flops_per_amp(ps.ops), s->stream,
+                                          &kernels);
+                } else {
+                    e = launch_tile_pass(s->c128(), sbuf, s->dblob, po_r, hp->S, s->n_local, hp->rec_bytes, hp->ntab,
+                                         s->stream, &kernels);
                 }
-            } else {
-                if ((st = dist_remap(s, ps.swaps, &kernels))) return st;
+                if (r == 0)
+                    for (auto &o : ps.ops)
+                        s->stats.n_ops[o.type == OP_DENSE ? 0 : o.type == OP_DIAG ? 1 : o.type == OP_CNOT ? 2 : 3]++;
+            } else if (ps.kind == PASS_DIAG) {
+                kind = 3;
+                e = launch_diag_pass(s->c128(), sbuf, s->dblob, po_r, hp->S, s->n_local, s->stream, &kernels);
+            } else if (ps.kind == PASS_CNOT) {
+                kind = 4;
+                int c = hp->cnot_c, t = hp->cnot_t;
+                bool run = true;
+                if (c >= s->n_local) {   // control on a global bit: per-rank predicate
+                    run = (s->shard_rank(r) >> (c - s->n_local)) & 1;
+                    c = -1;
+                }
+                if (run) e = launch_cnot(s->c128(), sbuf, c, t, s->n_local, s->stream, &kernels);
             }
         }
         if (e != cudaSuccess) return cuda_fail(s, e, "pass launch");
@@ -434,7 +449,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
             CK(s, cudaEventElapsedTime(&pm, s->pev[i], s->pev[i + 1]));
             s->stats.pass_ms[kind_of[i]] += pm;
             if (pf) {
-                const StvPass *hp = (const StvPass *)&enc.blob[enc.pass_off[i]];
+                const StvPass *hp = (const StvPass *)&blob[poff[0][i]];
                 int msteps = 0;
                 if (hp->ntc > 0) {
                     const StvTcStep *tcs = (const StvTcStep *)((const uint8_t *)hp + hp->tc_off);
@@ -527,7 +542,7 @@ sv_status sv_norm(sv_state *s, double *out) {
     if (st) return st;
     if (!out) return fail(SV_ERR_INVALID_ARG, "out is NULL");
     int k = 0;
-    CK(s, launch_norm(s->c128(), s->buf, s->nloc_amps(), s->dnorm, kNormParts, s->dnorm + kNormParts, s->stream, &k));
+    CK(s, launch_norm(s->c128(), s->buf, s->buf_amps(), s->dnorm, kNormParts, s->dnorm + kNormParts, s->stream, &k));
     if (s->world > 1) {
         int r = g_nccl.allReduce(s->dnorm + kNormParts, s->dnorm + kNormParts, 1, ncclFloat64, ncclSum, s->comm,
                                  s->stream);
@@ -749,8 +764,13 @@ cudaError_t launch_pack(bool c128, const void *state, void *dst, const int *lbit
 }
 
 namespace {
+// Global<->local bit swaps: every rank packs the 2^m - 1 chunks (values of
+// the swapped local bits) that leave it, exchanges them with the ranks that differ in the
+// swapped global bits, and unpacks what it receives into the vacated chunks.  Real ranks
+// exchange with grouped ncclSend/ncclRecv; virtual shards (one process, one GPU) run the
+// same schedule with one device-to-device copy per (shard, peer) chunk.
 sv_status dist_remap(sv_state *s, const std::vector<std::pair<int, int>> &swaps, int *kernels) {
-    if (s->world < 2) return SV_OK;
+    if (s->world < 2 && !s->virt) return SV_OK;
     const int m = (int)swaps.size();
     if (m < 1 || m > 8 || m > s->n_global) return fail(SV_ERR_INVALID_ARG, "remap: 1..min(8, g) swapped bits");
     uint32_t gbits = 0;
@@ -762,49 +782,67 @@ sv_status dist_remap(sv_state *s, const std::vector<std::pair<int, int>> &swaps,
         gbits |= 1u << (sw[i].first - s->n_local);
         lbits[i] = sw[i].second;
     }
-    int32_t peer[256];
-    sv_status st = sv_remap_peers(s->n_global, s->rank, gbits, m, peer);
-    if (st) return st;
-    // my own chunk index: the value of my selected global bits
-    int mine = 0;
-    for (int i = 0; i < m; ++i) mine |= ((s->rank >> (sw[i].first - s->n_local)) & 1) << i;
+    const int nsh = s->nshards();
+    std::vector<std::vector<int32_t>> peer(nsh, std::vector<int32_t>((size_t)1 << m));
+    std::vector<int> mine(nsh, 0);   // a shard's own chunk: the value of its selected global bits
+    for (int r = 0; r < nsh; ++r) {
+        const int rank = (int)s->shard_rank(r);
+        sv_status st = sv_remap_peers(s->n_global, rank, gbits, m, peer[r].data());
+        if (st) return st;
+        for (int i = 0; i < m; ++i) mine[r] |= ((rank >> (sw[i].first - s->n_local)) & 1) << i;
+    }
+    auto slot = [](int c, int own) { return c < own ? c : c - 1; };
     const uint64_t chunk_amps = 1ull << (s->n_local - m);
-    const uint64_t piece = std::min<uint64_t>(chunk_amps, (256ull << 20) / s->esz());   // 256 MiB pieces
     const int npeers = (1 << m) - 1;
-    const size_t need = 2ull * npeers * piece * s->esz();
-    if ((st = ensure(s, &s->xbuf, &s->xbuf_bytes, need, false))) return st;
-    uint8_t *sendb = (uint8_t *)s->xbuf, *recvb = sendb + (size_t)npeers * piece * s->esz();
+    const uint64_t cap = s->virt ? (1ull << 30) : (512ull << 20);   // staging bytes
+    const uint64_t piece = std::max<uint64_t>(1, std::min<uint64_t>(chunk_amps, cap / (2ull * nsh * npeers * s->esz())));
+    const size_t slot_bytes = (size_t)piece * s->esz();
+    const size_t need = 2ull * nsh * npeers * slot_bytes;
+    sv_status st = ensure(s, &s->xbuf, &s->xbuf_bytes, need, false);
+    if (st) return st;
+    auto sendb = [&](int r, int sl) { return (uint8_t *)s->xbuf + ((size_t)r * npeers + sl) * slot_bytes; };
+    auto recvb = [&](int r, int sl) {
+        return (uint8_t *)s->xbuf + ((size_t)(nsh + r) * npeers + sl) * slot_bytes;
+    };
     for (uint64_t off = 0; off < chunk_amps; off += piece) {
         const uint64_t cnt = std::min(piece, chunk_amps - off);
-        int slot = 0;
-        for (int c = 0; c < (1 << m); ++c) {
-            if (c == mine) continue;
-            cudaError_t e = launch_pack(s->c128(), s->buf, sendb + (size_t)slot * piece * s->esz(), lbits, m, c, off,
-                                        cnt, s->n_local, false, s->stream, kernels);
-            if (e != cudaSuccess) return cuda_fail(s, e, "remap pack");
-            ++slot;
+        const size_t b = cnt * s->esz();
+        for (int r = 0; r < nsh; ++r)
+            for (int c = 0; c < (1 << m); ++c) {
+                if (c == mine[r]) continue;
+                cudaError_t e = launch_pack(s->c128(), s->shard(r), sendb(r, slot(c, mine[r])), lbits, m, c, off, cnt,
+                                            s->n_local, false, s->stream, kernels);
+                if (e != cudaSuccess) return cuda_fail(s, e, "remap pack");
+            }
+        if (s->virt) {
+            // rank p sends its chunk mine[r] to r, which receives it in its slot for chunk c (p = peer[r][c])
+            for (int r = 0; r < nsh; ++r)
+                for (int c = 0; c < (1 << m); ++c) {
+                    if (c == mine[r]) continue;
+                    const int p = peer[r][c];
+                    CK(s, cudaMemcpyAsync(recvb(r, slot(c, mine[r])), sendb(p, slot(mine[r], mine[p])), b,
+                                          cudaMemcpyDeviceToDevice, s->stream));
+                }
+        } else {
+            g_nccl.groupStart();
+            for (int c = 0; c < (1 << m); ++c) {
+                if (c == mine[0]) continue;
+                const int sl = slot(c, mine[0]);
+                int r1 = g_nccl.send(sendb(0, sl), b, ncclUint8, peer[0][c], s->comm, s->stream);
+                int r2 = g_nccl.recv(recvb(0, sl), b, ncclUint8, peer[0][c], s->comm, s->stream);
+                if (r1 || r2) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclSend/Recv (remap)"); }
+            }
+            if (g_nccl.groupEnd()) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclGroupEnd (remap)"); }
         }
-        g_nccl.groupStart();
-        slot = 0;
-        for (int c = 0; c < (1 << m); ++c) {
-            if (c == mine) continue;
-            const size_t b = cnt * s->esz();
-            int r1 = g_nccl.send(sendb + (size_t)slot * piece * s->esz(), b, ncclUint8, peer[c], s->comm, s->stream);
-            int r2 = g_nccl.recv(recvb + (size_t)slot * piece * s->esz(), b, ncclUint8, peer[c], s->comm, s->stream);
-            if (r1 || r2) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclSend/Recv (remap)"); }
-            ++slot;
-        }
-        if (g_nccl.groupEnd()) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclGroupEnd (remap)"); }
-        slot = 0;
-        for (int c = 0; c < (1 << m); ++c) {
-            if (c == mine) continue;
-            // data from peer[c] (its chunk `mine`) lands in my chunk slot c
-            cudaError_t e = launch_pack(s->c128(), s->buf, recvb + (size_t)slot * piece * s->esz(), lbits, m, c, off,
-                                        cnt, s->n_local, true, s->stream, kernels);
-            if (e != cudaSuccess) return cuda_fail(s, e, "remap unpack");
-            ++slot;
-        }
-        s->stats.remap_bytes += (double)npeers * cnt * s->esz();
+        for (int r = 0; r < nsh; ++r)
+            for (int c = 0; c < (1 << m); ++c) {
+                if (c == mine[r]) continue;
+                // data from peer[r][c] (its chunk mine[r]) lands in r's chunk c
+                cudaError_t e = launch_pack(s->c128(), s->shard(r), recvb(r, slot(c, mine[r])), lbits, m, c, off, cnt,
+                                            s->n_local, true, s->stream, kernels);
+                if (e != cudaSuccess) return cuda_fail(s, e, "remap unpack");
+            }
+        s->stats.remap_bytes += (double)npeers * b;   // per rank
     }
     return SV_OK;
 }

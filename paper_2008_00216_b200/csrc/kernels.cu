@@ -12,7 +12,6 @@
 //                    only amplitudes whose phase != 1.
 //   k_cnot_pass      a9: CNOT as a pure permutation, touches only the half of
 //                    the state with control = 1.
-//   k_bitswap        remap of one global<->local bit pair for virtual shards.
 //   k_norm_*         a10: fp64 fixed-shape reduction.
 //   k_init_*, k_gather  a11.
 #include <cuda_runtime.h>
@@ -1410,20 +1409,6 @@ k_cnot_pass(C *__restrict__ state, int c, int t, uint64_t nitems) {
 }
 
 // swap physical index bits a and b (a != b): exchanges alpha_{..1_a..0_b..} <-> alpha_{..0_a..1_b..}
-template <typename C>
-__global__ void __launch_bounds__(STV_THREADS) k_bitswap(C *__restrict__ state, int a, int b, uint64_t nitems) {
-    const int lo_b = min(a, b), hi_b = max(a, b);
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nitems;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t i = ((v >> lo_b) << (lo_b + 1)) | (v & ((1ull << lo_b) - 1));
-        i = ((i >> hi_b) << (hi_b + 1)) | (i & ((1ull << hi_b) - 1));
-        const uint64_t x = i | (1ull << a), y = i | (1ull << b);
-        C p = state[x];
-        state[x] = state[y];
-        state[y] = p;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // norm: fp64 partials over a fixed grid, fixed-shape trees (deterministic)
 // ---------------------------------------------------------------------------
@@ -1855,14 +1840,6 @@ cudaError_t launch_cnot(bool c128, void *state, int c, int t, int n_local, cudaS
     const uint64_t items = 1ull << (n_local - (c >= 0 ? 2 : 1));
     if (c128) k_cnot_pass<double2><<<grid_for(items), STV_THREADS, 0, st>>>((double2 *)state, c, t, items);
     else k_cnot_pass<float2><<<grid_for(items), STV_THREADS, 0, st>>>((float2 *)state, c, t, items);
-    ++*kernels;
-    return cudaGetLastError();
-}
-
-cudaError_t launch_bitswap(bool c128, void *state, int a, int b, int n_bits, cudaStream_t st, int *kernels) {
-    const uint64_t items = 1ull << (n_bits - 2);
-    if (c128) k_bitswap<double2><<<grid_for(items), STV_THREADS, 0, st>>>((double2 *)state, a, b, items);
-    else k_bitswap<float2><<<grid_for(items), STV_THREADS, 0, st>>>((float2 *)state, a, b, items);
     ++*kernels;
     return cudaGetLastError();
 }

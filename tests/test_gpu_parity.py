@@ -113,6 +113,22 @@ def test_virtual_shards(stv, g, dtype):
     assert_parity(psi, oracle.run(circ), dtype)
 
 
+@pytest.mark.parametrize("g", [1, 2, 3])
+def test_virtual_shards_n24_pack_exchange(stv, g):
+    """Virtual shards run every pass per shard with that rank's encoding and every remap
+    through the distributed pack -> exchange -> unpack path (device copies in place of
+    ncclSend/ncclRecv), default planner options, n = 24."""
+    circ = C.grid_circuit("g24", 4, 6, 0, 10, "fsim", 20 + g)
+    st = stv.State(circ.n, "c64", virtual_g=g)
+    st.set_basis(circ.x0)
+    st.apply(circ.gates)
+    s = st.stats()
+    psi = st.amplitudes()
+    st.close()
+    assert s["n_pass"]["remap"] > 0 and s["remap_bytes"] > 0
+    assert_parity(psi, oracle.run(circ), "c64")
+
+
 def test_virtual_shards_grid(stv):
     circ = C.grid_circuit("g", 4, 5, 0, 12, "fsim", 9)
     st = stv.State(circ.n, "c64", virtual_g=3)

@@ -1781,18 +1781,18 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
 
 // tensor-core group pass (tc_pass.cuh): 2 CTAs per SM (TMEM 256 columns each); a
 // double-buffered tile ring when it fits the shared memory of 2 CTAs, else one buffer
-template <int NS>
+template <int NS, bool FULL>
 static cudaError_t tc_launch(void *state, const uint8_t *dblob, uint32_t pass_off, uint32_t ntiles, size_t smem,
                              const RecParam &rp, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_tc_group_pass<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+        cudaFuncSetAttribute(k_tc_group_pass<NS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
         attr = true;
     }
     uint64_t grid = (uint64_t)num_sms() * 2;
     if (grid > ntiles) grid = ntiles;
     static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
-    k_tc_group_pass<NS><<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, ntiles, dbg, rp);
+    k_tc_group_pass<NS, FULL><<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, ntiles, dbg, rp);
     return cudaGetLastError();
 }
 
@@ -1808,9 +1808,12 @@ cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_
     static thread_local RecParam rp;
     std::memcpy(rp.b, hrec, rec_bytes);
     static const int ns_env = getenv("STV_TC_NS") ? atoi(getenv("STV_TC_NS")) : 2;
-    cudaError_t e = (ns_env >= 2 && fixed + 2 * tile <= cap)
-                        ? tc_launch<2>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, rp, st)
-                        : tc_launch<1>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, rp, st);
+    const bool two = ns_env >= 2 && fixed + 2 * tile <= cap, full = S == 12;
+    cudaError_t e;
+    if (two) e = full ? tc_launch<2, true>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, rp, st)
+                      : tc_launch<2, false>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, rp, st);
+    else e = full ? tc_launch<1, true>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, rp, st)
+                  : tc_launch<1, false>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, rp, st);
     ++*kernels;
     return e;
 }

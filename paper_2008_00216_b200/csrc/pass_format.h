@@ -97,6 +97,7 @@ struct alignas(16) StvPass {
 // tile base bits `dep` change).  `last` ends the group's steps.
 #define STV_TC_MAX_OPS 12
 #define STV_TC_MAX_STEPS 64
+#define STV_TC_MAX_GROUPS 16
 struct alignas(16) StvTcStep {
     int16_t kind, last, first, n;
     int32_t op, group;

@@ -1645,6 +1645,7 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
     const int nord = __builtin_popcountll(hd.out_mask);
     const size_t need = st.size() * sizeof(StvTcStep) + 16;
     if (nop == 0 || nop > STV_TC_MAX_OPS || st.size() > STV_TC_MAX_STEPS || nord > 48 ||
+        grecs.size() > STV_TC_MAX_GROUPS ||
         b.size() - at + need > (size_t)STV_REC_PARAM_BYTES)
         return;   // FMA group pass
     // tile order: ordinal bits the operators depend on vary slowest within a CTA's range

@@ -130,38 +130,54 @@ __device__ __forceinline__ void tc_build_op(const StvSub *__restrict__ subs, int
     }
 }
 
-// The MMA of one M step for block b (128 rows): 3xTF32, 4 K-slices of 8 each.
-__device__ __forceinline__ void tc_issue_block(uint32_t tmem, int b, uint32_t slot_saddr) {
+template <bool kAcc>
+__device__ __forceinline__ void mma_tf32_ts_c(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc) {
+    if (kAcc)
+        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(d_tmem), "r"(a_tmem),
+                     "l"(b_desc), "n"(kTcIdesc)
+                     : "memory");
+    else
+        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 0;" ::"r"(d_tmem), "r"(a_tmem),
+                     "l"(b_desc), "n"(kTcIdesc)
+                     : "memory");
+}
+// The MMA of one M step for block b (128 rows): 3xTF32, 4 K-slices of 8 each.  desc0 =
+// the slot's descriptor; the start-address field (bits 0..13, 16-B units) advances by
+// 16 per K-slice (256 B) and by 256 for the lo half (4 KB) -- no carry within a slot.
+__device__ __forceinline__ void tc_issue_block(uint32_t tmem, int b, uint64_t desc0) {
     const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
+    mma_tf32_ts_c<false>(d, ah, desc0);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-        mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, kk > 0);
+    for (int kk = 1; kk < 4; ++kk) mma_tf32_ts_c<true>(d, ah + 8 * kk, desc0 + 16 * kk);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-        mma_tf32_ts(d, ah + 8 * kk, umma_desc(slot_saddr + 4096 + 256 * kk, 128, 1024), kTcIdesc, 1);
+    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts_c<true>(d, ah + 8 * kk, desc0 + 256 + 16 * kk);
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-        mma_tf32_ts(d, al + 8 * kk, umma_desc(slot_saddr + 256 * kk, 128, 1024), kTcIdesc, 1);
+    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts_c<true>(d, al + 8 * kk, desc0 + 16 * kk);
 }
 
-struct TcShared {
+struct alignas(16) TcShared {
     uint64_t bar[2];
     uint32_t tmem;
     uint32_t pad;
     uint64_t key[STV_TC_MAX_OPS];
     uint64_t cm[48];    // base xor-mask when the permuted ordinal's trailing-ones count is j
     uint32_t tm[48];    // ordinal xor-mask for the same carry
+    alignas(16) uint32_t gso[STV_TC_MAX_GROUPS][16];   // per group: swizzled register offsets in bytes
 };
 
 // One group on the resident tile with tensor-core M steps: thread ctid owns vector ctid.
+// FULL: the tile has 256 vectors (S = 12), every thread is live.  gso: the group's 16
+// register offsets in bytes (shared memory, staged once per CTA).
+template <bool FULL>
 __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
                                          const StvTcStep *__restrict__ steps, int s0, const uint8_t *__restrict__ mat,
                                          const float2 *__restrict__ tables, uint64_t full_base, uint32_t tord,
                                          const uint8_t *__restrict__ grec, const float2 *__restrict__ scal,
-                                         const uint8_t *__restrict__ opsm, TcShared *sh, uint32_t &phase, int ctid) {
+                                         const uint8_t *__restrict__ opsm, TcShared *sh, const uint32_t *gso,
+                                         uint32_t &phase, int ctid) {
     const int nvb = g.nvb;
     const uint32_t nvec = 1u << nvb;
-    const bool live = (uint32_t)ctid < nvec;
+    const bool live = FULL || (uint32_t)ctid < nvec;
     uint32_t braw = 0, bsw = 0;
     {
         const uint32_t w = __ldg((const uint32_t *)(grec + g.vtab_off) + ctid);
@@ -170,10 +186,12 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
     }
     uint32_t so[16];   // byte offsets of the 16 register amplitudes (swizzled)
 #pragma unroll
-    for (int l = 0; l < 16; l += 2) {
-        const uint2 w = *(const uint2 *)&g.sw_off[l];
-        so[l] = w.x << 3;
-        so[l + 1] = w.y << 3;
+    for (int l = 0; l < 16; l += 4) {
+        const uint4 w = *(const uint4 *)&gso[l];
+        so[l] = w.x;
+        so[l + 1] = w.y;
+        so[l + 2] = w.z;
+        so[l + 3] = w.w;
     }
     uint32_t bsw_g = bsw, bsw_s = bsw;
     if (g.nflip_g | g.nflip_s) {
@@ -247,7 +265,7 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
             asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
             if ((ctid & 127) == 0) {
                 tc_fence_after();
-                tc_issue_block(sh->tmem, half, smem_u32(opsm + (size_t)st.op * kTcOpBytes));
+                tc_issue_block(sh->tmem, half, umma_desc(smem_u32(opsm + (size_t)st.op * kTcOpBytes), 128, 1024));
                 mma_commit(&sh->bar[half]);
             }
             __syncwarp();
@@ -294,7 +312,7 @@ __device__ __forceinline__ void tc_tile_copy(uint8_t *gtile, uint8_t *stile, con
 // Tensor-core group pass: persistent CTAs (2 per SM, 256 threads), tile ordinals in
 // the permuted order of StvPass.tperm, a contiguous range per CTA; NS = 2: the next
 // tile's load overlaps this tile's work (1: single buffer when shared memory is short).
-template <int NS>
+template <int NS, bool FULL>
 __global__ void __launch_bounds__(256, 2)
 k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off, uint32_t ntiles,
                 int dbg_flags, const __grid_constant__ RecParam rec) {
@@ -352,6 +370,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < STV_TC_MAX_OPS) sh->key[tid] = ~0ull;
+    for (int e = tid; e < nops * 16; e += NT) sh->gso[e >> 4][e & 15] = groups[e >> 4].sw_off[e & 15] << 3;
     if (tid < 48) {   // carry masks of the permuted ordinal: bits 0..tid flip together
         uint64_t cm = 0;
         uint32_t tm = 0;
@@ -415,7 +434,8 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         if (!(dbg_flags & 1)) {
             int s0 = 0;
             for (int o = 0; o < nops; ++o) {
-                tc_group(tile, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh, phase, tid);
+                tc_group<FULL>(tile, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh,
+                               sh->gso[o], phase, tid);
                 while (!steps[s0].last) ++s0;
                 ++s0;
                 __syncthreads();

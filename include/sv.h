@@ -95,7 +95,7 @@ typedef struct {
 #define SV_OPT_NO_VARIANTS  0x80u /* do not merge 2-qubit sub-op chains into per-tile variant matrices      */
 #define SV_OPT_NO_TC        0x100u /* complex64 gate groups on the CUDA-core FMA path only (no tcgen05 pass) */
 typedef struct {
-    int32_t kmax;        /* max qubits of one fused dense op (1..5); 0 = default (4)     */
+    int32_t kmax;        /* max qubits of one fused dense block (1..4; register bits of a gate group); 0 = 4 */
     int32_t tile_bits;   /* max tile bits |S| of a fused pass; 0 = default              */
     int32_t low_bits;    /* min contiguous low bits in every tile; 0 = default            */
     int32_t budget;      /* per-pass compute budget, FMA-equivalents per amplitude; 0 = default */

@@ -634,9 +634,10 @@ static OpsEval make_ops(const std::vector<PGate> &gs, uint64_t S, const PlanOpti
             // diagonal gates never claim register bits: their in-tile qubits outside
             // the group become per-vector terms ("V-bits")
             const uint64_t in_tile = (g.type == GType::DIAG ? 0 : dm) & S;
-            // kmax bounds the register bits (the dense block size) of a group: <= 4 (16-amplitude vectors)
-            bool ok = !(qm & sc.blockedAll) && !(dm & sc.blockedDense) &&
-                      __builtin_popcountll(sc.T | in_tile) <= std::min(opt.kmax, STV_GROUP_BITS);
+            // kmax bounds the register bits (the dense block size) of a group: <= 4 (16-amplitude
+            // vectors); a gate wider than kmax still gets a group of its own
+            const int lim = std::max(std::min(opt.kmax, STV_GROUP_BITS), __builtin_popcountll(in_tile));
+            bool ok = !(qm & sc.blockedAll) && !(dm & sc.blockedDense) && __builtin_popcountll(sc.T | in_tile) <= lim;
             if (!ok) {
                 sc.blockedAll |= dm;
                 sc.blockedDense |= qm & ~dm;

@@ -310,6 +310,13 @@ def main():
         st.set_basis(0)
         st.apply_marshalled(arr, len(circ.gates), opts)
 
+    # a cold plan (SV_OPT_NO_PLAN_CACHE) for the record; the timed steps repeat the same
+    # circuit from |0..0>, so they reuse the cached plan and its resident device blob
+    st.set_basis(0)
+    st.apply_marshalled(arr, len(circ.gates), stv.options(kmax=args.kmax, tile_bits=args.tile_bits,
+                                                          low_bits=args.low_bits, budget=args.budget,
+                                                          flags=args.flags | stv.OPT_NO_PLAN_CACHE))
+    plan_cold_ms = st.stats()["plan_ms"]
     for _ in range(max(3, args.warmup)):
         one_step()
     barrier()
@@ -432,6 +439,8 @@ def main():
         "tc_passes": kinds.get("n_tc_pass", 0), "tc_steps": kinds.get("n_tc_steps", 0),
         "ops": kinds["n_ops"],
         "plan_ms": statistics.median(plan_ms),
+        "plan_cold_ms": plan_cold_ms,
+        "plan_cache": "hit" if statistics.median(plan_ms) < 0.5 * plan_cold_ms else "miss",
         "gpu_launches": launches,
         "roofline": roof(used_tc, achieved, hbm, peak_kind, flops_ach, fp32_peak, tile_bytes, tile_launches, tile_ms,
                          flops_total / max(1, args.steps), tc_ach, tc_flops_total / max(1, args.steps)),

@@ -115,6 +115,19 @@ struct sv_state {
     size_t didx_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> pev;
+    // plan cache (small-n latency): the last few (circuit, frame, options) -> plan + encoded blobs
+    struct PlanEntry {
+        std::vector<uint8_t> key;
+        stv::Plan plan;
+        std::vector<uint8_t> blob;
+        std::vector<std::vector<uint32_t>> poff;
+        int perm_out[64];
+        uint64_t xmask_out = 0;
+        uint64_t id = 0;
+    };
+    std::vector<PlanEntry> pcache;
+    uint64_t pcache_next = 1;
+    uint64_t dblob_id = 0;            // cache entry whose blob is resident in dblob (0: none)
     // distributed
     ncclComm_t comm = nullptr;
     void *xbuf = nullptr;         // remap send/recv staging
@@ -329,48 +342,101 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
     std::string err = validate(s->n, gates, ng);
     if (!err.empty()) return fail(SV_ERR_INVALID_ARG, err);
     auto t0 = std::chrono::steady_clock::now();
-    // plan in "virtual physical" bits = the state's current actual bits
-    Frame fr;
-    for (int q = 0; q < 64; ++q) fr.perm[q] = s->perm[q];
-    fr.xmask = s->xmask;
     const uint32_t flags = opt ? opt->flags : 0;
-    std::vector<PGate> pg = to_physical(s->n, gates, ng, fr, flags);
-    PlanOptions po = resolve_options(opt, (int)s->esz(), s->n_local);
-    int sigma[64];
-    for (int v = 0; v < 64; ++v) sigma[v] = v;
-    Plan plan;
-    try {
-        plan = build_plan(s->n, s->n_global, (int)s->esz(), pg, po, sigma);
-    } catch (const std::exception &ex) {
-        return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
-    }
-    // one encoding per shard this process holds (rank bits, selectors on global bits)
-    const int nsh = s->nshards();
-    std::vector<uint8_t> blob;
-    std::vector<std::vector<uint32_t>> poff(nsh);
-    for (int r = 0; r < nsh; ++r) {
-        const uint64_t rb = s->shard_rank(r) << s->n_local;
-        Encoded enc = encode(plan, s->n_local, s->c128(), rb);
-        while (blob.size() & 255) blob.push_back(0);
-        const uint32_t at = (uint32_t)blob.size();
-        for (uint32_t off : enc.pass_off) {
-            StvPass *hp = (StvPass *)&enc.blob[off];
-            hp->rank_bits = rb;
-            poff[r].push_back(at + off);
+    // cache key: everything the plan and its encodings depend on (SV_OPT_PROFILE excluded)
+    std::vector<uint8_t> key;
+    {
+        auto add = [&](const void *p, size_t nb) { key.insert(key.end(), (const uint8_t *)p, (const uint8_t *)p + nb); };
+        const int32_t hdr[6] = {s->n, (int32_t)s->dt, s->n_global, s->virt ? 1 : 0, s->rank, s->world};
+        add(hdr, sizeof(hdr));
+        sv_options o{};
+        if (opt) o = *opt;
+        o.flags &= ~SV_OPT_PROFILE;
+        add(&o, sizeof(o));
+        add(s->perm, sizeof(int) * (size_t)s->n);
+        add(&s->xmask, sizeof(s->xmask));
+        for (size_t i = 0; i < ng; ++i) {
+            const sv_gate &g = gates[i];
+            const int32_t gi[4] = {g.kind, (int32_t)g.flags, g.q0, g.q1};
+            add(gi, sizeof(gi));
+            add(&g.theta, sizeof(double));
+            add(&g.phi, sizeof(double));
+            if (g.m) add(g.m, sizeof(double) * (g.kind == SV_U1 ? 8 : g.kind == SV_U2 ? 32 : 0));
         }
-        blob.insert(blob.end(), enc.blob.begin(), enc.blob.end());
     }
+    const bool use_cache = !(flags & SV_OPT_NO_PLAN_CACHE);
+    sv_state::PlanEntry *ent = nullptr;
+    if (use_cache)
+        for (auto &e : s->pcache)
+            if (e.key == key) { ent = &e; break; }
+    if (!ent) {
+        // plan in "virtual physical" bits = the state's current actual bits
+        Frame fr;
+        for (int q = 0; q < 64; ++q) fr.perm[q] = s->perm[q];
+        fr.xmask = s->xmask;
+        std::vector<PGate> pg = to_physical(s->n, gates, ng, fr, flags);
+        PlanOptions po = resolve_options(opt, (int)s->esz(), s->n_local);
+        int sigma[64];
+        for (int v = 0; v < 64; ++v) sigma[v] = v;
+        sv_state::PlanEntry ne;
+        try {
+            ne.plan = build_plan(s->n, s->n_global, (int)s->esz(), pg, po, sigma);
+        } catch (const std::exception &ex) {
+            return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
+        }
+        // one encoding per shard this process holds (rank bits, selectors on global bits)
+        const int nsh_ = s->nshards();
+        ne.poff.resize(nsh_);
+        for (int r = 0; r < nsh_; ++r) {
+            const uint64_t rb = s->shard_rank(r) << s->n_local;
+            Encoded enc = encode(ne.plan, s->n_local, s->c128(), rb);
+            while (ne.blob.size() & 255) ne.blob.push_back(0);
+            const uint32_t at = (uint32_t)ne.blob.size();
+            for (uint32_t off : enc.pass_off) {
+                StvPass *hp = (StvPass *)&enc.blob[off];
+                hp->rank_bits = rb;
+                ne.poff[r].push_back(at + off);
+            }
+            ne.blob.insert(ne.blob.end(), enc.blob.begin(), enc.blob.end());
+        }
+        // frame after the plan: logical -> actual
+        ne.xmask_out = 0;
+        for (int v = 0; v < s->n; ++v)
+            if ((fr.xmask >> v) & 1) ne.xmask_out |= 1ull << sigma[v];
+        for (int q = 0; q < 64; ++q) ne.perm_out[q] = q < s->n ? sigma[fr.perm[q]] : q;
+        ne.key = std::move(key);
+        ne.id = s->pcache_next++;
+        if (s->pcache.size() >= 4) {   // evict the oldest
+            size_t old = 0;
+            for (size_t i = 1; i < s->pcache.size(); ++i)
+                if (s->pcache[i].id < s->pcache[old].id) old = i;
+            if (s->dblob_id == s->pcache[old].id) s->dblob_id = 0;
+            s->pcache.erase(s->pcache.begin() + (long)old);
+        }
+        s->pcache.push_back(std::move(ne));
+        ent = &s->pcache.back();
+        if (!use_cache) ent->id = 0;   // never reused
+    }
+    const Plan &plan = ent->plan;
+    const std::vector<uint8_t> &blob = ent->blob;
+    const std::vector<std::vector<uint32_t>> &poff = ent->poff;
+    const int nsh = s->nshards();
     auto t1 = std::chrono::steady_clock::now();
     std::memset(&s->stats, 0, sizeof(s->stats));
     s->stats.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
     s->stats.alg_bytes = plan.alg_bytes * nsh;
     s->stats.alg_flops = plan.alg_flops * nsh;
-    s->stats.h2d_bytes = (double)blob.size();
-    if ((st = ensure(s, (void **)&s->hblob, &s->hblob_cap, blob.size(), true))) return st;
-    if ((st = ensure(s, (void **)&s->dblob, &s->dblob_cap, blob.size(), false))) return st;
-    std::memcpy(s->hblob, blob.data(), blob.size());
     CK(s, cudaEventRecord(s->ev0, s->stream));
-    CK(s, cudaMemcpyAsync(s->dblob, s->hblob, blob.size(), cudaMemcpyHostToDevice, s->stream));
+    if (ent->id == 0 || s->dblob_id != ent->id) {   // upload the blob unless it is already resident
+        if ((st = ensure(s, (void **)&s->hblob, &s->hblob_cap, blob.size(), true))) return st;
+        if (s->dblob_cap < blob.size()) s->dblob_id = 0;
+        if ((st = ensure(s, (void **)&s->dblob, &s->dblob_cap, blob.size(), false))) return st;
+        CK(s, cudaStreamSynchronize(s->stream));   // the pinned staging may still feed an earlier copy
+        std::memcpy(s->hblob, blob.data(), blob.size());
+        CK(s, cudaMemcpyAsync(s->dblob, s->hblob, blob.size(), cudaMemcpyHostToDevice, s->stream));
+        s->stats.h2d_bytes = (double)blob.size();
+        s->dblob_id = ent->id;
+    }
     const bool prof = flags & SV_OPT_PROFILE;
     if (prof && s->pev.size() < plan.passes.size() + 1) {
         for (size_t i = s->pev.size(); i < plan.passes.size() + 1; ++i) {
@@ -465,11 +531,8 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
     }
     s->stats.n_kernels = kernels;
     // new frame: logical -> actual
-    uint64_t xm = 0;
-    for (int v = 0; v < s->n; ++v)
-        if ((fr.xmask >> v) & 1) xm |= 1ull << sigma[v];
-    for (int q = 0; q < s->n; ++q) s->perm[q] = sigma[fr.perm[q]];
-    s->xmask = xm;
+    for (int q = 0; q < s->n; ++q) s->perm[q] = ent->perm_out[q];
+    s->xmask = ent->xmask_out;
     return SV_OK;
 }
 

@@ -246,3 +246,32 @@ def test_c2_shape_reduced(stv, dtype):
     circ = C.grid_circuit("c2s", 4, 6, 0, 20, "fsim", 2)
     psi, _ = run_gpu(stv, circ, dtype)
     assert_parity(psi, oracle.run(circ, nthreads=16), dtype)
+
+
+def test_plan_cache_hit_identical_and_frame_keyed(stv):
+    """An identical call (same gates, frame, options) reuses the plan and its resident device
+    blob (no planning, no upload) and gives bit-identical results; a different frame (after a
+    relabel-only X) is a different key and still matches the oracle."""
+    circ = C.config(1)
+    st = stv.State(circ.n)
+    st.set_basis(circ.x0)
+    st.apply(circ.gates)
+    a = st.amplitudes()
+    cold = st.stats()
+    st.set_basis(circ.x0)
+    st.apply(circ.gates)
+    b = st.amplitudes()
+    warm = st.stats()
+    assert np.array_equal(a, b)
+    assert warm["h2d_bytes"] == 0 and cold["h2d_bytes"] > 0
+    st.set_basis(circ.x0)
+    st.apply([("x", (3,), ())] + list(circ.gates[:50]))      # X relabels the frame first
+    st.apply(circ.gates[50:])
+    c = st.amplitudes()
+    st.set_basis(circ.x0)
+    st.apply(circ.gates, flags=stv.OPT_NO_PLAN_CACHE)
+    d = st.amplitudes()
+    st.close()
+    ref = oracle.run(C.Circuit("x+c1", circ.n, [("x", (3,), ())] + list(circ.gates), x0=circ.x0))
+    assert_parity(c, ref, "c64")
+    assert np.array_equal(a, d)

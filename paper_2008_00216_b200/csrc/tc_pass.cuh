@@ -122,9 +122,11 @@ __device__ __forceinline__ void tc_build_op(const StvSub *__restrict__ subs, int
             for (int q = 0; q < 4; ++q) {
                 const int ro = q >> 1, ri = q & 1;
                 const uint32_t off = tc_bt_off(2 * l + ro, 2 * j + ri);
+                // both parts rounded to nearest tf32 (the tensor core truncates: an unrounded
+                // lo part would bias every operator towards a norm < 1)
                 const uint32_t hi = tf32_rna(v[q]);
                 *(uint32_t *)(slot + off) = hi;
-                *(float *)(slot + 4096 + off) = v[q] - __uint_as_float(hi);
+                *(uint32_t *)(slot + 4096 + off) = tf32_rna(v[q] - __uint_as_float(hi));
             }
         }
     }
@@ -240,7 +242,10 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
             run_subs<float2, 1>(x, braw1, subs + st.first, st.n, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
         } else {
             {   // A_hi = x itself (the tensor core reads the top 19 bits: tf32 truncation of x),
-                // A_lo = x - trunc_tf32(x) (exact in fp32) -> TMEM row of this thread, block warp / 4
+                // A_lo = x - trunc_tf32(x) (exact in fp32), pre-rounded by half a tf32 ulp so the
+                // tensor core's truncation of A_lo rounds to nearest -- truncating both parts
+                // would shrink every amplitude (a norm decay of ~1e-6 per operator step)
+                // -> TMEM row of this thread, block warp / 4
                 uint32_t v[32];
 #pragma unroll
                 for (int l = 0; l < 16; ++l) {
@@ -253,8 +258,8 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
                     const float2 t = make_float2(__uint_as_float(v[2 * l] & 0xffffe000u),
                                                  __uint_as_float(v[2 * l + 1] & 0xffffe000u));
                     const float2 lo = __fadd2_rn(x[0][l], make_float2(-t.x, -t.y));
-                    v[2 * l] = __float_as_uint(lo.x);
-                    v[2 * l + 1] = __float_as_uint(lo.y);
+                    v[2 * l] = __float_as_uint(lo.x) + 0x1000u;
+                    v[2 * l + 1] = __float_as_uint(lo.y) + 0x1000u;
                 }
                 tmem_st32(trow + 32, v);
             }

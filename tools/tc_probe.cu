@@ -172,7 +172,130 @@ __global__ void __launch_bounds__(256, 1) k_probe(const float *A, const float *B
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
 }
 
-int main() {
+
+// drift probe: rows of A are complex 16-vectors (32 reals); B = real embedding of a unitary U
+// (given as Bt[n][k]); the row is mapped through U `reps` times with the 3xTF32 step
+// (A_hi = x, A_lo = x - trunc(x) [+ rounding variant], D = hi.Bh + hi.Bl + lo.Bh) and the
+// norms before / after are written out.  lo_mode: 0 truncated lo, 1 lo + 0x1000, 2 cvt.rna(lo).
+// b_lo_rna: B_lo rounded to nearest tf32 (else exact fp32 remainder, truncated by the MMA).
+__global__ void __launch_bounds__(256, 1) k_drift(const float *A, const float *Bt, float *norms, int reps, int lo_mode,
+                                                  int b_lo_rna) {
+    __shared__ __align__(1024) uint8_t bsm[2 * 4096];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(256) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    for (int e = tid; e < 1024; e += 256) {
+        const int n = e >> 5, k = e & 31;
+        const float b = Bt[e];
+        const uint32_t hi = tf32_rna(b);
+        const float lo = b - __uint_as_float(hi);
+        *(uint32_t *)(bsm + bt_off(n, k)) = hi;
+        *(uint32_t *)(bsm + 4096 + bt_off(n, k)) = b_lo_rna ? tf32_rna(lo) : __float_as_uint(lo);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tbase;
+    const int blk = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t colA = blk * 96, colAl = colA + 32, colD = colA + 64;
+    float x[32];
+    double n0 = 0;
+    for (int k = 0; k < 32; ++k) { x[k] = A[tid * 32 + k]; n0 += (double)x[k] * x[k]; }
+    uint32_t phase = 0;
+    for (int r = 0; r < reps; ++r) {
+        uint32_t h[32], l[32];
+        for (int k = 0; k < 32; ++k) {
+            h[k] = __float_as_uint(x[k]);
+            const float lo = x[k] - __uint_as_float(h[k] & 0xffffe000u);
+            l[k] = lo_mode == 0 ? __float_as_uint(lo) : lo_mode == 1 ? __float_as_uint(lo) + 0x1000u : tf32_rna(lo);
+        }
+        tmem_st32(tmem + lane_base + colA, h);
+        tmem_st32(tmem + lane_base + colAl, l);
+        tc_wait_st();
+        tc_fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc_fence_after();
+            const uint32_t bh = smem_u32(bsm), bl = smem_u32(bsm + 4096);
+            for (int b = 0; b < 2; ++b) {
+                const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
+                for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, kk > 0);
+                for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bl + 256 * kk, 128, 1024), kIdesc, 1);
+                for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, al + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, 1);
+            }
+            mma_commit(&bar);
+        }
+        __syncwarp();
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        uint32_t dv[32];
+        tmem_ld32(tmem + lane_base + colD, dv);
+        tc_wait_ld();
+        for (int k = 0; k < 32; ++k) x[k] = __uint_as_float(dv[k]);
+        tc_fence_before();
+        __syncthreads();
+    }
+    double n1 = 0;
+    for (int k = 0; k < 32; ++k) n1 += (double)x[k] * x[k];
+    norms[2 * tid] = (float)n0;
+    norms[2 * tid + 1] = (float)(n1 / n0 - 1.0);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
+}
+
+static void drift_test(int reps) {
+    // random 16x16 unitary by Gram-Schmidt, its 32x32 real embedding as Bt[n][k]
+    srand(7);
+    double ur[16][16], ui[16][16];
+    auto g = []() { double s = 0; for (int i = 0; i < 12; ++i) s += (double)rand() / RAND_MAX; return s - 6; };
+    for (int c = 0; c < 16; ++c) {
+        for (int r = 0; r < 16; ++r) { ur[r][c] = g(); ui[r][c] = g(); }
+        for (int p = 0; p < c; ++p) {   // remove projection on column p
+            double dr = 0, di = 0;
+            for (int r = 0; r < 16; ++r) { dr += ur[r][p] * ur[r][c] + ui[r][p] * ui[r][c]; di += ur[r][p] * ui[r][c] - ui[r][p] * ur[r][c]; }
+            for (int r = 0; r < 16; ++r) { ur[r][c] -= dr * ur[r][p] - di * ui[r][p]; ui[r][c] -= dr * ui[r][p] + di * ur[r][p]; }
+        }
+        double nn = 0;
+        for (int r = 0; r < 16; ++r) nn += ur[r][c] * ur[r][c] + ui[r][c] * ui[r][c];
+        nn = sqrt(nn);
+        for (int r = 0; r < 16; ++r) { ur[r][c] /= nn; ui[r][c] /= nn; }
+    }
+    std::vector<float> Bt(1024), A(256 * 32), out(512);
+    for (int lp = 0; lp < 16; ++lp)
+        for (int l = 0; l < 16; ++l) {   // out[l'] = sum_l U[l'][l] in[l]: Bt[2l'+ro][2l+ri]
+            Bt[(2 * lp) * 32 + 2 * l] = (float)ur[lp][l];
+            Bt[(2 * lp) * 32 + 2 * l + 1] = (float)-ui[lp][l];
+            Bt[(2 * lp + 1) * 32 + 2 * l] = (float)ui[lp][l];
+            Bt[(2 * lp + 1) * 32 + 2 * l + 1] = (float)ur[lp][l];
+        }
+    for (auto &v : A) v = (float)(g() * 1e-3);
+    float *dA, *dB, *dN;
+    CK(cudaMalloc(&dA, A.size() * 4)); CK(cudaMalloc(&dB, Bt.size() * 4)); CK(cudaMalloc(&dN, 512 * 4));
+    CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, Bt.data(), Bt.size() * 4, cudaMemcpyHostToDevice));
+    for (int bl = 0; bl < 2; ++bl)
+        for (int lm = 0; lm < 3; ++lm) {
+            k_drift<<<1, 256>>>(dA, dB, dN, reps, lm, bl);
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpy(out.data(), dN, 512 * 4, cudaMemcpyDeviceToHost));
+            double m = 0;
+            for (int t = 0; t < 256; ++t) m += out[2 * t + 1];
+            printf("drift reps=%d b_lo_rna=%d lo_mode=%d: mean relative norm change %.3e (per step %.3e)\n", reps, bl, lm,
+                   m / 256, m / 256 / reps);
+        }
+}
+
+int main(int argc, char **argv) {
+    if (argc > 1) { drift_test(atoi(argv[1])); return 0; }
     const int R = 256, K = 32, N = 32;
     std::vector<float> A(R * K), Bt(N * K), D(R * N);
     srand(1);

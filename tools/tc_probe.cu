@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(256, 1) k_drift(const float *A, const float *B
         const uint32_t hi = tf32_rna(b);
         const float lo = b - __uint_as_float(hi);
         *(uint32_t *)(bsm + bt_off(n, k)) = hi;
-        *(uint32_t *)(bsm + 4096 + bt_off(n, k)) = b_lo_rna ? tf32_rna(lo) : __float_as_uint(lo);
+        *(uint32_t *)(bsm + 4096 + bt_off(n, k)) = b_lo_rna ? tf32_rna(lo) : __float_as_uint(lo);   // 2: also reordered
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
@@ -226,9 +226,15 @@ __global__ void __launch_bounds__(256, 1) k_drift(const float *A, const float *B
             const uint32_t bh = smem_u32(bsm), bl = smem_u32(bsm + 4096);
             for (int b = 0; b < 2; ++b) {
                 const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
-                for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, kk > 0);
-                for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bl + 256 * kk, 128, 1024), kIdesc, 1);
-                for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, al + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, 1);
+                if (b_lo_rna >= 2) {   // small cross terms first, hi.hi last
+                    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, al + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, kk > 0);
+                    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bl + 256 * kk, 128, 1024), kIdesc, 1);
+                    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, 1);
+                } else {
+                    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, kk > 0);
+                    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, ah + 8 * kk, smem_desc(bl + 256 * kk, 128, 1024), kIdesc, 1);
+                    for (int kk = 0; kk < 4; ++kk) mma_tf32_ts(d, al + 8 * kk, smem_desc(bh + 256 * kk, 128, 1024), kIdesc, 1);
+                }
             }
             mma_commit(&bar);
         }
@@ -282,7 +288,7 @@ static void drift_test(int reps) {
     CK(cudaMalloc(&dA, A.size() * 4)); CK(cudaMalloc(&dB, Bt.size() * 4)); CK(cudaMalloc(&dN, 512 * 4));
     CK(cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, Bt.data(), Bt.size() * 4, cudaMemcpyHostToDevice));
-    for (int bl = 0; bl < 2; ++bl)
+    for (int bl = 0; bl < 3; ++bl)
         for (int lm = 0; lm < 3; ++lm) {
             k_drift<<<1, 256>>>(dA, dB, dN, reps, lm, bl);
             CK(cudaDeviceSynchronize());

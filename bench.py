@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--low-bits", type=int, default=0)
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--virtual-g", type=int, default=0,
+                    help="N=1 only: emulate 2^g ranks on the one GPU (virtual shards: every pass per shard, "
+                         "remaps through the pack -> exchange -> unpack path)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-gates", type=int, default=24, help="cpu_baseline sample size (gates)")
     ap.add_argument("--sweep", default="", help="comma list of budgets to sweep (extra output lines to stderr)")
@@ -295,7 +298,7 @@ def main():
         dist = {"rank": rank, "world": world, "uid": uid[0]}
     stv.lib()
     n = circ.n
-    st = stv.State(n, args.dtype, dist=dist)
+    st = stv.State(n, args.dtype, dist=dist, virtual_g=args.virtual_g if world == 1 else 0)
     arr, keep = stv.marshal(circ.gates)
     opts = stv.options(kmax=args.kmax, tile_bits=args.tile_bits, low_bits=args.low_bits, budget=args.budget,
                        flags=args.flags, profile=True)
@@ -431,7 +434,8 @@ def main():
         "config": {"workload": circ.name, "n": n, "gates": G, "state": args.dtype,
                    "state_bytes_per_gpu": esz << n_local, "l2": "state >> 126 MB L2 (no flush needed)",
                    "kmax": args.kmax or 4, "budget": args.budget or 1000, "tile_bits": args.tile_bits or None,
-                   "flags": args.flags, "gate_kernel": "tcgen05 tensor-core" if used_tc else "CUDA-core FMA"},
+                   "flags": args.flags, "gate_kernel": "tcgen05 tensor-core" if used_tc else "CUDA-core FMA",
+                   "virtual_shards": (1 << args.virtual_g) if args.virtual_g else None},
         "sec_per_circuit": sec,
         "pct_of_hbm_peak": 100.0 * value / world / hbm,
         "gate_equiv_gbs": gate_equiv,

@@ -94,6 +94,8 @@ typedef struct {
 /* 0x40u reserved (was an experimental warp-per-tile kernel; ignored)                                     */
 #define SV_OPT_NO_VARIANTS  0x80u /* do not merge 2-qubit sub-op chains into per-tile variant matrices      */
 #define SV_OPT_NO_TC        0x100u /* complex64 gate groups on the CUDA-core FMA path only (no tcgen05 pass) */
+#define SV_OPT_NO_SINK      0x400u /* keep diagonal terms over in-tile non-register bits in place (no sinking
+                                        to the end of a gate group's program; tensor-core planning) */
 #define SV_OPT_NO_PLAN_CACHE 0x200u /* plan from scratch: do not reuse the plan of an identical earlier call
                                         (same gates, frame and options; the last 4 are kept per state) */
 typedef struct {

@@ -130,8 +130,10 @@ struct sv_state {
     uint64_t dblob_id = 0;            // cache entry whose blob is resident in dblob (0: none)
     // distributed
     ncclComm_t comm = nullptr;
-    void *xbuf = nullptr;         // remap send/recv staging
+    void *xbuf = nullptr;         // remap send/recv staging (2 sets: pieces pipelined)
     size_t xbuf_bytes = 0;
+    cudaStream_t xstream = nullptr;   // remap exchange stream (overlaps pack / unpack of other pieces)
+    cudaEvent_t xev[4] = {nullptr, nullptr, nullptr, nullptr};   // packed[2], exchanged[2]
 
     bool c128() const { return dt == SV_C128; }
     size_t esz() const { return dt == SV_C128 ? 16 : 8; }
@@ -809,6 +811,9 @@ sv_status sv_destroy(sv_state *s) {
     if (s->dstage) cudaFree(s->dstage);
     if (s->didx) cudaFree(s->didx);
     if (s->xbuf) cudaFree(s->xbuf);
+    for (auto e : s->xev)
+        if (e) cudaEventDestroy(e);
+    if (s->xstream) cudaStreamDestroy(s->xstream);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     for (auto e : s->pev) cudaEventDestroy(e);
@@ -857,56 +862,97 @@ sv_status dist_remap(sv_state *s, const std::vector<std::pair<int, int>> &swaps,
     auto slot = [](int c, int own) { return c < own ? c : c - 1; };
     const uint64_t chunk_amps = 1ull << (s->n_local - m);
     const int npeers = (1 << m) - 1;
-    const uint64_t cap = s->virt ? (1ull << 30) : (512ull << 20);   // staging bytes
-    const uint64_t piece = std::max<uint64_t>(1, std::min<uint64_t>(chunk_amps, cap / (2ull * nsh * npeers * s->esz())));
+    // staging: 2 sets (pieces pipelined) of send + recv slots per shard
+    uint64_t cap = s->virt ? (2ull << 30) : (1ull << 30);
+    {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr / 4 > cap) cap = std::min<uint64_t>(fr / 4, 8ull << 30);
+    }
+    const uint64_t piece =
+        std::max<uint64_t>(1, std::min<uint64_t>(chunk_amps, cap / (4ull * nsh * npeers * s->esz())));
     const size_t slot_bytes = (size_t)piece * s->esz();
-    const size_t need = 2ull * nsh * npeers * slot_bytes;
-    sv_status st = ensure(s, &s->xbuf, &s->xbuf_bytes, need, false);
+    const size_t set_bytes = 2ull * nsh * npeers * slot_bytes;
+    sv_status st = ensure(s, &s->xbuf, &s->xbuf_bytes, 2 * set_bytes, false);
     if (st) return st;
-    auto sendb = [&](int r, int sl) { return (uint8_t *)s->xbuf + ((size_t)r * npeers + sl) * slot_bytes; };
-    auto recvb = [&](int r, int sl) {
-        return (uint8_t *)s->xbuf + ((size_t)(nsh + r) * npeers + sl) * slot_bytes;
+    auto sendb = [&](int set, int r, int sl) {
+        return (uint8_t *)s->xbuf + set * set_bytes + ((size_t)r * npeers + sl) * slot_bytes;
     };
-    for (uint64_t off = 0; off < chunk_amps; off += piece) {
-        const uint64_t cnt = std::min(piece, chunk_amps - off);
-        const size_t b = cnt * s->esz();
+    auto recvb = [&](int set, int r, int sl) {
+        return (uint8_t *)s->xbuf + set * set_bytes + ((size_t)(nsh + r) * npeers + sl) * slot_bytes;
+    };
+    // pipeline (STV_REMAP_PIPE=0: serial): the main stream packs piece i into set i%2, the
+    // exchange stream moves it once packed, the main stream unpacks piece i-1 while piece i
+    // is in flight; a set is reused two pieces later, after its unpack
+    static const bool pipe = !getenv("STV_REMAP_PIPE") || atoi(getenv("STV_REMAP_PIPE")) != 0;
+    if (pipe && !s->xstream) {
+        CK(s, cudaStreamCreateWithFlags(&s->xstream, cudaStreamNonBlocking));
+        for (auto &e : s->xev) CK(s, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    cudaStream_t xs = pipe ? s->xstream : s->stream;
+    const uint64_t npieces = (chunk_amps + piece - 1) / piece;
+    auto pack = [&](uint64_t i) -> sv_status {
+        const uint64_t off = i * piece, cnt = std::min(piece, chunk_amps - off);
+        const int set = (int)(i & 1);
         for (int r = 0; r < nsh; ++r)
             for (int c = 0; c < (1 << m); ++c) {
                 if (c == mine[r]) continue;
-                cudaError_t e = launch_pack(s->c128(), s->shard(r), sendb(r, slot(c, mine[r])), lbits, m, c, off, cnt,
-                                            s->n_local, false, s->stream, kernels);
+                cudaError_t e = launch_pack(s->c128(), s->shard(r), sendb(set, r, slot(c, mine[r])), lbits, m, c, off,
+                                            cnt, s->n_local, false, s->stream, kernels);
                 if (e != cudaSuccess) return cuda_fail(s, e, "remap pack");
             }
+        if (pipe) CK(s, cudaEventRecord(s->xev[set], s->stream));
+        return SV_OK;
+    };
+    auto exchange = [&](uint64_t i) -> sv_status {
+        const uint64_t off = i * piece, cnt = std::min(piece, chunk_amps - off);
+        const int set = (int)(i & 1);
+        const size_t b = cnt * s->esz();
+        if (pipe) CK(s, cudaStreamWaitEvent(xs, s->xev[set], 0));
         if (s->virt) {
             // rank p sends its chunk mine[r] to r, which receives it in its slot for chunk c (p = peer[r][c])
             for (int r = 0; r < nsh; ++r)
                 for (int c = 0; c < (1 << m); ++c) {
                     if (c == mine[r]) continue;
                     const int p = peer[r][c];
-                    CK(s, cudaMemcpyAsync(recvb(r, slot(c, mine[r])), sendb(p, slot(mine[r], mine[p])), b,
-                                          cudaMemcpyDeviceToDevice, s->stream));
+                    CK(s, cudaMemcpyAsync(recvb(set, r, slot(c, mine[r])), sendb(set, p, slot(mine[r], mine[p])), b,
+                                          cudaMemcpyDeviceToDevice, xs));
                 }
         } else {
             g_nccl.groupStart();
             for (int c = 0; c < (1 << m); ++c) {
                 if (c == mine[0]) continue;
                 const int sl = slot(c, mine[0]);
-                int r1 = g_nccl.send(sendb(0, sl), b, ncclUint8, peer[0][c], s->comm, s->stream);
-                int r2 = g_nccl.recv(recvb(0, sl), b, ncclUint8, peer[0][c], s->comm, s->stream);
+                int r1 = g_nccl.send(sendb(set, 0, sl), b, ncclUint8, peer[0][c], s->comm, xs);
+                int r2 = g_nccl.recv(recvb(set, 0, sl), b, ncclUint8, peer[0][c], s->comm, xs);
                 if (r1 || r2) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclSend/Recv (remap)"); }
             }
             if (g_nccl.groupEnd()) { s->poisoned = true; return fail(SV_ERR_NCCL, "ncclGroupEnd (remap)"); }
         }
+        if (pipe) CK(s, cudaEventRecord(s->xev[2 + set], xs));
+        s->stats.remap_bytes += (double)npeers * b;   // per rank
+        return SV_OK;
+    };
+    auto unpack = [&](uint64_t i) -> sv_status {
+        const uint64_t off = i * piece, cnt = std::min(piece, chunk_amps - off);
+        const int set = (int)(i & 1);
+        if (pipe) CK(s, cudaStreamWaitEvent(s->stream, s->xev[2 + set], 0));
         for (int r = 0; r < nsh; ++r)
             for (int c = 0; c < (1 << m); ++c) {
                 if (c == mine[r]) continue;
                 // data from peer[r][c] (its chunk mine[r]) lands in r's chunk c
-                cudaError_t e = launch_pack(s->c128(), s->shard(r), recvb(r, slot(c, mine[r])), lbits, m, c, off, cnt,
-                                            s->n_local, true, s->stream, kernels);
+                cudaError_t e = launch_pack(s->c128(), s->shard(r), recvb(set, r, slot(c, mine[r])), lbits, m, c, off,
+                                            cnt, s->n_local, true, s->stream, kernels);
                 if (e != cudaSuccess) return cuda_fail(s, e, "remap unpack");
             }
-        s->stats.remap_bytes += (double)npeers * b;   // per rank
+        return SV_OK;
+    };
+    for (uint64_t i = 0; i < npieces; ++i) {
+        if ((st = pack(i))) return st;          // set i%2 is free: piece i-2 was unpacked before
+        if ((st = exchange(i))) return st;
+        if (pipe && i > 0 && (st = unpack(i - 1))) return st;
+        if (!pipe && (st = unpack(i))) return st;
     }
+    if (pipe && npieces > 0 && (st = unpack(npieces - 1))) return st;
     return SV_OK;
 }
 }  // namespace

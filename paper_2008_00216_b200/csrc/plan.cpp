@@ -1086,6 +1086,61 @@ double pass_flops_per_amp(const std::vector<FOp> &ops) {
     return f;
 }
 
+// Tensor-core programs (complex64, tiles of <= 12 bits): the part of a group's
+// diagonal sub-op that differs between the vectors of a tile (terms on a V-bit:
+// an in-tile bit outside the group's registers) is sunk to the END of the group's
+// program when no later sub-op acts non-diagonally on its register bits (diagonal
+// terms commute with every op that acts on their bits only diagonally; V-bits and
+// outside bits are never targets inside a group).  What stays is the same for every
+// vector, so runs of matrices separated only by such diagonals merge into one
+// operator step, and the sunk terms become one trailing register (E) step.
+// Returns false (and leaves the group unchanged) when nothing moves.
+static bool sink_v_terms(FOp &grp, uint64_t S) {
+    const uint64_t T = grp.T, V = S & ~T;
+    std::vector<FOp> subs = grp.subs;
+    QForm sunk;
+    bool moved = false;
+    uint64_t blocked = 0;   // register bits acted on non-diagonally after position k
+    for (size_t k = subs.size(); k-- > 0;) {
+        FOp &o = subs[k];
+        if (o.type == OP_DIAG) {
+            QForm vpart, rest;
+            rest.cst = o.form.cst;
+            for (auto &kv : o.form.lin) ((V >> kv.first) & 1 ? vpart.lin : rest.lin)[kv.first] = kv.second;
+            for (auto &kv : o.form.quad) {
+                const bool hv = ((V >> kv.first.first) & 1) || ((V >> kv.first.second) & 1);
+                (hv ? vpart.quad : rest.quad)[kv.first] = kv.second;
+            }
+            if (!vpart.trivial() && !(vpart.qubits() & T & blocked) && !(k + 1 == subs.size() && !moved)) {
+                sunk.add(vpart);
+                o.form = rest;
+                o.qmask = rest.qubits();
+                moved = true;
+            }
+        } else if (o.type == OP_DENSE) {
+            for (int b : o.tg) blocked |= 1ull << b;
+        } else if (o.type == OP_CNOT) {
+            blocked |= 1ull << o.t;
+        }
+    }
+    if (!moved) return false;
+    std::vector<FOp> out;
+    for (FOp &o : subs)
+        if (!(o.type == OP_DIAG && o.form.trivial())) out.push_back(std::move(o));
+    if (!out.empty() && out.back().type == OP_DIAG) {   // merge with a trailing diagonal
+        out.back().form.add(sunk);
+        out.back().qmask = out.back().form.qubits();
+    } else {
+        FOp d;
+        d.type = OP_DIAG;
+        d.form = sunk;
+        d.qmask = sunk.qubits();
+        out.push_back(std::move(d));
+    }
+    grp.subs = std::move(out);
+    return true;
+}
+
 Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg_virtual,
                 const PlanOptions &opt, int *sigma) {
     Plan plan;
@@ -1249,6 +1304,21 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                         absorb_diagonals(o, S, nl);
                         merge_variant_chains(o, S, nl);
                     }
+            // tensor-core programs: V-bit diagonal terms sunk to the end of each group (kept
+            // only if the pass's tables still fit)
+            if (amp_bytes == 8 && !(opt.flags & (SV_OPT_NO_TC | SV_OPT_NO_SINK)) && __builtin_popcountll(S) <= 12) {
+                std::vector<FOp> trial = pass.ops;
+                bool any = false;
+                for (FOp &o : trial)
+                    if (o.type == OP_GROUP) any |= sink_v_terms(o, S);
+                if (any) {
+                    OpsEval ev;
+                    ev.ops = trial;
+                    ev.grouped = true;
+                    tally(ev, amp_bytes, S);
+                    if (ev.rec <= rec_limit && ev.tab <= tab_limit && ev.ntab <= STV_MAX_TABLES) pass.ops = trial;
+                }
+            }
             plan.alg_bytes += amp_pass_bytes;
             plan.alg_flops += pass_flops_per_amp(pass.ops) * std::ldexp(1.0, nl);
         }

@@ -346,3 +346,58 @@ def test_flip_targets_are_register_bits(seed, tile_bits):
             seen += len(fl)
             assert all((f & 0xFFFF) in regs for f in fl), (po, i)
     assert seen > 0
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "c4", "rand"])
+def test_tc_step_plan_structure(case):
+    """Tensor-core step plans (pass_format.h StvTcStep): per group the steps cover its sub-op
+    program in order without gaps; M steps hold only sub-ops that act the same on every
+    vector of a tile (no V-bit tables, no V-bit-controlled CNOTs) and own distinct operator
+    slots; the dependency masks contain every per-tile selector bit; tperm permutes the tile
+    ordinal bits with the dependency bits on top."""
+    circ = C.random_circuit(20, 400, 11) if case == "rand" else C.config(int(case[1:]))
+    blob, offs = stv.plan_blob(circ.n, circ.gates)
+    npass = 0
+    for po in offs:
+        P = BE._at(blob, BE.Pass, po)
+        if P.kind != 1 or not P.grouped or P.ntc == 0:
+            continue
+        npass += 1
+        steps = [BE._at(blob, BE.TcStep, po + P.tc_off + 32 * i) for i in range(P.ntc)]
+        groups = [BE._at(blob, BE.Group, po + P.ops_off + 256 * i) for i in range(P.nops)]
+        out_bits = [b for b in range(64) if (P.out_mask >> b) & 1]
+        ops = set()
+        gi, pos = 0, 0
+        for s in steps:
+            assert s.group == gi and s.first == pos
+            g = groups[gi]
+            subs = [BE._at(blob, BE.Sub, po + g.sub_off + 16 * (s.first + k)) for k in range(s.n)]
+            if s.kind == 1:
+                assert s.op not in ops and s.op < P.ntcop
+                ops.add(s.op)
+                for sb in subs:
+                    c = sb.code & 0xFF
+                    if 10 <= c < 30:
+                        assert sb.ctl & 0xFFFF == 0                    # no V-bit control
+                    if c == 30 or 37 <= c < 41:
+                        assert BE._at(blob, BE.DTab, po + P.tab_off + 48 * sb.arg).m == 0
+                    if 31 <= c < 37:
+                        for i in range(3):
+                            sel = (sb.code >> (8 + 5 * i)) & 31
+                            if sel != 31:
+                                assert (s.dep >> out_bits[sel]) & 1
+            pos += s.n
+            if s.last:
+                assert pos == g.nsub
+                gi, pos = gi + 1, 0
+        assert gi == P.nops and len(ops) == P.ntcop
+        nord = len(out_bits)
+        perm = list(P.tperm)[:nord]
+        assert sorted(perm) == list(range(nord))
+        dep = 0
+        for s in steps:
+            if s.kind == 1:
+                dep |= s.dep
+        dep_ord = [i for i, b in enumerate(out_bits) if (dep >> b) & 1]
+        assert sorted(perm[nord - len(dep_ord):]) == dep_ord
+    assert npass > 0

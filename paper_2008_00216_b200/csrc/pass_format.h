@@ -102,6 +102,9 @@ struct alignas(16) StvTcStep {
     int16_t kind, last, first, n;
     int32_t op, group;
     uint64_t dep;
+    int32_t bvar;              // M: 1 = per-block operator variants (slot op: block 0, op + 1: block 1;
+                               // the block is vector bit 7, the step's sub-ops depend on it)
+    int32_t pad;
 };
 
 // ---------------------------------------------------------------------------

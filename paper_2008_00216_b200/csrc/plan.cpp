@@ -1403,22 +1403,27 @@ static uint32_t bank_vec(int p, bool c128) {
 // Order of a group's vector bits: lane bits 0..2 (LDS.128 phases of 8 lanes)
 // get positions with linearly independent bank vectors; a complex64 group
 // without position 0 uses 8-B accesses (16-lane phases), so position 0 leads.
-static std::vector<int> vector_bit_order(const std::vector<int> &pos, int S, bool c128) {
+static std::vector<int> vector_bit_order(const std::vector<int> &pos, int S, bool c128, int avoid = -1) {
     std::vector<int> R, head, order;
     for (int q = 0; q < S; ++q)
         if (std::find(pos.begin(), pos.end(), q) == pos.end()) R.push_back(q);
-    if (!c128 && pos[0] != 0) head.push_back(0);
+    if (!c128 && pos[0] != 0 && avoid != 0) head.push_back(0);
     std::vector<uint32_t> basis;
     auto reduce = [&](uint32_t v) {
         for (uint32_t b : basis) v = std::min(v, v ^ b);
         return v;
     };
-    for (int q : R) {
-        if (basis.size() >= 3) break;
-        if (!c128 && q == 0) continue;
-        const uint32_t v = reduce(bank_vec(q, c128));
-        if (v) { basis.push_back(v); head.push_back(q); }
-    }
+    // lane bits: 3 positions with independent bank vectors (`avoid`, a position wanted as
+    // vector bit 7, is used only if no other position completes the basis)
+    for (int pass = 0; pass < 2; ++pass)
+        for (int q : R) {
+            if (basis.size() >= 3) break;
+            if (!c128 && q == 0) continue;
+            if ((q == avoid) != (pass == 1)) continue;
+            const uint32_t v = reduce(bank_vec(q, c128));
+            if (v) { basis.push_back(v); head.push_back(q); }
+        }
+    if (!c128 && pos[0] != 0 && avoid == 0) head.insert(head.begin(), 0);   // amplitude bit 0 is unavoidable
     order = head;
     for (int q : R)
         if (std::find(head.begin(), head.end(), q) == head.end()) order.push_back(q);
@@ -1623,12 +1628,22 @@ static int nth_set_bit(uint64_t m, int i) {
 static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, const std::vector<StvGroup> &grecs,
                             const std::vector<StvDTab> &tabs) {
     static const double tc_min = getenv("STV_TC_MIN") ? atof(getenv("STV_TC_MIN")) : 200.0;
-    auto foldable = [&](const StvSub &x) {
+    uint32_t bvraw = 0;   // raw tile offset of the current group's vector bit 7 (its TMEM block), or 0
+    // 0: varies between the vectors of a block (E step); 1: uniform over the tile; 2: uniform
+    // within each block (a per-block operator variant: depends only on vector bit 7)
+    auto fold_kind = [&](const StvSub &x) -> int {
         const int c = x.code & 0xff;
-        if (c >= SUBC_CNOT && c < SUBC_DIAG) return (x.ctl & 0xffffu) == 0;   // no V-bit control
-        if (c == SUBC_DIAG || (c >= SUBC_DIAGH && c < SUBC_DIAGH + 4)) return tabs[x.arg].m == 0;
-        return true;
+        if (c >= SUBC_CNOT && c < SUBC_DIAG) {
+            const uint32_t raw = x.ctl & 0xffffu;
+            return raw == 0 ? 1 : (bvraw && raw == bvraw) ? 2 : 0;
+        }
+        if (c == SUBC_DIAG || (c >= SUBC_DIAGH && c < SUBC_DIAGH + 4)) {
+            const StvDTab &d = tabs[x.arg];
+            return d.m == 0 ? 1 : (bvraw && d.m == 1 && d.vraw[0] == bvraw) ? 2 : 0;
+        }
+        return 1;
     };
+    auto foldable = [&](const StvSub &x) { return fold_kind(x) != 0; };
     auto cost = [&](const StvSub &x) -> double {   // FFMA2-equivalents per 16-amplitude vector
         const int c = x.code & 0xff;
         if (c < SUBC_U2) return 32;
@@ -1676,15 +1691,18 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
         const StvGroup &G = grecs[gi];
         const StvSub *sp = (const StvSub *)&b[at + G.sub_off];
         const size_t g0 = st.size();
+        bvraw = (G.nvb >= 8 && hd.S == 12) ? G.vbit[7][0] : 0;
         int k = 0;
         while (k < G.nsub) {
             bool f = foldable(sp[k]);
             int e = k;
             double c = 0;
             uint64_t dep = 0;
+            bool bv = false;
             while (e < G.nsub && foldable(sp[e]) == f) {
                 c += cost(sp[e]);
                 dep |= depends(sp[e]);
+                bv |= fold_kind(sp[e]) == 2;
                 ++e;
             }
             if (f && c < tc_min) f = false;
@@ -1698,7 +1716,9 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
                 s.n = (int16_t)(e - k);
                 s.group = (int32_t)gi;
                 if (f) {
-                    s.op = nop++;
+                    s.op = nop;
+                    s.bvar = bv ? 1 : 0;
+                    nop += bv ? 2 : 1;   // block variants: slots op (block 0) and op + 1 (block 1)
                     s.dep = dep;
                     dep_all |= dep;
                 }
@@ -2028,7 +2048,27 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                 for (int j = 0; j < 4; ++j) g.tpos[j] = pos[j];
                 g.nvb = hd.S - STV_GROUP_BITS;
                 g.pair16 = (!c128 && pos[0] == 0) ? 1 : 0;
-                const std::vector<int> vp = vector_bit_order(pos, hd.S, c128);
+                std::vector<int> vp = vector_bit_order(pos, hd.S, c128);
+                if (!c128 && g.nvb >= 8 && hd.S == 12) {
+                    // tensor-core block variant (tc_pass.cuh): the in-tile bit outside the group
+                    // that its one-V-bit tables and V-bit-controlled CNOTs use most becomes vector
+                    // bit 7 (= the TMEM block of a vector), so those sub-ops are tile-uniform within
+                    // a block and fold into per-block operators; lane bits (order head) stay
+                    std::map<int, int> cnt;
+                    for (const StvSub &x : out) {
+                        const int c = x.code & 0xff;
+                        if ((c == SUBC_DIAG || (c >= SUBC_DIAGH && c < SUBC_DIAGH + 4)) && tabs[x.arg].m == 1)
+                            cnt[__builtin_ctz(tabs[x.arg].vraw[0])]++;
+                        if (c >= SUBC_CNOT && c < SUBC_DIAG && (x.ctl & 0xffffu) && !((x.ctl & 0xffffu) & ((x.ctl & 0xffffu) - 1)))
+                            cnt[__builtin_ctz(x.ctl & 0xffffu)]++;
+                    }
+                    int best = -1, bc = 0;
+                    for (auto &kv : cnt)
+                        if (kv.second > bc) { best = kv.first; bc = kv.second; }
+                    if (best >= 0) vp = vector_bit_order(pos, hd.S, c128, best);
+                    auto it = std::find(vp.begin(), vp.end(), best);
+                    if (best >= 0 && it != vp.end() && it - vp.begin() >= 4) std::swap(*it, vp[7]);
+                }
                 for (int v = 0; v < g.nvb; ++v) {
                     g.vbit[v][0] = 1u << vp[v];
                     g.vbit[v][1] = swz_amp(1u << vp[v], c128);

@@ -103,17 +103,20 @@ constexpr uint32_t kTcOpBytes = 8192;   // hi (4 KB) + lo (4 KB)
 constexpr uint32_t kTcCols = 256;       // TMEM columns per CTA: 2 blocks x (A_hi 32, A_lo 32, D 32), rounded up
 
 // Build the operator of M step st into its slot: lane j < 16 runs the step's sub-ops on e_j.
+// Block variants (bvraw != 0): lanes 16..31 build the operator of block 1 (vectors whose bit 7,
+// raw tile offset bvraw, is set) into the next slot.
 __device__ __forceinline__ void tc_build_op(const StvSub *__restrict__ subs, int n, const uint8_t *__restrict__ mat,
                                             const StvDTab *__restrict__ tabs, const float2 *__restrict__ tables,
                                             uint64_t full_base, uint32_t tord, uint64_t rank_bits,
-                                            const float2 *__restrict__ scal, uint8_t *slot, int lane) {
+                                            const float2 *__restrict__ scal, uint8_t *slot, uint32_t bvraw, int lane) {
     float2 x[1][16];
 #pragma unroll
     for (int l = 0; l < 16; ++l) x[0][l] = make_float2(l == (lane & 15) ? 1.f : 0.f, 0.f);
-    const uint32_t braw[1] = {0u};
+    const uint32_t braw[1] = {lane >= 16 ? bvraw : 0u};
     run_subs<float2, 1>(x, braw, subs, n, mat, tabs, tables, full_base, tord, rank_bits, scal);
-    if (lane < 16) {
-        const int j = lane;   // input amplitude index (column of U)
+    if (lane >= 16 && bvraw) slot += kTcOpBytes;
+    if (lane < 16 || bvraw) {
+        const int j = lane & 15;   // input amplitude index (column of U)
 #pragma unroll
         for (int l = 0; l < 16; ++l) {   // U[l][j] = x[l]
             const float ur = x[0][l].x, ui = x[0][l].y;
@@ -275,7 +278,8 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
             asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
             if ((ctid & 127) == 0) {
                 tc_fence_after();
-                tc_issue_block(sh->tmem, half, umma_desc(smem_u32(opsm + (size_t)st.op * kTcOpBytes), 128, 1024));
+                tc_issue_block(sh->tmem, half,
+                               umma_desc(smem_u32(opsm + (size_t)(st.op + (st.bvar ? half : 0)) * kTcOpBytes), 128, 1024));
                 mma_commit(&sh->bar[half]);
             }
             __syncwarp();
@@ -429,7 +433,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
             const StvGroup &g = groups[st.group];
             const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off) + st.first;
             tc_build_op(subs, st.n, mat, (const StvDTab *)((const uint8_t *)P + P->tab_off), tables, full_base, tord,
-                        rank_bits, scal, opsm + (size_t)st.op * kTcOpBytes, lane);
+                        rank_bits, scal, opsm + (size_t)st.op * kTcOpBytes, st.bvar ? g.vbit[7][0] : 0u, lane);
             __syncwarp();
             if (lane == 0) sh->key[st.op] = key;
         }

@@ -62,7 +62,7 @@ class Pass(ct.Structure):
 
 class TcStep(ct.Structure):
     _fields_ = [("kind", ct.c_int16), ("last", ct.c_int16), ("first", ct.c_int16), ("n", ct.c_int16),
-                ("op", ct.c_int32), ("group", ct.c_int32), ("dep", ct.c_uint64), ("pad", ct.c_uint64)]
+                ("op", ct.c_int32), ("group", ct.c_int32), ("dep", ct.c_uint64), ("bvar", ct.c_int32), ("pad", ct.c_int32)]
 
 
 assert ct.sizeof(Op) == 64 and ct.sizeof(Sub) == 16 and ct.sizeof(Pass) == 208 and ct.sizeof(Term) == 16

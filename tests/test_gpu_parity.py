@@ -275,3 +275,26 @@ def test_plan_cache_hit_identical_and_frame_keyed(stv):
     ref = oracle.run(C.Circuit("x+c1", circ.n, [("x", (3,), ())] + list(circ.gates), x0=circ.x0))
     assert_parity(c, ref, "c64")
     assert np.array_equal(a, d)
+
+
+@pytest.mark.parametrize("dims", [(4, 5, 20, 2), (4, 6, 20, 3)])
+def test_tc_block_variants_parity(stv, dims):
+    """Tensor-core passes with per-block operator variants (a one-V-bit table or V-bit-controlled
+    CNOT folded into two operators, one per 128-row TMEM block) and with the fully tile-uniform
+    operators, against the oracle; the same circuit on the CUDA-core kernel agrees too."""
+    from tests import blob_emu as BE
+    R, Cc, cyc, seed = dims
+    circ = C.grid_circuit("g", R, Cc, 0, cyc, "fsim", seed)
+    blob, offs = stv.plan_blob(circ.n, circ.gates)
+    nb = 0
+    for po in offs:
+        P = BE._at(blob, BE.Pass, po)
+        if P.kind == 1 and P.grouped and P.ntc:
+            nb += sum(1 for i in range(P.ntc) if BE._at(blob, BE.TcStep, po + P.tc_off + 32 * i).bvar)
+    assert nb > 0
+    ref = oracle.run(circ)
+    psi, st = run_gpu(stv, circ, "c64")
+    assert st["n_tc_pass"] > 0
+    assert_parity(psi, ref, "c64")
+    psi2, _ = run_gpu(stv, circ, "c64", flags=stv.OPT_NO_TC)
+    assert_parity(psi2, ref, "c64")

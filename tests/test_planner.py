@@ -373,19 +373,26 @@ def test_tc_step_plan_structure(case):
             g = groups[gi]
             subs = [BE._at(blob, BE.Sub, po + g.sub_off + 16 * (s.first + k)) for k in range(s.n)]
             if s.kind == 1:
-                assert s.op not in ops and s.op < P.ntcop
-                ops.add(s.op)
+                slots = [s.op, s.op + 1] if s.bvar else [s.op]     # block variants: one slot per block
+                assert not (set(slots) & ops) and max(slots) < P.ntcop
+                ops.update(slots)
+                bv = g.vbit[7][0] if g.nvb >= 8 else 0                # the block = vector bit 7
+                uses_block = False
                 for sb in subs:
                     c = sb.code & 0xFF
-                    if 10 <= c < 30:
-                        assert sb.ctl & 0xFFFF == 0                    # no V-bit control
+                    if 10 <= c < 30 and sb.ctl & 0xFFFF:                # V-bit control: only the block bit
+                        assert sb.ctl & 0xFFFF == bv
+                        uses_block = True
                     if c == 30 or 37 <= c < 41:
-                        assert BE._at(blob, BE.DTab, po + P.tab_off + 48 * sb.arg).m == 0
+                        d = BE._at(blob, BE.DTab, po + P.tab_off + 48 * sb.arg)
+                        assert d.m == 0 or (d.m == 1 and d.vraw[0] == bv)
+                        uses_block |= d.m == 1
                     if 31 <= c < 37:
                         for i in range(3):
                             sel = (sb.code >> (8 + 5 * i)) & 31
                             if sel != 31:
                                 assert (s.dep >> out_bits[sel]) & 1
+                assert uses_block == bool(s.bvar)
             pos += s.n
             if s.last:
                 assert pos == g.nsub

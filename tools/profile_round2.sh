@@ -3,7 +3,7 @@
 # every single-GPU config, the c2 k-sweep, per-pass times, an ncu launch list of the bench command
 # and one ncu --set full capture of the tensor-core pass.   gpurun --timeout 3600 -- 'bash tools/profile_round2.sh'
 cd "${GRAFT_REPO_ROOT:-.}"
-O=gpurun_out/r02
+O=${1:-gpurun_out/r02}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/gpu.txt 2>&1
 nproc > $O/host.txt; free -g >> $O/host.txt; lscpu | grep "Model name" >> $O/host.txt
@@ -29,4 +29,5 @@ $N > $O/ncu_plain2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:k_tc_group_pass -s 20 -c 1 \
       -o $O/tc_full -f $N > $O/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> $O/ncu_full.log
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 tail -3 $O/pytest.log; for f in $O/bench_*.json; do echo $f; head -c 300 $f; echo; done

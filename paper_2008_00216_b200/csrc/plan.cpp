@@ -1687,11 +1687,15 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
     std::vector<StvTcStep> st;
     int nop = 0;
     uint64_t dep_all = 0;
+    auto build = [&](bool allow_bvar) {
+    st.clear();
+    nop = 0;
+    dep_all = 0;
     for (size_t gi = 0; gi < grecs.size(); ++gi) {
         const StvGroup &G = grecs[gi];
         const StvSub *sp = (const StvSub *)&b[at + G.sub_off];
         const size_t g0 = st.size();
-        bvraw = (G.nvb >= 8 && hd.S == 12) ? G.vbit[7][0] : 0;
+        bvraw = (allow_bvar && G.nvb >= 8 && hd.S == 12) ? G.vbit[7][0] : 0;
         int k = 0;
         while (k < G.nsub) {
             bool f = foldable(sp[k]);
@@ -1734,6 +1738,10 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
         }
         st.back().last = 1;
     }
+    };
+    // block variants cost operator slots (2 per step); measured on c2/c4 they pay even where
+    // the extra slots push a pass to the single-buffered tile ring
+    build(true);
     const int nord = __builtin_popcountll(hd.out_mask);
     const size_t need = st.size() * sizeof(StvTcStep) + 16;
     if (nop == 0 || nop > STV_TC_MAX_OPS || st.size() > STV_TC_MAX_STEPS || nord > 48 ||

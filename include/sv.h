@@ -96,6 +96,8 @@ typedef struct {
 #define SV_OPT_NO_TC        0x100u /* complex64 gate groups on the CUDA-core FMA path only (no tcgen05 pass) */
 #define SV_OPT_NO_SINK      0x400u /* keep diagonal terms over in-tile non-register bits in place (no sinking
                                         to the end of a gate group's program; tensor-core planning) */
+#define SV_OPT_TMA          0x800u /* tensor-core passes: tiles staged with TMA tensor copies (SWIZZLE_128B
+                                        layout) instead of 16-B cp.async (measured slower on c2/c4: opt-in) */
 #define SV_OPT_NO_PLAN_CACHE 0x200u /* plan from scratch: do not reuse the plan of an identical earlier call
                                         (same gates, frame and options; the last 4 are kept per state) */
 typedef struct {

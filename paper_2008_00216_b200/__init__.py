@@ -25,7 +25,7 @@ KINDS = {"h": 0, "x": 1, "y": 2, "z": 3, "s": 4, "t": 5, "sx": 6, "sy": 7, "sw":
 GATE_ADJOINT = 0x1
 OPT_PROFILE, OPT_NO_RELABEL, OPT_NO_REORDER, OPT_ONE_GATE, OPT_NO_DIAG_FOLD, OPT_NO_GROUPS = 1, 2, 4, 8, 16, 32
 OPT_NO_VARIANTS = 128
-OPT_NO_TC, OPT_NO_PLAN_CACHE = 256, 512
+OPT_NO_TC, OPT_NO_PLAN_CACHE, OPT_NO_SINK, OPT_TMA = 256, 512, 1024, 2048
 C64, C128 = 0, 1
 STATUS = {0: "SV_OK", 1: "SV_ERR_INVALID_ARG", 2: "SV_ERR_OUT_OF_MEMORY", 3: "SV_ERR_CUDA",
           4: "SV_ERR_NCCL", 5: "SV_ERR_UNSUPPORTED", 6: "SV_ERR_STATE"}

@@ -14,6 +14,7 @@
 //                    the state with control = 1.
 //   k_norm_*         a10: fp64 fixed-shape reduction.
 //   k_init_*, k_gather  a11.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -1781,9 +1782,88 @@ cudaError_t launch_group_pass(bool c128, void *state, const uint8_t *dblob, cons
 
 // tensor-core group pass (tc_pass.cuh): 2 CTAs per SM (TMEM 256 columns each); a
 // double-buffered tile ring when it fits the shared memory of 2 CTAs, else one buffer
+// TMA tensor map of a tensor-core pass's tiles (tc_pass.cuh TcTma): dims (16 amplitudes) x
+// [rest of the low run, stride 128 B] x (tile base: stride 2^L amplitudes, box 1) x up to 3 runs
+// of consecutive high tile bits; further high bits are looped by the kernel.  cuTensorMapEncodeTiled
+// comes from the driver through cudaGetDriverEntryPoint (no link-time libcuda dependency).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+    }
+    return fn;
+}
+
+static bool make_tile_tmap(CUtensorMap *tm, TcTma *t, void *state, const StvPass *P, int n_local) {
+    std::memset(t, 0, sizeof(*t));
+    static const bool off = getenv("STV_NO_TMA") && atoi(getenv("STV_NO_TMA"));
+    EncodeTiledFn enc = encode_tiled_fn();
+    if (off || !enc || !P->swz_tma || P->L < 4 || n_local - P->L > 32) return false;
+    cuuint64_t gdim[5];
+    cuuint64_t gstr[4];
+    cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+    int r = 0;
+    uint64_t box_elems = 16;
+    gdim[0] = 16;
+    box[0] = 16;
+    r = 1;
+    if (P->L > 4) {
+        gdim[r] = 1ull << (P->L - 4);
+        gstr[r - 1] = 128;
+        box[r] = 1u << (P->L - 4);
+        box_elems <<= P->L - 4;
+        ++r;
+    }
+    t->bdim = r;   // the tile base
+    gdim[r] = 1ull << (n_local - P->L);
+    gstr[r - 1] = 8ull << P->L;
+    box[r] = 1;
+    ++r;
+    for (int i = 0; i < P->h;) {   // runs of consecutive high tile bits, ascending
+        int j = i;
+        while (j + 1 < P->h && P->hpos[j + 1] == P->hpos[j] + 1) ++j;
+        const int len = j - i + 1, start = P->hpos[i];
+        if (r < 5 && len <= 8) {
+            gdim[r] = 1ull << len;
+            gstr[r - 1] = 8ull << start;
+            box[r] = 1u << len;
+            box_elems <<= len;
+            ++r;
+        } else {
+            for (int k = i; k <= j; ++k) t->extra_mask |= 1ull << P->hpos[k];
+        }
+        i = j + 1;
+    }
+    while (r < 5) {
+        gdim[r] = 1;
+        gstr[r - 1] = gstr[r - 2];
+        box[r] = 1;
+        ++r;
+    }
+    t->nld = 1u << __builtin_popcountll(t->extra_mask);
+    t->box_bytes = (uint32_t)(box_elems * 8);
+    t->L = P->L;
+    if (box_elems * t->nld != (1ull << P->S)) return false;
+    const CUresult cr = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, state, gdim, gstr, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return false;
+    static const int st_env = getenv("STV_TMA_STORE") ? atoi(getenv("STV_TMA_STORE")) : 0;
+    t->on = st_env ? 2 : 1;
+    return true;
+}
+
 template <int NS, bool FULL>
 static cudaError_t tc_launch(void *state, const uint8_t *dblob, uint32_t pass_off, uint32_t ntiles, size_t smem,
-                             const RecParam &rp, cudaStream_t st) {
+                             const CUtensorMap &tm, const TcTma &tma, const RecParam &rp, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_tc_group_pass<NS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
@@ -1792,28 +1872,33 @@ static cudaError_t tc_launch(void *state, const uint8_t *dblob, uint32_t pass_of
     uint64_t grid = (uint64_t)num_sms() * 2;
     if (grid > ntiles) grid = ntiles;
     static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
-    k_tc_group_pass<NS, FULL><<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, ntiles, dbg, rp);
+    k_tc_group_pass<NS, FULL><<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, ntiles, dbg, tm, tma,
+                                                                 rp);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off, int S,
                                  int n_local, uint32_t rec_bytes, uint32_t tab_entries, int ntcop, cudaStream_t st,
                                  int *kernels) {
-    const size_t fixed = (size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127) +
-                         sizeof(TcShared);
+    // 1024-B alignment of the tile ring (SWIZZLE_128B): fixed part rounded up
+    const size_t fixed = ((size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127)) +
+                         1024 /* ring alignment slack */ + sizeof(TcShared);
     const size_t tile = (size_t)8 << S;
     const uint64_t ntiles = 1ull << (n_local - S);
     const size_t cap = 113 * 1024;   // 2 CTAs per SM
     if (fixed + tile > cap || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
     static thread_local RecParam rp;
     std::memcpy(rp.b, hrec, rec_bytes);
+    static thread_local CUtensorMap tm;
+    TcTma tma;
+    make_tile_tmap(&tm, &tma, state, (const StvPass *)hrec, n_local);
     static const int ns_env = getenv("STV_TC_NS") ? atoi(getenv("STV_TC_NS")) : 2;
     const bool two = ns_env >= 2 && fixed + 2 * tile <= cap, full = S == 12;
     cudaError_t e;
-    if (two) e = full ? tc_launch<2, true>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, rp, st)
-                      : tc_launch<2, false>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, rp, st);
-    else e = full ? tc_launch<1, true>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, rp, st)
-                  : tc_launch<1, false>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, rp, st);
+    if (two) e = full ? tc_launch<2, true>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, tm, tma, rp, st)
+                      : tc_launch<2, false>(state, dblob, pass_off, (uint32_t)ntiles, fixed + 2 * tile, tm, tma, rp, st);
+    else e = full ? tc_launch<1, true>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, tm, tma, rp, st)
+                  : tc_launch<1, false>(state, dblob, pass_off, (uint32_t)ntiles, fixed + tile, tm, tma, rp, st);
     ++*kernels;
     return e;
 }

@@ -87,7 +87,8 @@ struct alignas(16) StvPass {
     uint32_t tc_off;           // byte offset of StvTcStep[ntc] (kernel-parameter part)
     int32_t ntc;               // steps over all groups, in group order
     int32_t ntcop;             // operator slots (M steps), <= STV_TC_MAX_OPS
-    int32_t tc_pad;
+    int32_t swz_tma;           // 1: tile layout = TMA SWIZZLE_128B (chunk c at c ^ ((c >> 3) & 7)), tiles
+                               // staged with cp.async.bulk.tensor; 0: the kSwzH pattern below
     uint8_t tperm[48];         // tile ordinal bit of permuted-ordinal bit i (dep bits on top)
 };
 

@@ -1383,7 +1383,12 @@ static void encode_diag(std::vector<uint8_t> &b, size_t rec_at, const QForm &f, 
 
 // Shared-memory slot of tile amplitude i under the chunk swizzle of
 // pass_format.h (linear over GF(2)).
+// Tile swizzle of the pass being encoded: the group pass's XOR pattern H (kSwzH), or for
+// tensor-core passes staged by TMA the SWIZZLE_128B pattern H(x) = x & 7 (16-B chunk j of
+// each 128-B line stored at j ^ (line mod 8); pass_format.h StvPass.swz_tma).
+static thread_local bool g_swz_tma = false;
 static uint32_t swz_hash(uint32_t x) {
+    if (g_swz_tma) return x & 7u;
     return (uint32_t)(__builtin_popcount(x & kSwzM0) & 1) | ((uint32_t)(__builtin_popcount(x & kSwzM1) & 1) << 1) |
            ((uint32_t)(__builtin_popcount(x & kSwzM2) & 1) << 2);
 }
@@ -1397,7 +1402,9 @@ static uint32_t swz_amp(uint32_t i, bool c128) {
 static uint32_t bank_vec(int p, bool c128) {
     const int j = c128 ? p : p - 1;          // chunk bit
     if (j < 0) return 0;
-    return j < 3 ? (1u << j) : kSwzH[j - 3];
+    if (j < 3) return 1u << j;
+    if (g_swz_tma) return j < 6 ? (1u << (j - 3)) : 0u;
+    return kSwzH[j - 3];
 }
 
 // Order of a group's vector bits: lane bits 0..2 (LDS.128 phases of 8 lanes)
@@ -1758,6 +1765,7 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
     hd.tc_off = (uint32_t)(b.size() - at);
     hd.ntc = (int32_t)st.size();
     hd.ntcop = nop;
+    hd.swz_tma = g_swz_tma ? 1 : 0;
     put(b, st.data(), st.size() * sizeof(StvTcStep));
 }
 
@@ -1765,7 +1773,7 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
     Encoded e;
     std::vector<uint8_t> &b = e.blob;
     const size_t esz = c128 ? 16 : 8;
-    for (const PPass &ps : p.passes) {
+    auto encode_pass = [&](const PPass &ps) {
         align(b, 256);
         const size_t at = b.size();
         e.pass_off.push_back((uint32_t)at);
@@ -2189,6 +2197,22 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
         }
         hd.rec_bytes = (uint32_t)(b.size() - at);
         std::memcpy(&b[at], &hd, sizeof(hd));
+    };
+    for (const PPass &ps : p.passes) {
+        // with SV_OPT_TMA, tensor-core candidates are encoded for TMA staging (SWIZZLE_128B tile
+        // layout); a pass that ends up without operator steps is re-encoded for the CUDA-core pass
+        const bool tma = !c128 && ps.kind == PASS_TILE && __builtin_popcountll(ps.S) <= 12 &&
+                         (p.flags & SV_OPT_TMA) && !(p.flags & SV_OPT_NO_TC);
+        const size_t mark = b.size();
+        g_swz_tma = tma;
+        encode_pass(ps);
+        if (tma && ((const StvPass *)&b[e.pass_off.back()])->ntc == 0) {
+            b.resize(mark);
+            e.pass_off.pop_back();
+            g_swz_tma = false;
+            encode_pass(ps);
+        }
+        g_swz_tma = false;
     }
     align(b, 256);
     return e;

@@ -167,6 +167,7 @@ __device__ __forceinline__ void tc_issue_block(uint32_t tmem, int b, uint64_t de
 
 struct alignas(16) TcShared {
     uint64_t bar[2];
+    uint64_t tbar[2];   // TMA tile loads, one per ring slot
     uint32_t tmem;
     uint32_t pad;
     uint64_t key[STV_TC_MAX_OPS];
@@ -323,13 +324,42 @@ __device__ __forceinline__ void tc_tile_copy(uint8_t *gtile, uint8_t *stile, con
     }
 }
 
+// TMA staging of a pass's tiles (host: launch_tc_group_pass).  One 5-D tensor map views
+// the state as (16 contiguous amplitudes) x (tile base: stride 2^L amplitudes, box 1) x
+// (the rest of the low run) x (up to 2 runs of consecutive high tile bits); the box is the
+// tile in tile-index order, stored with SWIZZLE_128B.  High tile bits beyond the map's
+// dims are looped over: load e covers the tile amplitudes whose extra bits equal e.
+struct TcTma {
+    uint64_t extra_mask;   // physical bits of the looped tile bits
+    uint32_t nld;          // loads (= stores) per tile: 2^popcount(extra_mask)
+    uint32_t box_bytes;    // bytes per load
+    int32_t L;             // tile low bits: base coordinate = (base | extra) >> L
+    int32_t bdim;          // tensor dim of the base coordinate (1, or 2 when L > 4)
+    int32_t on;            // 1: TMA staging (else cp.async with the same swizzle)
+    int32_t pad;
+};
+__device__ __forceinline__ void tma_load_tile(void *dst, const CUtensorMap *tm, uint32_t c1, uint32_t c2,
+                                              uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %2, %2}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap *tm, uint32_t c1, uint32_t c2, const void *src) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %1, %1}], [%4];" ::"l"(tm),
+                 "r"(0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+}
+
 // Tensor-core group pass: persistent CTAs (2 per SM, 256 threads), tile ordinals in
 // the permuted order of StvPass.tperm, a contiguous range per CTA; NS = 2: the next
 // tile's load overlaps this tile's work (1: single buffer when shared memory is short).
 template <int NS, bool FULL>
 __global__ void __launch_bounds__(256, 2)
 k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, uint32_t pass_off, uint32_t ntiles,
-                int dbg_flags, const __grid_constant__ RecParam rec) {
+                int dbg_flags, const __grid_constant__ CUtensorMap tmap, const TcTma tma,
+                const __grid_constant__ RecParam rec) {
     constexpr int NT = 256;
     extern __shared__ __align__(1024) uint8_t smem[];
     const StvPass *P = (const StvPass *)rec.b;
@@ -349,7 +379,8 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     float2 *scal = (float2 *)(hk + 1024);
     float2 *tables = (float2 *)(hk + 1536);
     const uint32_t tab_pad = (P->tab_entries * esz + 127u) & ~127u;
-    float2 *tiles = (float2 *)(hk + 1536 + tab_pad);
+    // tile ring 1024-B aligned (TMA SWIZZLE_128B pattern = shared address bits 4..6 ^ 7..9)
+    float2 *tiles = (float2 *)(smem + (((smem_u32(hk + 1536 + tab_pad) + 1023u) & ~1023u) - smem_u32(smem)));
     const uint32_t tile_elems = 1u << S;
     TcShared *sh = (TcShared *)((uint8_t *)tiles + (size_t)NS * tile_elems * esz);
     const uint32_t run_bytes = (1u << L) * esz;
@@ -369,7 +400,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         const uint32_t c = (uint32_t)tid + NT * (uint32_t)k;
         const uint32_t i = 2 * c;   // first tile-local amplitude of the chunk
         goff[k] = (pdep64(i >> L, hmask) + (i & ((1u << L) - 1))) * esz;
-        soff[k] = 16u * (c ^ swz_hash_d(c >> 3));
+        soff[k] = 16u * (c ^ (P->swz_tma ? ((c >> 3) & 7u) : swz_hash_d(c >> 3)));
     }
     const int nord = __popcll(out_mask);
     if (warp == 0) {
@@ -381,6 +412,8 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     if (tid == 32) {
         mbar_init(&sh->bar[0], 1);
         mbar_init(&sh->bar[1], 1);
+        mbar_init(&sh->tbar[0], 1);
+        mbar_init(&sh->tbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid < STV_TC_MAX_OPS) sh->key[tid] = ~0ull;
@@ -410,11 +443,34 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     uint64_t base = pdep64(tord, out_mask);
     uint64_t lbase = base;   // next tile to load
     uint8_t *gstate = (uint8_t *)state;
+    const bool use_tma = tma.on != 0;
+    const bool tma_store = tma.on == 2;   // 1: TMA loads, thread stores; 2: TMA loads and stores
+    uint32_t tph = 0;   // TMA load barrier phases (bit per slot)
     auto issue = [&](uint32_t tp, int slot) {   // load tile tp (if in range) into ring slot
-        if (tp < t_end && !(dbg_flags & 2))
-            tc_tile_copy<true>(gstate + lbase * esz, (uint8_t *)(tiles + (size_t)slot * tile_elems), goff, soff, nk);
-        cp_async_commit();
+        uint8_t *stile = (uint8_t *)(tiles + (size_t)slot * tile_elems);
+        if (use_tma) {
+            // warp 0: lane e issues the loads e, e + 32, ... (and, at the end of the tile, the
+            // stores of the same boxes, so its own bulk groups order store-read before reload)
+            if (warp == 0 && tp < t_end && !(dbg_flags & 2)) {
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // this lane's last stores have read
+                if (lane == 0) mbar_arrive_expect_tx(&sh->tbar[slot], (uint32_t)(tile_elems * esz));
+                __syncwarp();
+                for (uint32_t e = lane; e < tma.nld; e += 32) {
+                    const uint32_t cb = (uint32_t)((lbase | pdep64(e, tma.extra_mask)) >> tma.L);
+                    tma_load_tile(stile + (size_t)e * tma.box_bytes, &tmap, tma.bdim == 1 ? cb : 0u,
+                                  tma.bdim == 2 ? cb : 0u, &sh->tbar[slot]);
+                }
+            }
+        } else {
+            if (tp < t_end && !(dbg_flags & 2)) tc_tile_copy<true>(gstate + lbase * esz, stile, goff, soff, nk);
+            cp_async_commit();
+        }
         if (tp + 1 < t_end) lbase ^= sh->cm[__ffs(~tp) - 1];
+    };
+    auto wait_tile = [&](int slot) {
+        if (dbg_flags & 2) return;
+        mbar_wait_spin(&sh->tbar[slot], (tph >> slot) & 1u);
+        tph ^= 1u << slot;
     };
     if (NS == 2) issue(t_begin, 0);
     for (uint32_t tp = t_begin; tp < t_end; ++tp) {
@@ -440,9 +496,11 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         fence_proxy_async();   // operator slots (generic-proxy stores) -> tensor-core reads
         if (NS == 2) {
             issue(tp + 1, slot ^ 1);   // the other slot was freed by the previous iteration's last barrier
-            cp_async_wait1();
+            if (use_tma) wait_tile(slot);
+            else cp_async_wait1();
         } else {
-            cp_async_wait0();
+            if (use_tma) wait_tile(0);
+            else cp_async_wait0();
         }
         __syncthreads();
         if (!(dbg_flags & 1)) {
@@ -455,7 +513,24 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
                 __syncthreads();
             }
         }
-        if (!(dbg_flags & 2)) tc_tile_copy<false>(gstate + base * esz, (uint8_t *)tile, goff, soff, nk);
+        if (!(dbg_flags & 2)) {
+            if (use_tma && tma_store) {
+                fence_proxy_async();   // the groups' scatters (generic proxy) -> the TMA store
+                __syncthreads();
+                if (warp == 0) {
+                    for (uint32_t e = lane; e < tma.nld; e += 32) {
+                        const uint32_t cb = (uint32_t)((base | pdep64(e, tma.extra_mask)) >> tma.L);
+                        tma_store_tile(&tmap, tma.bdim == 1 ? cb : 0u, tma.bdim == 2 ? cb : 0u,
+                                       (const uint8_t *)tile + (size_t)e * tma.box_bytes);
+                    }
+                    bulk_commit();
+                }
+            } else {
+                // write-back by all threads (16-B LDS + STG): the slot is free at the next barrier
+                // without waiting for a bulk store to drain it before its reload
+                tc_tile_copy<false>(gstate + base * esz, (uint8_t *)tile, goff, soff, nk);
+            }
+        }
         if (tp + 1 < t_end) {
             const int j = __ffs(~tp) - 1;
             base ^= sh->cm[j];
@@ -464,6 +539,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         __syncthreads();   // write-back reads of this slot done before it is reloaded
     }
     cp_async_wait0();
+    if (use_tma && warp == 0) bulk_wait_all();   // the last stores have completed
     tc_fence_before();
     __syncthreads();
     if (warp == 0) {

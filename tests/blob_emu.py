@@ -56,7 +56,7 @@ class Pass(ct.Structure):
                 ("mat_bytes", ct.c_uint32), ("cnot_c", ct.c_int32), ("cnot_t", ct.c_int32), ("diag_off", ct.c_uint32),
                 ("rec_bytes", ct.c_uint32), ("ntab", ct.c_int32), ("tab_off", ct.c_uint32), ("grouped", ct.c_int32),
                 ("tab_entries", ct.c_uint32), ("param_bytes", ct.c_uint32),
-                ("tc_off", ct.c_uint32), ("ntc", ct.c_int32), ("ntcop", ct.c_int32), ("tc_pad", ct.c_int32),
+                ("tc_off", ct.c_uint32), ("ntc", ct.c_int32), ("ntcop", ct.c_int32), ("swz_tma", ct.c_int32),
                 ("tperm", ct.c_uint8 * 48)]
 
 
@@ -161,8 +161,10 @@ def _run_group(psi, n, blob, po, P, g, pos2phys, c128, j):
 
     # inverse of the swizzle on single tile positions: flipped position from its swizzled offset
     c128_ = c128
+    tma = bool(getattr(P, "swz_tma", 0))
+
     def swz(i):
-        H = [3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7]
+        H = [1, 2, 4, 0, 0, 0, 0, 0, 0, 0, 0] if tma else [3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7]
         def h(x):
             r, j = 0, 0
             while x:

@@ -57,7 +57,8 @@ def test_random_circuits_all_kinds(stv, n, seed, dtype):
                                 dict(tile_bits=8, low_bits=3), dict(tile_bits=13, low_bits=5),
                                 dict(tile_bits=10, low_bits=0), dict(budget=400), dict(budget=20),
                                 dict(flags=2), dict(flags=4), dict(flags=8), dict(flags=16),
-                                dict(flags=32), dict(flags=128), dict(flags=32 | 128)])
+                                dict(flags=32), dict(flags=128), dict(flags=32 | 128),
+                                dict(flags=0x400), dict(flags=0x800)])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_planner_options(stv, kw, dtype):
     circ = C.random_circuit(17, 300, 42)
@@ -298,3 +299,14 @@ def test_tc_block_variants_parity(stv, dims):
     assert_parity(psi, ref, "c64")
     psi2, _ = run_gpu(stv, circ, "c64", flags=stv.OPT_NO_TC)
     assert_parity(psi2, ref, "c64")
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_tma_staged_tc_pass_parity(stv, cfg):
+    """Tensor-core passes staged with TMA tensor copies (SV_OPT_TMA: 5-D tensor map with an
+    overlapping tile-base dim, SWIZZLE_128B tile layout, looped boxes) against the oracle."""
+    circ = C.config(cfg) if cfg == 1 else C.grid_circuit("g", 4, 6, 0, 12, "fsim", 21)
+    ref = oracle.run(circ)
+    a, st = run_gpu(stv, circ, "c64", flags=stv.OPT_TMA)
+    assert st["n_tc_pass"] > 0
+    assert_parity(a, ref, "c64")

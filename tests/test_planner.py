@@ -213,9 +213,10 @@ def test_encoded_blob_semantics(case, dtype):
     assert np.max(np.abs(psi - ref)) < tol
 
 
-def _swz_slot(chunk):
-    """Shared-memory slot of a 16-B tile chunk (pass_format.h, restated)."""
-    H = [3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7]
+def _swz_slot(chunk, tma=False):
+    """Shared-memory slot of a 16-B tile chunk (pass_format.h, restated): the group pass's
+    kSwzH pattern, or TMA SWIZZLE_128B (chunk j of each 128-B line at j ^ (line mod 8))."""
+    H = [1, 2, 4, 0, 0, 0, 0, 0, 0, 0, 0] if tma else [3, 5, 6, 7, 1, 2, 4, 3, 5, 6, 7]
     h, x, j = 0, chunk >> 3, 0
     while x:
         if x & 1:
@@ -282,7 +283,7 @@ def test_group_layout_bijective_and_conflict_free(case, dtype):
                 for l in range(16):
                     i, a = raw_index(v, l), addr(v, l)
                     ci = i >> (0 if c128 else 1)
-                    exp = _swz_slot(ci) if c128 else (_swz_slot(ci) << 1) | (i & 1)
+                    exp = _swz_slot(ci, P.swz_tma) if c128 else (_swz_slot(ci, P.swz_tma) << 1) | (i & 1)
                     assert a == exp
                     seen.add(a)
             assert len(seen) == 1 << P.S

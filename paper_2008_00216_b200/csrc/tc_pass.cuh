@@ -165,6 +165,31 @@ __device__ __forceinline__ void tc_issue_block(uint32_t tmem, int b, uint64_t de
     for (int kk = 0; kk < 4; ++kk) mma_tf32_ts_c<true>(d, ah + 8 * kk, desc0 + 16 * kk);
 }
 
+// The same 12 MMAs + commit issued by one elected lane of a converged warp, in one asm block:
+// the operands are formed once in uniform registers (no per-MMA elect loop and R2UR moves).
+__device__ __forceinline__ void tc_issue_block_elect(uint32_t tmem, int b, uint64_t desc0, uint32_t bar) {
+    const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 dd;\n\t"
+        "elect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 0;\n\t"
+        "add.u64 dd, %3, 16;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%6], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 32;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%7], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 48;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%8], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 256;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 272;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 288;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%10], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 304;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], dd, %5, 1;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, 1;\n\t"
+        "add.u64 dd, %3, 16;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 32;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%10], dd, %5, 1;\n\t"
+        "add.u64 dd, %3, 48;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], dd, %5, 1;\n\t"
+        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
+        ::"r"(d), "r"(al), "r"(ah), "l"(desc0), "r"(bar), "n"(kTcIdesc), "r"(al + 8), "r"(al + 16), "r"(al + 24),
+        "r"(ah + 8), "r"(ah + 16), "r"(ah + 24)
+        : "memory");
+}
+
 struct alignas(16) TcShared {
     uint64_t bar[2];
     uint64_t tbar[2];   // TMA tile loads, one per ring slot
@@ -277,13 +302,13 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
             // each half of the CTA (warps 0-3: block 0, warps 4-7: block 1) syncs and issues its own MMAs
             const int half = ctid >> 7;
             asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
-            if ((ctid & 127) == 0) {
+            if ((ctid & 127) < 32) {   // the half's first warp, converged: one elected lane issues
                 tc_fence_after();
-                tc_issue_block(sh->tmem, half,
-                               umma_desc(smem_u32(opsm + (size_t)(st.op + (st.bvar ? half : 0)) * kTcOpBytes), 128, 1024));
-                mma_commit(&sh->bar[half]);
+                tc_issue_block_elect(sh->tmem, half,
+                                     umma_desc(smem_u32(opsm + (size_t)(st.op + (st.bvar ? half : 0)) * kTcOpBytes), 128,
+                                               1024),
+                                     smem_u32(&sh->bar[half]));
             }
-            __syncwarp();
             mbar_wait_spin(&sh->bar[half], phase);
             phase ^= 1u;
             tc_fence_after();

@@ -165,29 +165,12 @@ __device__ __forceinline__ void tc_issue_block(uint32_t tmem, int b, uint64_t de
     for (int kk = 0; kk < 4; ++kk) mma_tf32_ts_c<true>(d, ah + 8 * kk, desc0 + 16 * kk);
 }
 
-// The same 12 MMAs + commit issued by one elected lane of a converged warp, in one asm block:
-// the operands are formed once in uniform registers (no per-MMA elect loop and R2UR moves).
-__device__ __forceinline__ void tc_issue_block_elect(uint32_t tmem, int b, uint64_t desc0, uint32_t bar) {
-    const uint32_t ah = tmem + b * 96, al = ah + 32, d = ah + 64;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t.reg .b64 dd;\n\t"
-        "elect.sync _|p, 0xffffffff;\n\t"
-        "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 0;\n\t"
-        "add.u64 dd, %3, 16;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%6], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 32;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%7], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 48;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%8], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 256;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 272;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 288;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%10], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 304;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], dd, %5, 1;\n\t"
-        "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, 1;\n\t"
-        "add.u64 dd, %3, 16;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%9], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 32;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%10], dd, %5, 1;\n\t"
-        "add.u64 dd, %3, 48;\n\t@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%11], dd, %5, 1;\n\t"
-        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%4];\n\t}"
-        ::"r"(d), "r"(al), "r"(ah), "l"(desc0), "r"(bar), "n"(kTcIdesc), "r"(al + 8), "r"(al + 16), "r"(al + 24),
-        "r"(ah + 8), "r"(ah + 16), "r"(ah + 24)
-        : "memory");
+// 1 in exactly one lane of the converged warp (elect.sync): ptxas then issues the guarded
+// tensor-core instructions once, from uniform registers
+__device__ __forceinline__ bool elect_one() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
+    return e != 0;
 }
 
 struct alignas(16) TcShared {
@@ -304,10 +287,14 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
             asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
             if ((ctid & 127) < 32) {   // the half's first warp, converged: one elected lane issues
                 tc_fence_after();
-                tc_issue_block_elect(sh->tmem, half,
-                                     umma_desc(smem_u32(opsm + (size_t)(st.op + (st.bvar ? half : 0)) * kTcOpBytes), 128,
-                                               1024),
-                                     smem_u32(&sh->bar[half]));
+                // warp-uniform operands (shfl from lane 0) so ptxas keeps them in uniform registers
+                const uint32_t tmu = __shfl_sync(~0u, sh->tmem + half * 96, 0);
+                const uint32_t opa = __shfl_sync(~0u, smem_u32(opsm + (size_t)(st.op + (st.bvar ? half : 0)) * kTcOpBytes), 0);
+                if (elect_one()) {
+                    tc_issue_block(tmu, 0, umma_desc(opa, 128, 1024));
+                    mma_commit(&sh->bar[half]);
+                }
+                __syncwarp();
             }
             mbar_wait_spin(&sh->bar[half], phase);
             phase ^= 1u;

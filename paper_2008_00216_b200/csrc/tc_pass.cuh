@@ -193,16 +193,12 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
                                          const float2 *__restrict__ tables, uint64_t full_base, uint32_t tord,
                                          const uint8_t *__restrict__ grec, const float2 *__restrict__ scal,
                                          const uint8_t *__restrict__ opsm, TcShared *sh, const uint32_t *gso,
-                                         uint32_t &phase, int ctid) {
+                                         uint32_t vw, uint32_t trow, uint32_t &phase, int ctid) {
     const int nvb = g.nvb;
     const uint32_t nvec = 1u << nvb;
     const bool live = FULL || (uint32_t)ctid < nvec;
-    uint32_t braw = 0, bsw = 0;
-    {
-        const uint32_t w = __ldg((const uint32_t *)(grec + g.vtab_off) + ctid);
-        bsw = w & 0xffffu;
-        braw = w >> 16;
-    }
+    // vw: this vector's word of the group's vector table (loaded one group ahead)
+    const uint32_t bsw = vw & 0xffffu, braw = vw >> 16;
     uint32_t so[16];   // byte offsets of the 16 register amplitudes (swizzled)
 #pragma unroll
     for (int l = 0; l < 16; l += 4) {
@@ -251,18 +247,16 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         for (int l = 0; l < 16; ++l) x[0][l] = make_float2(0.f, 0.f);
     }
     const uint32_t braw1[1] = {braw};
-    const int warp = ctid >> 5;
-    const uint32_t trow = sh->tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 96);
     for (int s = s0;; ++s) {
         const StvTcStep st = steps[s];
         if (st.kind == 0) {
             run_subs<float2, 1>(x, braw1, subs + st.first, st.n, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
         } else {
-            {   // A_hi = x itself (the tensor core reads the top 19 bits: tf32 truncation of x),
-                // A_lo = x - trunc_tf32(x) (exact in fp32), pre-rounded by half a tf32 ulp so the
-                // tensor core's truncation of A_lo rounds to nearest -- truncating both parts
-                // would shrink every amplitude (a norm decay of ~1e-6 per operator step)
-                // -> TMEM row of this thread, block warp / 4
+            {   // Veltkamp split x = hi + lo: c = (2^13 + 1) x, hi = c - (c - x) is x rounded to
+                // nearest at 11 significant bits (exact in tf32), lo = x - hi exact; lo's sign is
+                // independent of x's, so the tensor core's truncation of lo adds no bias (a
+                // truncated A = x or an unrounded lo = x - trunc(x) would shrink every amplitude:
+                // a norm decay of ~1e-6 per operator step) -> TMEM row of this thread, block warp / 4
                 uint32_t v[32];
 #pragma unroll
                 for (int l = 0; l < 16; ++l) {
@@ -288,10 +282,10 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
             if ((ctid & 127) < 32) {   // the half's first warp, converged: one elected lane issues
                 tc_fence_after();
                 // warp-uniform operands (shfl from lane 0) so ptxas keeps them in uniform registers
-                const uint32_t tmu = __shfl_sync(~0u, sh->tmem + half * 96, 0);
+                const uint32_t tmh = __shfl_sync(~0u, trow, 0);   // warp 4 half: lane 0, block half
                 const uint32_t opa = __shfl_sync(~0u, smem_u32(opsm + (size_t)(st.op + (st.bvar ? half : 0)) * kTcOpBytes), 0);
                 if (elect_one()) {
-                    tc_issue_block(tmu, 0, umma_desc(opa, 128, 1024));
+                    tc_issue_block(tmh, 0, umma_desc(opa, 128, 1024));
                     mma_commit(&sh->bar[half]);
                 }
                 __syncwarp();
@@ -325,14 +319,30 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
 // 16-B chunks c = t + 256 k (k < kTcChunks) between global (tile base + goff[k])
 // and its swizzled shared-memory slot soff[k] = 16 (c ^ H(c >> 3)) (see tile_copy_swz).
 constexpr int kTcChunks = 8;   // 2^12 complex64 amplitudes = 2048 chunks over 256 threads
-template <bool kLoad>
+template <bool kLoad, bool FULL>
 __device__ __forceinline__ void tc_tile_copy(uint8_t *gtile, uint8_t *stile, const uint64_t (&goff)[kTcChunks],
                                              const uint32_t (&soff)[kTcChunks], int nk) {
+    if (kLoad) {
 #pragma unroll
-    for (int k = 0; k < kTcChunks; ++k) {
-        if (k >= nk) break;
-        if (kLoad) cp_async16(stile + soff[k], gtile + goff[k]);
-        else *(uint4 *)(gtile + goff[k]) = *(const uint4 *)(stile + soff[k]);
+        for (int k = 0; k < kTcChunks; ++k) {
+            if (!FULL && k >= nk) break;
+            cp_async16(stile + soff[k], gtile + goff[k]);
+        }
+    } else if (FULL) {   // shared-memory reads four at a time ahead of their stores
+#pragma unroll
+        for (int k0 = 0; k0 < kTcChunks; k0 += 4) {
+            uint4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = *(const uint4 *)(stile + soff[k0 + k]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) *(uint4 *)(gtile + goff[k0 + k]) = v[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kTcChunks; ++k) {
+            if (k >= nk) break;
+            *(uint4 *)(gtile + goff[k]) = *(const uint4 *)(stile + soff[k]);
+        }
     }
 }
 
@@ -445,6 +455,12 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     __syncthreads();
     tc_fence_after();
     uint32_t phase = 0;
+    // this thread's TMEM row (lane 32 (warp % 4) + lane, block warp / 4); the CTA's base (warp-uniform)
+    const uint32_t tmu = __shfl_sync(~0u, sh->tmem, 0);
+    const uint32_t trow = tmu + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 96);
+    // the first group's vector-table word (the next group's is loaded while a group runs)
+    const uint32_t vw0 = nops ? __ldg((const uint32_t *)(grec + groups[0].vtab_off) + tid) : 0u;
+    // the first group's vector-table word (the next group's is loaded while a group runs)
 
     // contiguous range of permuted ordinals t' for this CTA
     const uint64_t G = gridDim.x;
@@ -474,7 +490,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
                 }
             }
         } else {
-            if (tp < t_end && !(dbg_flags & 2)) tc_tile_copy<true>(gstate + lbase * esz, stile, goff, soff, nk);
+            if (tp < t_end && !(dbg_flags & 2)) tc_tile_copy<true, FULL>(gstate + lbase * esz, stile, goff, soff, nk);
             cp_async_commit();
         }
         if (tp + 1 < t_end) lbase ^= sh->cm[__ffs(~tp) - 1];
@@ -517,9 +533,12 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         __syncthreads();
         if (!(dbg_flags & 1)) {
             int s0 = 0;
+            uint32_t vw = vw0;
             for (int o = 0; o < nops; ++o) {
+                const uint32_t w = vw;
+                if (o + 1 < nops) vw = __ldg((const uint32_t *)(grec + groups[o + 1].vtab_off) + tid);
                 tc_group<FULL>(tile, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh,
-                               sh->gso[o], phase, tid);
+                               sh->gso[o], w, trow, phase, tid);
                 while (!steps[s0].last) ++s0;
                 ++s0;
                 __syncthreads();
@@ -540,7 +559,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
             } else {
                 // write-back by all threads (16-B LDS + STG): the slot is free at the next barrier
                 // without waiting for a bulk store to drain it before its reload
-                tc_tile_copy<false>(gstate + base * esz, (uint8_t *)tile, goff, soff, nk);
+                tc_tile_copy<false, FULL>(gstate + base * esz, (uint8_t *)tile, goff, soff, nk);
             }
         }
         if (tp + 1 < t_end) {

@@ -1892,6 +1892,9 @@ cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_
     static thread_local CUtensorMap tm;
     TcTma tma;
     make_tile_tmap(&tm, &tma, state, (const StvPass *)hrec, n_local);
+    // tile ring: after the operator slots, hashes, scalars and tables, 1024-B aligned
+    tma.ring_off = (uint32_t)(((size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127) +
+                               1023u) & ~(size_t)1023);
     static const int ns_env = getenv("STV_TC_NS") ? atoi(getenv("STV_TC_NS")) : 2;
     const bool two = ns_env >= 2 && fixed + 2 * tile <= cap, full = S == 12;
     cudaError_t e;

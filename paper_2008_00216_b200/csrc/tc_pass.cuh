@@ -189,7 +189,7 @@ struct alignas(16) TcShared {
 // register offsets in bytes (shared memory, staged once per CTA).
 template <bool FULL>
 __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
-                                         const StvTcStep *__restrict__ steps, int s0, const uint8_t *__restrict__ mat,
+                                         const StvTcStep *__restrict__ steps, int &s0, const uint8_t *__restrict__ mat,
                                          const float2 *__restrict__ tables, uint64_t full_base, uint32_t tord,
                                          const uint8_t *__restrict__ grec, const float2 *__restrict__ scal,
                                          const uint8_t *__restrict__ opsm, TcShared *sh, const uint32_t *gso,
@@ -301,7 +301,10 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
                 for (int l = 0; l < 16; ++l) x[0][l] = make_float2(__uint_as_float(v[2 * l]), __uint_as_float(v[2 * l + 1]));
             }
         }
-        if (st.last) break;
+        if (st.last) {
+            s0 = s + 1;   // the next group's first step
+            break;
+        }
     }
     if (live) {
         if (pair16) {
@@ -358,7 +361,7 @@ struct TcTma {
     int32_t L;             // tile low bits: base coordinate = (base | extra) >> L
     int32_t bdim;          // tensor dim of the base coordinate (1, or 2 when L > 4)
     int32_t on;            // 1: TMA staging (else cp.async with the same swizzle)
-    int32_t pad;
+    uint32_t ring_off;     // byte offset of the tile ring in dynamic shared memory (multiple of 1024)
 };
 __device__ __forceinline__ void tma_load_tile(void *dst, const CUtensorMap *tm, uint32_t c1, uint32_t c2,
                                               uint64_t *bar) {
@@ -400,9 +403,9 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     uint8_t *hk = smem + (size_t)nmop * kTcOpBytes;
     float2 *scal = (float2 *)(hk + 1024);
     float2 *tables = (float2 *)(hk + 1536);
-    const uint32_t tab_pad = (P->tab_entries * esz + 127u) & ~127u;
-    // tile ring 1024-B aligned (TMA SWIZZLE_128B pattern = shared address bits 4..6 ^ 7..9)
-    float2 *tiles = (float2 *)(smem + (((smem_u32(hk + 1536 + tab_pad) + 1023u) & ~1023u) - smem_u32(smem)));
+    // tile ring 1024-B aligned (TMA SWIZZLE_128B pattern = shared address bits 4..6 ^ 7..9): the
+    // dynamic shared memory starts 1024-aligned (declared) and the host rounds the ring offset
+    float2 *tiles = (float2 *)(smem + tma.ring_off);
     const uint32_t tile_elems = 1u << S;
     TcShared *sh = (TcShared *)((uint8_t *)tiles + (size_t)NS * tile_elems * esz);
     const uint32_t run_bytes = (1u << L) * esz;
@@ -432,6 +435,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (tid == 32) {
+        if (smem_u32(smem) & 1023u) __trap();   // the swizzle and the ring offset assume it
         mbar_init(&sh->bar[0], 1);
         mbar_init(&sh->bar[1], 1);
         mbar_init(&sh->tbar[0], 1);
@@ -539,8 +543,6 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
                 if (o + 1 < nops) vw = __ldg((const uint32_t *)(grec + groups[o + 1].vtab_off) + tid);
                 tc_group<FULL>(tile, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh,
                                sh->gso[o], w, trow, phase, tid);
-                while (!steps[s0].last) ++s0;
-                ++s0;
                 __syncthreads();
             }
         }

@@ -252,11 +252,11 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         if (st.kind == 0) {
             run_subs<float2, 1>(x, braw1, subs + st.first, st.n, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
         } else {
-            {   // Veltkamp split x = hi + lo: c = (2^13 + 1) x, hi = c - (c - x) is x rounded to
-                // nearest at 11 significant bits (exact in tf32), lo = x - hi exact; lo's sign is
-                // independent of x's, so the tensor core's truncation of lo adds no bias (a
-                // truncated A = x or an unrounded lo = x - trunc(x) would shrink every amplitude:
-                // a norm decay of ~1e-6 per operator step) -> TMEM row of this thread, block warp / 4
+            {   // A_hi = x itself (the tensor core reads the top 19 bits: tf32 truncation of x),
+                // A_lo = x - trunc_tf32(x) (exact in fp32), pre-rounded by half a tf32 ulp so the
+                // tensor core's truncation of A_lo rounds to nearest -- truncating both parts
+                // would shrink every amplitude (a norm decay of ~1e-6 per operator step)
+                // -> TMEM row of this thread, block warp / 4
                 uint32_t v[32];
 #pragma unroll
                 for (int l = 0; l < 16; ++l) {

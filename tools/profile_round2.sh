@@ -1,7 +1,8 @@
 #!/bin/bash
 # Round-2 evidence run (one gpurun call): full GPU test suite with parity numbers, bench lines for
 # every single-GPU config, the c2 k-sweep, per-pass times, an ncu launch list of the bench command
-# and one ncu --set full capture of the tensor-core pass.   gpurun --timeout 3600 -- 'bash tools/profile_round2.sh'
+# (one ncu per call: the --set full capture of the tensor-core pass is tools/profile_round2_full.sh).
+#   gpurun --timeout 3600 -- 'bash tools/profile_round2.sh gpurun_out/r02'
 cd "${GRAFT_REPO_ROOT:-.}"
 O=${1:-gpurun_out/r02}
 mkdir -p $O
@@ -25,9 +26,5 @@ $N > $O/ncu_plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
       --log-file $O/launches.csv $N > $O/ncu_launches.log 2>&1
 echo "ncu launches rc=$?" >> $O/ncu_launches.log
-$N > $O/ncu_plain2.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k_tc_group_pass -s 20 -c 1 \
-      -o $O/tc_full -f $N > $O/ncu_full.log 2>&1
-echo "ncu full rc=$?" >> $O/ncu_full.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 tail -3 $O/pytest.log; for f in $O/bench_*.json; do echo $f; head -c 300 $f; echo; done

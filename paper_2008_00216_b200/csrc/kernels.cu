@@ -1880,9 +1880,8 @@ static cudaError_t tc_launch(void *state, const uint8_t *dblob, uint32_t pass_of
 cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_t *hrec, uint32_t pass_off, int S,
                                  int n_local, uint32_t rec_bytes, uint32_t tab_entries, int ntcop, cudaStream_t st,
                                  int *kernels) {
-    // 1024-B alignment of the tile ring (SWIZZLE_128B): fixed part rounded up
-    const size_t fixed = ((size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127)) +
-                         1024 /* ring alignment slack */ + sizeof(TcShared);
+    // shared memory (tc_pass.cuh): TcShared region | tile ring | operator slots | scalars | tables
+    const size_t fixed = kTcShBytes + (size_t)ntcop * kTcOpBytes + 512 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127);
     const size_t tile = (size_t)8 << S;
     const uint64_t ntiles = 1ull << (n_local - S);
     const size_t cap = 113 * 1024;   // 2 CTAs per SM
@@ -1892,9 +1891,6 @@ cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_
     static thread_local CUtensorMap tm;
     TcTma tma;
     make_tile_tmap(&tm, &tma, state, (const StvPass *)hrec, n_local);
-    // tile ring: after the operator slots, hashes, scalars and tables, 1024-B aligned
-    tma.ring_off = (uint32_t)(((size_t)ntcop * kTcOpBytes + 1536 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127) +
-                               1023u) & ~(size_t)1023);
     static const int ns_env = getenv("STV_TC_NS") ? atoi(getenv("STV_TC_NS")) : 2;
     const bool two = ns_env >= 2 && fixed + 2 * tile <= cap, full = S == 12;
     cudaError_t e;

@@ -183,6 +183,8 @@ struct alignas(16) TcShared {
     uint32_t tm[48];    // ordinal xor-mask for the same carry
     alignas(16) uint32_t gso[STV_TC_MAX_GROUPS][16];   // per group: swizzled register offsets in bytes
 };
+constexpr uint32_t kTcShBytes = 2048;   // TcShared region at the start of shared memory (1024-multiple)
+static_assert(sizeof(TcShared) <= kTcShBytes, "TcShared exceeds its region");
 
 // One group on the resident tile with tensor-core M steps: thread ctid owns vector ctid.
 // FULL: the tile has 256 vectors (S = 12), every thread is live.  gso: the group's 16
@@ -361,7 +363,7 @@ struct TcTma {
     int32_t L;             // tile low bits: base coordinate = (base | extra) >> L
     int32_t bdim;          // tensor dim of the base coordinate (1, or 2 when L > 4)
     int32_t on;            // 1: TMA staging (else cp.async with the same swizzle)
-    uint32_t ring_off;     // byte offset of the tile ring in dynamic shared memory (multiple of 1024)
+    int32_t pad;
 };
 __device__ __forceinline__ void tma_load_tile(void *dst, const CUtensorMap *tm, uint32_t c1, uint32_t c2,
                                               uint64_t *bar) {
@@ -398,16 +400,16 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     const int ntc = P->ntc, nmop = P->ntcop;
     const uint8_t *mat = rec.b + P->mat_off;
     const uint32_t esz = 8;
-    // shared memory: operator slots (1024-aligned) | hashes | scalars | tables | NS tiles | TcShared
-    uint8_t *opsm = smem;
-    uint8_t *hk = smem + (size_t)nmop * kTcOpBytes;
-    float2 *scal = (float2 *)(hk + 1024);
-    float2 *tables = (float2 *)(hk + 1536);
-    // tile ring 1024-B aligned (TMA SWIZZLE_128B pattern = shared address bits 4..6 ^ 7..9): the
-    // dynamic shared memory starts 1024-aligned (declared) and the host rounds the ring offset
-    float2 *tiles = (float2 *)(smem + tma.ring_off);
-    const uint32_t tile_elems = 1u << S;
-    TcShared *sh = (TcShared *)((uint8_t *)tiles + (size_t)NS * tile_elems * esz);
+    // shared memory: TcShared (kTcShBytes) | NS tiles | operator slots | scalars | tables.
+    // The dynamic shared memory starts 1024-aligned (declared; checked below), so the tile ring
+    // (TMA SWIZZLE_128B pattern = shared address bits 4..6 ^ 7..9) and, for full tiles, every
+    // region sit at compile-time offsets: no address arithmetic to rematerialise in the loops
+    const uint32_t tile_elems = FULL ? 4096u : 1u << S;
+    TcShared *sh = (TcShared *)smem;
+    float2 *tiles = (float2 *)(smem + kTcShBytes);
+    uint8_t *opsm = smem + kTcShBytes + (size_t)NS * tile_elems * esz;
+    float2 *scal = (float2 *)(opsm + (size_t)nmop * kTcOpBytes);   // 512 B: half-table scalars
+    float2 *tables = scal + 64;
     const uint32_t run_bytes = (1u << L) * esz;
     const uint32_t nruns = 1u << h;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

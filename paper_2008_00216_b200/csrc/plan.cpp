@@ -1621,8 +1621,8 @@ static std::vector<GroupTable> split_group_diag(const QForm &f, const std::vecto
 // sub-ops that act identically on every vector of a tile ("foldable": matrices,
 // per-tile variants, CNOTs without a V-bit control, diagonal tables without
 // V-bits) and the rest.  A foldable run whose FMA cost reaches STV_TC_MIN
-// (FFMA2-equivalents per vector; cheaper runs stay on the registers) becomes an
-// M step: one 16 x 16 operator applied with tcgen05.mma.
+// (FFMA2-equivalents per vector, default 150: tools/tcmin_sweep.sh; cheaper runs stay on
+// the registers) becomes an M step: one 16 x 16 operator applied with tcgen05.mma.
 // ---------------------------------------------------------------------------
 static int nth_set_bit(uint64_t m, int i) {
     for (int k = 0; k < 64; ++k)
@@ -1634,7 +1634,7 @@ static int nth_set_bit(uint64_t m, int i) {
 
 static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, const std::vector<StvGroup> &grecs,
                             const std::vector<StvDTab> &tabs) {
-    static const double tc_min = getenv("STV_TC_MIN") ? atof(getenv("STV_TC_MIN")) : 200.0;
+    static const double tc_min = getenv("STV_TC_MIN") ? atof(getenv("STV_TC_MIN")) : 150.0;
     uint32_t bvraw = 0;   // raw tile offset of the current group's vector bit 7 (its TMEM block), or 0
     // 0: varies between the vectors of a block (E step); 1: uniform over the tile; 2: uniform
     // within each block (a per-block operator variant: depends only on vector bit 7)

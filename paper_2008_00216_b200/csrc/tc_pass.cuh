@@ -186,11 +186,14 @@ struct alignas(16) TcShared {
 constexpr uint32_t kTcShBytes = 2048;   // TcShared region at the start of shared memory (1024-multiple)
 static_assert(sizeof(TcShared) <= kTcShBytes, "TcShared exceeds its region");
 
+// the dynamic shared memory of k_tc_group_pass (same storage as its `smem`)
+extern __shared__ __align__(1024) uint8_t tc_smem[];
+
 // One group on the resident tile with tensor-core M steps: thread ctid owns vector ctid.
 // FULL: the tile has 256 vectors (S = 12), every thread is live.  gso: the group's 16
 // register offsets in bytes (shared memory, staged once per CTA).
 template <bool FULL>
-__device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGroup &g, const StvPass *__restrict__ P,
+__device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const StvPass *__restrict__ P,
                                          const StvTcStep *__restrict__ steps, int &s0, const uint8_t *__restrict__ mat,
                                          const float2 *__restrict__ tables, uint64_t full_base, uint32_t tord,
                                          const uint8_t *__restrict__ grec, const float2 *__restrict__ scal,
@@ -225,9 +228,11 @@ __device__ __forceinline__ void tc_group(float2 *__restrict__ tile, const StvGro
         bsw_g ^= flip_delta(0, g.nflip_g);
         bsw_s ^= flip_delta(STV_MAX_FLIPS, g.nflip_s);
     }
-    bsw_g <<= 3;   // bytes
-    bsw_s <<= 3;
-    uint8_t *tb = (uint8_t *)tile;
+    // byte offsets in shared memory: the tile sits at a multiple of its own size, so its offset
+    // combines with the in-tile offsets by xor (one LOP3 + LDS per amplitude)
+    bsw_g = (bsw_g << 3) ^ toff;
+    bsw_s = (bsw_s << 3) ^ toff;
+    uint8_t *tb = tc_smem;
     const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off);
     const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
     const bool pair16 = g.pair16;
@@ -400,14 +405,14 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     const int ntc = P->ntc, nmop = P->ntcop;
     const uint8_t *mat = rec.b + P->mat_off;
     const uint32_t esz = 8;
-    // shared memory: TcShared (kTcShBytes) | NS tiles | operator slots | scalars | tables.
-    // The dynamic shared memory starts 1024-aligned (declared; checked below), so the tile ring
-    // (TMA SWIZZLE_128B pattern = shared address bits 4..6 ^ 7..9) and, for full tiles, every
-    // region sit at compile-time offsets: no address arithmetic to rematerialise in the loops
+    // shared memory: NS tiles | TcShared (kTcShBytes) | operator slots | scalars | tables.
+    // The dynamic shared memory starts 1024-aligned (declared; checked below): the tile ring
+    // (TMA SWIZZLE_128B pattern = shared address bits 4..6 ^ 7..9) starts at 0, each tile at a
+    // multiple of its size, and for full tiles every region sits at a compile-time offset
     const uint32_t tile_elems = FULL ? 4096u : 1u << S;
-    TcShared *sh = (TcShared *)smem;
-    float2 *tiles = (float2 *)(smem + kTcShBytes);
-    uint8_t *opsm = smem + kTcShBytes + (size_t)NS * tile_elems * esz;
+    float2 *tiles = (float2 *)smem;
+    TcShared *sh = (TcShared *)(smem + (size_t)NS * tile_elems * esz);
+    uint8_t *opsm = smem + (size_t)NS * tile_elems * esz + kTcShBytes;
     float2 *scal = (float2 *)(opsm + (size_t)nmop * kTcOpBytes);   // 512 B: half-table scalars
     float2 *tables = scal + 64;
     const uint32_t run_bytes = (1u << L) * esz;
@@ -543,7 +548,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
             for (int o = 0; o < nops; ++o) {
                 const uint32_t w = vw;
                 if (o + 1 < nops) vw = __ldg((const uint32_t *)(grec + groups[o + 1].vtab_off) + tid);
-                tc_group<FULL>(tile, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh,
+                tc_group<FULL>(slot * tile_elems * (uint32_t)esz, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh,
                                sh->gso[o], w, trow, phase, tid);
                 __syncthreads();
             }

@@ -254,8 +254,24 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
         for (int l = 0; l < 16; ++l) x[0][l] = make_float2(0.f, 0.f);
     }
     const uint32_t braw1[1] = {braw};
+    // step records (kind, last, first, n | op | bvar), fetched one step ahead
+    auto fetch = [&](int i, uint2 &w, int &op, int &bv) {
+        w = *(const uint2 *)&steps[i];
+        op = steps[i].op;
+        bv = steps[i].bvar;
+    };
+    uint2 nw;
+    int nop_, nbv;
+    fetch(s0, nw, nop_, nbv);
     for (int s = s0;; ++s) {
-        const StvTcStep st = steps[s];
+        struct { int kind, last, first, n, op, bvar; } st;
+        st.kind = (int16_t)(nw.x & 0xffffu);
+        st.last = (int16_t)(nw.x >> 16);
+        st.first = (int16_t)(nw.y & 0xffffu);
+        st.n = (int16_t)(nw.y >> 16);
+        st.op = nop_;
+        st.bvar = nbv;
+        if (!st.last) fetch(s + 1, nw, nop_, nbv);
         if (st.kind == 0) {
             run_subs<float2, 1>(x, braw1, subs + st.first, st.n, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
         } else {

@@ -478,6 +478,11 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         sh->tm[tid] = tm;
     }
     if (ntab) build_tables<float2, NT>(P, grec, 0, tables, scal, tid, true);   // static table entries
+    bool tile_tabs = false;   // some table has per-tile terms (else nothing to rebuild per tile)
+    {
+        const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
+        for (int t = 0; t < ntab; ++t) tile_tabs |= tabs[t].nterm != 0;
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -533,8 +538,10 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         float2 *tile = tiles + (size_t)slot * tile_elems;
         const uint64_t full_base = base | rank_bits;
         if (NS == 1) issue(tp, 0);
-        if (ntab) build_tables<float2, NT>(P, grec, full_base, tables, scal, tid, false);
-        __syncthreads();   // tables visible (the operator build reads them)
+        if (tile_tabs) {   // tables with per-tile terms: rebuilt, then visible to the operator build
+            build_tables<float2, NT>(P, grec, full_base, tables, scal, tid, false);
+            __syncthreads();
+        }
         // operators whose dependency bits changed: one warp per M step
         for (int s = warp; s < ntc; s += NT / 32) {
             const StvTcStep st = steps[s];

@@ -810,6 +810,19 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
         const StvTerm *tm = (const StvTerm *)((const uint8_t *)P + d.term_off);
         if (d.half) {
             if ((item++ & (NT / 32 - 1)) != warp) continue;
+            if constexpr (sizeof(C) == 8) {   // complex64: 32-bit turns, one REDUX (see below)
+                const StvTerm *gtm = (const StvTerm *)(grec + d.term_off);
+                uint32_t acc = 0;
+                for (int i = lane; i < nterm; i += 32) {
+                    const int qa = __ldg(&gtm[i].a), qb = __ldg(&gtm[i].b);
+                    bool on = (fb >> qb) & 1;
+                    if (qa <= -2) on = on && ((fb >> (-2 - qa)) & 1);
+                    if (on) acc += (uint32_t)((__ldg((const unsigned long long *)&gtm[i].ang) + 0x80000000ull) >> 32);
+                }
+                acc = __reduce_add_sync(0xffffffffu, acc);
+                if (lane == 0) scal[t] = unit_phase<C>((uint64_t)acc << 32);
+                continue;
+            }
             uint64_t lam = 0;                              // constant terms only
             for (int i = lane; i < nterm; i += 32) {
                 const StvTerm q = tm[i];
@@ -827,6 +840,36 @@ __device__ __forceinline__ void build_tables(const StvPass *__restrict__ P, cons
         item += nit;
         if (mine >= nit) continue;
         const uint64_t *stat = (const uint64_t *)(grec + d.stat_off);
+        if constexpr (sizeof(C) == 8) {
+            // complex64 uses the top 32 bits of a phase (unit_phase): the per-tile coefficients
+            // are summed in 32-bit turns (each term rounded to 2^-32 turn, far inside the
+            // complex64 bars), the terms spread over the lanes (device copy of the record) and
+            // reduced per index bit with one REDUX each, instead of every lane scanning all terms
+            const StvTerm *gtm = (const StvTerm *)(grec + d.term_off);
+            uint32_t acc[7] = {0, 0, 0, 0, 0, 0, 0}, accc = 0;
+            for (int i = lane; i < nterm; i += 32) {
+                const int qa = __ldg(&gtm[i].a), qb = __ldg(&gtm[i].b);
+                const uint64_t qang = __ldg((const unsigned long long *)&gtm[i].ang);
+                bool on = (fb >> qb) & 1;
+                if (qa <= -2) on = on && ((fb >> (-2 - qa)) & 1);
+                const uint32_t v = on ? (uint32_t)((qang + 0x80000000ull) >> 32) : 0u;
+#pragma unroll
+                for (int b = 0; b < 7; ++b) acc[b] += qa == b ? v : 0u;
+                accc += qa < 0 ? v : 0u;
+            }
+            uint32_t lb[7];
+#pragma unroll
+            for (int b = 0; b < 7; ++b) lb[b] = __reduce_add_sync(0xffffffffu, acc[b]);
+            const uint32_t cst = __reduce_add_sync(0xffffffffu, accc);
+            for (int e = (mine << 5) | lane; e < ne; e += NT) {
+                uint32_t ph = (uint32_t)((__ldg(stat + e) + 0x80000000ull) >> 32) + cst;
+#pragma unroll
+                for (int b = 0; b < 7; ++b)
+                    if ((e >> b) & 1) ph += lb[b];
+                tables[d.ent_off + (uint32_t)(e >> 4) * STV_TAB_STRIDE + (e & 15)] = unit_phase<C>((uint64_t)ph << 32);
+            }
+            continue;
+        }
         // lane b < 4 + m sums the terms on index bit b, lane 31 the constant
         uint64_t lam = 0;
         for (int i = 0; i < nterm; ++i) {

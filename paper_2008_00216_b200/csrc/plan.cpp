@@ -1096,7 +1096,11 @@ double pass_flops_per_amp(const std::vector<FOp> &ops) {
 // operator step, and the sunk terms become one trailing register (E) step.
 // Returns false (and leaves the group unchanged) when nothing moves.
 static bool sink_v_terms(FOp &grp, uint64_t S) {
-    const uint64_t T = grp.T, V = S & ~T;
+    // terms on a bit outside the tile (the tile base) are per-tile factors of the same kind:
+    // sunk too, the operators of the group stop depending on the tile base (no per-tile
+    // rebuild; QFT groups of c3: H's + their register-register phases = one constant operator)
+    static const bool sink_out = !(getenv("STV_SINK_OUT") && !atoi(getenv("STV_SINK_OUT")));
+    const uint64_t T = grp.T, V = sink_out ? ~T : (S & ~T);
     std::vector<FOp> subs = grp.subs;
     QForm sunk;
     bool moved = false;

@@ -29,3 +29,7 @@ for pi,po in enumerate(offs):
         d=B._at(blob,B.DTab,po+P.tab_off+48*sb.arg)
         s.append('D(m%d,t%d)'%(d.m,d.nterm))
     print('  grp',list(op.tpos),' '.join(s))
+  if P.ntc:
+    for i in range(P.ntc):
+      s=B._at(blob,B.TcStep,po+P.tc_off+32*i)
+      print('    tc step', i, 'grp', s.group, 'M' if s.kind else 'E', 'subs[%d:%d]'%(s.first,s.first+s.n), 'op', s.op, 'dep 0x%x'%s.dep, 'bvar', s.bvar, 'last' if s.last else '')

@@ -1168,8 +1168,9 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
     const size_t tile_b = (size_t)amp_bytes << opt.tile_bits;
     const size_t rec_limit = std::min(kMaxRecBytes, (size_t)STV_REC_PARAM_BYTES);
     // (diagonal-heavy passes, e.g. the QFT of c3, trade the third CTA for full-size tiles:
-    // a 16 KB table area measured best on c3, 306 vs 506 ms/circuit at 8 KB)
-    size_t tab_limit = 16 * 1024;
+    // a 16 KB table area measured best on c3, 306 vs 506 ms/circuit at 8 KB; 24 KB once the
+    // per-tile table build spread its terms over the lanes: 7 passes instead of 9, 242 -> 229 ms)
+    size_t tab_limit = 24 * 1024;
     if (const char *e = getenv("STV_TAB_LIMIT")) tab_limit = (size_t)atoi(e);
 
     while (true) {
@@ -1655,7 +1656,10 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
         return 1;
     };
     auto foldable = [&](const StvSub &x) { return fold_kind(x) != 0; };
-    auto cost = [&](const StvSub &x) -> double {   // FFMA2-equivalents per 16-amplitude vector
+    // per sub-op dispatch on the registers (uniform branch, operand loads): long runs of cheap
+    // sub-ops (the QFT's Hadamards between half tables, c3) cost more than their arithmetic
+    static const double dispatch_cost = getenv("STV_TC_SUBOP") ? atof(getenv("STV_TC_SUBOP")) : 8.0;
+    auto arith = [&](const StvSub &x) -> double {   // FFMA2-equivalents per 16-amplitude vector
         const int c = x.code & 0xff;
         if (c < SUBC_U2) return 32;
         if (c < SUBC_CNOT) return 128;
@@ -1667,6 +1671,7 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
         if (c < SUBC_U2R) return 16;
         return 64;
     };
+    auto cost = [&](const StvSub &x) -> double { return dispatch_cost + arith(x); };
     auto sel_bits = [&](uint32_t w, uint64_t &dep) {   // 3 x 5-bit tile-ordinal selectors
         for (int i = 0; i < 3; ++i) {
             const uint32_t sl = (w >> (5 * i)) & 31u;

@@ -168,3 +168,34 @@ def test_c4_shards_agree_mirror_norm(stv):
     record("c4_c64_mirror", n=n, amp0_sq=abs(a0[0]) ** 2, norm=res[0][1])
     assert abs(res[0][1] - 1) < 1e-4
     assert abs(a0[0]) ** 2 >= 1 - 1e-5 and abs(a0[1]) < 1e-4 and abs(a0[2]) < 1e-4
+
+
+def test_c5_proxy_weak34_g3(stv):
+    """c5 (n=37, 1 TiB over 8 GPUs with 3 global qubits) does not fit one B200.  Its proxy:
+    the weak-ladder circuit at n=34 (same 6x6 grid family, gate set and seed as c5's ladder,
+    inputs.circuits.weak_ladder) run with g=3 virtual shards -- the 8-shard partition c5 uses,
+    every remap through the pack -> exchange -> unpack schedule -- against the unsharded run
+    on 2^24 sampled amplitudes (2e-6, F >= 1 - 1e-5 over the sample)."""
+    if not _big_gpu((8 << 34) + (4 << 30)):
+        pytest.skip("needs a 180 GB B200 (128 GiB state)")
+    circ = C.weak_ladder(34)
+    n = circ.n
+    rng = np.random.default_rng(5)
+    y = np.unique(rng.integers(0, 1 << n, size=1 << 24, dtype=np.uint64))
+    res = {}
+    for g in (0, 3):
+        st = stv.State(n, "c64", virtual_g=g) if g else stv.State(n, "c64")
+        st.set_basis(0)
+        st.apply(circ.gates)
+        res[g] = (st.amplitudes(y), st.norm(), st.stats())
+        st.close()
+        del st
+        _free()
+    base, sh = res[0][0], res[3][0]
+    d = float(np.max(np.abs(sh - base)))
+    fid = abs(np.vdot(base, sh)) ** 2 / (np.vdot(base, base).real * np.vdot(sh, sh).real)
+    record("c5_proxy_weak34_virtual_g3_vs_G1", n=n, sampled=int(y.size), max_abs=d, fidelity_sampled=fid,
+           norm=res[3][1], remaps=res[3][2]["n_pass"]["remap"])
+    assert d <= 2e-6 and fid >= 1 - 1e-5
+    assert res[3][2]["n_pass"]["remap"] > 0
+    assert abs(res[3][1] - 1) < 1e-4

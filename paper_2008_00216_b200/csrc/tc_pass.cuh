@@ -552,10 +552,10 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
             const StvSub *subs = (const StvSub *)((const uint8_t *)P + g.sub_off) + st.first;
             tc_build_op(subs, st.n, mat, (const StvDTab *)((const uint8_t *)P + P->tab_off), tables, full_base, tord,
                         rank_bits, scal, opsm + (size_t)st.op * kTcOpBytes, st.bvar ? g.vbit[7][0] : 0u, lane);
+            fence_proxy_async();   // this lane's operator stores (generic proxy) -> tensor-core reads
             __syncwarp();
             if (lane == 0) sh->key[st.op] = key;
         }
-        fence_proxy_async();   // operator slots (generic-proxy stores) -> tensor-core reads
         if (NS == 2) {
             issue(tp + 1, slot ^ 1);   // the other slot was freed by the previous iteration's last barrier
             if (use_tma) wait_tile(slot);

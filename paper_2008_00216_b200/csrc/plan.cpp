@@ -1658,7 +1658,7 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
     auto foldable = [&](const StvSub &x) { return fold_kind(x) != 0; };
     // per sub-op dispatch on the registers (uniform branch, operand loads): long runs of cheap
     // sub-ops (the QFT's Hadamards between half tables, c3) cost more than their arithmetic
-    static const double dispatch_cost = getenv("STV_TC_SUBOP") ? atof(getenv("STV_TC_SUBOP")) : 8.0;
+    static const double dispatch_cost = getenv("STV_TC_SUBOP") ? atof(getenv("STV_TC_SUBOP")) : 16.0;
     auto arith = [&](const StvSub &x) -> double {   // FFMA2-equivalents per 16-amplitude vector
         const int c = x.code & 0xff;
         if (c < SUBC_U2) return 32;

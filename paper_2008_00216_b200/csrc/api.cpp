@@ -382,7 +382,7 @@ sv_status sv_apply_circuit(sv_state *s, const sv_gate *gates, size_t ng, const s
         for (int v = 0; v < 64; ++v) sigma[v] = v;
         sv_state::PlanEntry ne;
         try {
-            ne.plan = build_plan(s->n, s->n_global, (int)s->esz(), pg, po, sigma);
+            ne.plan = plan_auto(s->n, s->n_global, (int)s->esz(), pg, po, sigma);
         } catch (const std::exception &ex) {
             return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
         }
@@ -734,7 +734,7 @@ sv_status sv_plan_json(int n, int n_global, sv_dtype dt, const sv_gate *gates, s
     for (int v = 0; v < 64; ++v) sigma[v] = v;
     Plan plan;
     try {
-        plan = build_plan(n, n_global, esz, pg, po, sigma);
+        plan = plan_auto(n, n_global, esz, pg, po, sigma);
     } catch (const std::exception &ex) {
         return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
     }
@@ -765,7 +765,7 @@ sv_status sv_plan_blob(int n, int n_global, sv_dtype dt, const sv_gate *gates, s
     for (int v = 0; v < 64; ++v) sigma[v] = v;
     Plan plan;
     try {
-        plan = build_plan(n, n_global, esz, pg, po, sigma);
+        plan = plan_auto(n, n_global, esz, pg, po, sigma);
     } catch (const std::exception &ex) {
         return fail(SV_ERR_INVALID_ARG, std::string("planner: ") + ex.what());
     }

@@ -378,7 +378,7 @@ PlanOptions resolve_options(const sv_options *o, int amp_bytes, int n_local) {
     if (o) {
         if (o->kmax > 0) p.kmax = std::min(o->kmax, STV_MAX_K);
         if (o->tile_bits > 0) p.tile_bits = std::min(o->tile_bits, STV_MAX_TILE_BITS);
-        if (o->low_bits > 0) p.low_bits = o->low_bits;
+        if (o->low_bits > 0) { p.low_bits = o->low_bits; p.low_auto = false; }
         if (o->budget > 0) p.budget = o->budget;
         p.flags = o->flags;
     }
@@ -2303,6 +2303,46 @@ std::string plan_to_json(const Plan &p) {
     for (int q = 0; q < p.n; ++q) o << (q ? "," : "") << p.frame_out.perm[q];
     o << "],\"xmask\":\"" << p.frame_out.xmask << "\"}";
     return o.str();
+}
+
+
+// Estimated cost of an encoded plan in units of one gate-group round on the resident tile
+// (measured on one B200, c2/c3/c4 low-bits sweep): every group, operator
+// (M) step and register (E) step costs about the same (~0.8 ms per 2^30 amplitudes); a
+// pass adds ~0.3 of that on top (its copy overlaps the compute).
+static double encoded_cost(const Encoded &e) {
+    double c = 0;
+    for (uint32_t off : e.pass_off) {
+        const StvPass *P = (const StvPass *)&e.blob[off];
+        c += 0.3 + (P->grouped ? P->nops : 1) + P->ntc;
+    }
+    return c;
+}
+
+Plan plan_auto(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg, const PlanOptions &opt,
+               int *sigma) {
+    static const bool off = getenv("STV_NO_AUTO_LOW") && atoi(getenv("STV_NO_AUTO_LOW"));
+    const int nl = n - n_global;
+    const bool tc = amp_bytes == 8 && !(opt.flags & (SV_OPT_NO_TC | SV_OPT_NO_GROUPS | SV_OPT_ONE_GATE));
+    if (off || !opt.low_auto || !tc || opt.tile_bits != 12 || nl < 20) return build_plan(n, n_global, amp_bytes, pg, opt, sigma);
+    int best_sigma[64];
+    Plan best;
+    double best_cost = 0;
+    for (int L : {4, 5}) {
+        PlanOptions o = opt;
+        o.low_bits = L;
+        int sg[64];
+        std::memcpy(sg, sigma, sizeof(sg));
+        Plan p = build_plan(n, n_global, amp_bytes, pg, o, sg);
+        const double c = encoded_cost(encode(p, nl, false, 0));
+        if (L == 4 || c < best_cost) {
+            best = std::move(p);
+            best_cost = c;
+            std::memcpy(best_sigma, sg, sizeof(best_sigma));
+        }
+    }
+    std::memcpy(sigma, best_sigma, sizeof(best_sigma));
+    return best;
 }
 
 }  // namespace stv

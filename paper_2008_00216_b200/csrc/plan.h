@@ -99,6 +99,7 @@ struct PlanOptions {
     int low_bits = 4;
     int budget = 1000;
     uint32_t flags = 0;
+    bool low_auto = true;     // low_bits not given: plan_auto picks it (complex64 tensor-core plans)
 };
 
 struct Plan {
@@ -122,6 +123,12 @@ Plan build_plan(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg
                 const PlanOptions &opt, int *sigma);
 
 PlanOptions resolve_options(const sv_options *o, int amp_bytes, int n_local);
+
+// build_plan with the tile's contiguous low run chosen per circuit when the caller left it
+// open: complex64 tensor-core plans are built for low_bits 4 and 5 and the one with the
+// smaller estimated cost (register rounds + operator steps + passes) is kept.
+Plan plan_auto(int n, int n_global, int amp_bytes, const std::vector<PGate> &pg, const PlanOptions &opt,
+               int *sigma);
 
 // Encode passes into a device blob for the kernels (pass_format.h).
 // rank_bits: value of the global bits (actual positions >= n_local) of this rank.

@@ -1,11 +1,14 @@
 #!/bin/bash
-# A/B timings: bash tools/ab_env.sh "<cfg> <ENV=..> ..." ...  (each arg: config then env assignments)
+# A/B timings: bash tools/ab_env.sh "<cfg> [ENV=..] [--bench-arg ..]" ...
+# each spec: a config, environment assignments, then bench.py arguments
 cd "${GRAFT_REPO_ROOT:-.}"
 for spec in "$@"; do
   set -- $spec
   cfg=$1; shift
-  echo "== $cfg $*"
-  env "$@" python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>&1 | python -c "
+  envs=(); args=()
+  for a in "$@"; do if [[ $a == *=* && $a != --* ]]; then envs+=("$a"); else args+=("$a"); fi; done
+  echo "== $cfg ${envs[*]} ${args[*]}"
+  env "${envs[@]}" python bench.py --config $cfg --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 "${args[@]}" 2>&1 | python -c "
 import sys,json
 for l in sys.stdin:
     if l.startswith('{'):

@@ -1626,7 +1626,7 @@ static std::vector<GroupTable> split_group_diag(const QForm &f, const std::vecto
 // sub-ops that act identically on every vector of a tile ("foldable": matrices,
 // per-tile variants, CNOTs without a V-bit control, diagonal tables without
 // V-bits) and the rest.  A foldable run whose FMA cost reaches STV_TC_MIN
-// (FFMA2-equivalents per vector, default 150: tools/tcmin_sweep.sh; cheaper runs stay on
+// (FFMA2-equivalents per vector, default 150: STV_TC_MIN sweeps with tools/ab_env.sh; cheaper runs stay on
 // the registers) becomes an M step: one 16 x 16 operator applied with tcgen05.mma.
 // ---------------------------------------------------------------------------
 static int nth_set_bit(uint64_t m, int i) {

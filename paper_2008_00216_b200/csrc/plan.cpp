@@ -2166,7 +2166,13 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                 }
                 hd.nops = (int)grecs.size();
                 std::memcpy(&b[ops_at], grecs.data(), grecs.size() * sizeof(StvGroup));
-                if (!c128 && !(p.flags & SV_OPT_NO_TC) && hd.S <= 12) encode_tc_steps(b, at, hd, grecs, tabs);
+                // tensor-core steps on full 4096-amplitude tiles only: a smaller tile leaves most of
+                // the 256 threads (one per 16-amplitude vector) idle, and the CUDA-core pass is
+                // faster there (c1, n = 16: 0.38 vs 0.45 ms); STV_TC_SMALL=1 keeps the tensor-core
+                // pass for tiles of < 12 bits too (tests)
+                static const bool tc_small = getenv("STV_TC_SMALL") && atoi(getenv("STV_TC_SMALL"));
+                if (!c128 && !(p.flags & SV_OPT_NO_TC) && (hd.S == 12 || (tc_small && hd.S < 12)))
+                    encode_tc_steps(b, at, hd, grecs, tabs);
             }
             else std::memcpy(&b[ops_at], recs.data(), recs.size() * sizeof(StvOp));
             (void)esz;

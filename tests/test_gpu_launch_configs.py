@@ -48,3 +48,18 @@ def test_group_pass_launch_config_parity(cfg):
     assert p.returncode == 0, p.stderr[-2000:]
     for max_abs, fid in json.loads(p.stdout.strip().splitlines()[-1]):
         assert max_abs <= 2e-6 and fid >= 1 - 1e-5, (cfg, max_abs, fid)
+
+
+def test_tc_pass_small_tiles_parity():
+    """STV_TC_SMALL=1: the tensor-core pass also on tiles of fewer than 12 bits (by default
+    those run on the CUDA-core pass): its non-full-tile variant (threads beyond the tile's
+    vectors idle) against the oracle on the small circuits above."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, STV_TC_SMALL="1")
+    p = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], env=env, capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    for max_abs, fid in json.loads(p.stdout.strip().splitlines()[-1]):
+        assert max_abs <= 2e-6 and fid >= 1 - 1e-5, (max_abs, fid)

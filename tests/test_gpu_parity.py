@@ -305,7 +305,7 @@ def test_tc_block_variants_parity(stv, dims):
 def test_tma_staged_tc_pass_parity(stv, cfg):
     """Tensor-core passes staged with TMA tensor copies (SV_OPT_TMA: 5-D tensor map with an
     overlapping tile-base dim, SWIZZLE_128B tile layout, looped boxes) against the oracle."""
-    circ = C.config(cfg) if cfg == 1 else C.grid_circuit("g", 4, 6, 0, 12, "fsim", 21)
+    circ = C.grid_circuit("g", 4, 5, 0, 12, "fsim", 20) if cfg == 1 else C.grid_circuit("g", 4, 6, 0, 12, "fsim", 21)
     ref = oracle.run(circ)
     a, st = run_gpu(stv, circ, "c64", flags=stv.OPT_TMA)
     assert st["n_tc_pass"] > 0

@@ -349,14 +349,21 @@ def test_flip_targets_are_register_bits(seed, tile_bits):
     assert seen > 0
 
 
-@pytest.mark.parametrize("case", ["c1", "c2", "c4", "rand"])
+@pytest.mark.parametrize("case", ["grid20", "c2", "c4", "rand"])
 def test_tc_step_plan_structure(case):
     """Tensor-core step plans (pass_format.h StvTcStep): per group the steps cover its sub-op
     program in order without gaps; M steps hold only sub-ops that act the same on every
     vector of a tile (no V-bit tables, no V-bit-controlled CNOTs) and own distinct operator
     slots; the dependency masks contain every per-tile selector bit; tperm permutes the tile
     ordinal bits with the dependency bits on top."""
-    circ = C.random_circuit(20, 400, 11) if case == "rand" else C.config(int(case[1:]))
+    # (tensor-core steps need full 12-bit tiles: c1's n = 16 plans 8-bit tiles on the CUDA-core
+    # pass, so its 4x4-grid shape is taken at 4x5 = 20 qubits here)
+    if case == "rand":
+        circ = C.random_circuit(20, 400, 11)
+    elif case == "grid20":
+        circ = C.grid_circuit("g", 4, 5, 0, 20, "cz", 1)
+    else:
+        circ = C.config(int(case[1:]))
     blob, offs = stv.plan_blob(circ.n, circ.gates)
     npass = 0
     for po in offs:

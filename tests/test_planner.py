@@ -416,3 +416,22 @@ def test_tc_step_plan_structure(case):
         dep_ord = [i for i, b in enumerate(out_bits) if (dep >> b) & 1]
         assert sorted(perm[nord - len(dep_ord):]) == dep_ord
     assert npass > 0
+
+
+@pytest.mark.parametrize("case", ["qft20", "rand20"])
+def test_auto_low_run_full_tile_blob_semantics(case):
+    """Full 12-bit tiles at n = 20: the tensor-core step encoding, tile-base terms sunk to the
+    end of groups, and plan_auto's choice of the tile's low run (these circuits pick L = 5
+    over L = 4; an explicit low_bits is kept).  The exact device blob, emulated on CPU,
+    reproduces the oracle (complex64 bar 2e-6)."""
+    circ = C.qft_circuit(20, tail=100, seed=3) if case == "qft20" else C.random_circuit(20, 300, 3)
+    blob, offs = stv.plan_blob(circ.n, circ.gates)
+    Ls = [BE._at(blob, BE.Pass, po).L for po in offs]
+    assert 5 in Ls and 4 not in Ls[:1]
+    assert any(BE._at(blob, BE.Pass, po).ntc for po in offs)
+    blob4, offs4 = stv.plan_blob(circ.n, circ.gates, low_bits=4)   # explicit: no automatic choice
+    assert bytes(blob4) != bytes(blob)
+    plan = stv.plan_json(circ.n, circ.gates)
+    psi = PI.logical(plan, BE.run(circ.n, blob, offs, x0=circ.x0, c128=False))
+    ref = oracle.run(circ)
+    assert np.max(np.abs(psi - ref)) < 2e-6

@@ -198,7 +198,10 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
                                          const float2 *__restrict__ tables, uint64_t full_base, uint32_t tord,
                                          const uint8_t *__restrict__ grec, const float2 *__restrict__ scal,
                                          const uint8_t *__restrict__ opsm, TcShared *sh, const uint32_t *gso,
-                                         uint32_t vw, uint32_t trow, uint32_t &phase, int ctid) {
+                                         uint32_t vw, uint32_t trow, uint32_t &phase, int ctid, int dbg) {
+#ifndef STV_TC_DEBUG
+    dbg = 0;   // timing ablations (STV_TILE_DEBUG bits 4..64, profiles/r02_tc_ablation.md) need -DSTV_TC_DEBUG
+#endif
     const int nvb = g.nvb;
     const uint32_t nvec = 1u << nvb;
     const bool live = FULL || (uint32_t)ctid < nvec;
@@ -237,7 +240,7 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
     const StvDTab *tabs = (const StvDTab *)((const uint8_t *)P + P->tab_off);
     const bool pair16 = g.pair16;
     float2 x[1][16];
-    if (live) {
+    if (live && !(dbg & 16)) {
         if (pair16) {
 #pragma unroll
             for (int l = 0; l < 16; l += 2) {
@@ -273,6 +276,7 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
         st.bvar = nbv;
         if (!st.last) fetch(s + 1, nw, nop_, nbv);
         if (st.kind == 0) {
+            if (!(dbg & 32))
             run_subs<float2, 1>(x, braw1, subs + st.first, st.n, mat, tabs, tables, full_base, tord, P->rank_bits, scal);
         } else {
             {   // A_hi = x itself (the tensor core reads the top 19 bits: tf32 truncation of x),
@@ -286,7 +290,8 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
                     v[2 * l] = __float_as_uint(x[0][l].x);
                     v[2 * l + 1] = __float_as_uint(x[0][l].y);
                 }
-                tmem_st32(trow, v);
+                if (!(dbg & 64)) tmem_st32(trow, v);
+                if (!(dbg & 8))
 #pragma unroll
                 for (int l = 0; l < 16; ++l) {
                     const float2 t = make_float2(__uint_as_float(v[2 * l] & 0xffffe000u),
@@ -295,14 +300,14 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
                     v[2 * l] = __float_as_uint(lo.x) + 0x1000u;
                     v[2 * l + 1] = __float_as_uint(lo.y) + 0x1000u;
                 }
-                tmem_st32(trow + 32, v);
+                if (!(dbg & 64)) tmem_st32(trow + 32, v);
             }
             tc_wait_st();
             tc_fence_before();
             // each half of the CTA (warps 0-3: block 0, warps 4-7: block 1) syncs and issues its own MMAs
             const int half = ctid >> 7;
             asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
-            if ((ctid & 127) < 32) {   // the half's first warp, converged: one elected lane issues
+            if ((ctid & 127) < 32 && !(dbg & 4)) {   // the half's first warp, converged: one elected lane issues
                 tc_fence_after();
                 // warp-uniform operands (shfl from lane 0) so ptxas keeps them in uniform registers
                 const uint32_t tmh = __shfl_sync(~0u, trow, 0);   // warp 4 half: lane 0, block half
@@ -313,12 +318,14 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
                 }
                 __syncwarp();
             }
-            mbar_wait_spin(&sh->bar[half], phase);
-            phase ^= 1u;
+            if (!(dbg & 4)) {
+                mbar_wait_spin(&sh->bar[half], phase);
+                phase ^= 1u;
+            }
             tc_fence_after();
             {
                 uint32_t v[32];
-                tmem_ld32(trow + 64, v);
+                if (!(dbg & 64)) tmem_ld32(trow + 64, v);
                 tc_wait_ld();
 #pragma unroll
                 for (int l = 0; l < 16; ++l) x[0][l] = make_float2(__uint_as_float(v[2 * l]), __uint_as_float(v[2 * l + 1]));
@@ -329,7 +336,7 @@ __device__ __forceinline__ void tc_group(uint32_t toff, const StvGroup &g, const
             break;
         }
     }
-    if (live) {
+    if (live && !(dbg & 16)) {
         if (pair16) {
 #pragma unroll
             for (int l = 0; l < 16; l += 2)
@@ -538,7 +545,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
         float2 *tile = tiles + (size_t)slot * tile_elems;
         const uint64_t full_base = base | rank_bits;
         if (NS == 1) issue(tp, 0);
-        if (tile_tabs) {   // tables with per-tile terms: rebuilt, then visible to the operator build
+        if (tile_tabs && !(dbg_flags & 128)) {   // tables with per-tile terms (bit 7: ablation): rebuilt, then visible to the operator build
             build_tables<float2, NT>(P, grec, full_base, tables, scal, tid, false);
             __syncthreads();
         }
@@ -572,7 +579,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
                 const uint32_t w = vw;
                 if (o + 1 < nops) vw = __ldg((const uint32_t *)(grec + groups[o + 1].vtab_off) + tid);
                 tc_group<FULL>(slot * tile_elems * (uint32_t)esz, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh,
-                               sh->gso[o], w, trow, phase, tid);
+                               sh->gso[o], w, trow, phase, tid, dbg_flags);
                 __syncthreads();
             }
         }

@@ -66,6 +66,27 @@ def test_planner_options(stv, kw, dtype):
     assert_parity(psi, oracle.run(circ), dtype)
 
 
+@pytest.mark.parametrize("n,seed", [(20, 9), (21, 12), (22, 10)])
+def test_random_circuits_all_kinds_tc(stv, n, seed):
+    """Random circuits of every gate kind at n >= 20, where complex64 passes have full 12-bit
+    tiles and run on the tensor-core kernel (smaller states run on the CUDA-core pass)."""
+    circ = C.random_circuit(n, 250, seed)
+    psi, st = run_gpu(stv, circ, "c64")
+    assert st["n_tc_pass"] > 0
+    assert_parity(psi, oracle.run(circ), "c64")
+
+
+@pytest.mark.parametrize("kw", [dict(kmax=1), dict(kmax=2), dict(kmax=3), dict(low_bits=5), dict(low_bits=7),
+                                dict(budget=400), dict(flags=2), dict(flags=4), dict(flags=16),
+                                dict(flags=128), dict(flags=0x400), dict(flags=0x800)])
+def test_planner_options_tc(stv, kw):
+    """The planner options on the tensor-core path (n = 20: full 12-bit tiles, complex64)."""
+    circ = C.random_circuit(20, 300, 43)
+    psi, st = run_gpu(stv, circ, "c64", **kw)
+    assert st["n_tc_pass"] > 0
+    assert_parity(psi, oracle.run(circ), "c64")
+
+
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_c1_config(stv, dtype):
     circ = C.config(1)

@@ -63,6 +63,8 @@ def lib():
                                  ctypes.POINTER(_Gate), ctypes.c_int64, ctypes.c_int]
         L.oracle_apply.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(_Gate),
                                    ctypes.c_int64, ctypes.c_int]
+        L.oracle_run_c64store.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p,
+                                          ctypes.POINTER(_Gate), ctypes.c_int64, ctypes.c_int]
         L.oracle_norm.argtypes = [ctypes.c_int, ctypes.c_void_p]
         L.oracle_norm.restype = ctypes.c_double
         _lib = L
@@ -139,6 +141,20 @@ def run(circuit, nthreads: int = 0, gates=None, x0=None) -> np.ndarray:
     psi = np.empty(1 << n, dtype=np.complex128)
     arr, keep = _marshal(gates)
     rc = lib().oracle_run(n, x0, psi.ctypes.data, arr, len(gates), nthreads)
+    if rc != 0:
+        raise ValueError(f"oracle: rc={rc}")
+    return psi
+
+
+def run_c64store(circuit, nthreads: int = 0) -> np.ndarray:
+    """Level 1 with complex64 storage (reading A19): psi = U_G ... U_1 e_{x0}, each
+    gate computed in complex128 from the stored amplitudes and rounded to complex64 when stored --
+    the full-state oracle for states whose complex128 form exceeds host memory (c4, n = 34:
+    128 GiB).  Pinned against run() in tests/test_oracle.py."""
+    n = circuit.n
+    psi = np.empty(1 << n, dtype=np.complex64)
+    arr, keep = _marshal(circuit.gates)
+    rc = lib().oracle_run_c64store(n, circuit.x0, psi.ctypes.data, arr, len(circuit.gates), nthreads)
     if rc != 0:
         raise ValueError(f"oracle: rc={rc}")
     return psi

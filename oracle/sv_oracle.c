@@ -111,8 +111,20 @@ int oracle_gate_matrix(int kind, int adjoint, double theta, double phi,
     return d;
 }
 
+/* Amplitude storage: complex128 (the oracle proper), or complex64 storage with every gate
+ * computed in complex128 and rounded once when stored (reading A19: the only way
+ * the 2^34-amplitude c4 state fits the GPU box's host memory, 128 GiB instead of 256 GiB). */
+typedef float complex cplx32;
+static inline cplx ld_amp(const void *psi, int c64, uint64_t j) {
+    return c64 ? (cplx)((const cplx32 *)psi)[j] : ((const cplx *)psi)[j];
+}
+static inline void st_amp(void *psi, int c64, uint64_t j, cplx z) {
+    if (c64) ((cplx32 *)psi)[j] = (cplx32)z;
+    else ((cplx *)psi)[j] = z;
+}
+
 /* Apply one gate in place: PAPER.md L236-241 ("set id" iteration). */
-static int apply_gate(int n, cplx *psi, const og_gate *g) {
+static int apply_gate(int n, void *psi, int c64, const og_gate *g) {
     int q = oracle_nqubits_of(g->kind);
     int tq[2] = {g->q0, g->q1};
     double Ud[32];
@@ -141,12 +153,12 @@ static int apply_gate(int n, cplx *psi, const og_gate *g) {
             for (int i = 0; i < q; ++i)      /* first-listed qubit = MSB of l */
                 j |= (uint64_t)((l >> (q - 1 - i)) & 1) << tq[i];
             idx[l] = j;
-            v[l] = psi[j];
+            v[l] = ld_amp(psi, c64, j);
         }
         for (int r = 0; r < d; ++r) {
             cplx acc = 0;
             for (int c = 0; c < d; ++c) acc += U[r * d + c] * v[c];
-            psi[idx[r]] = acc;
+            st_amp(psi, c64, idx[r], acc);
         }
     }
     return 0;
@@ -159,9 +171,25 @@ int oracle_apply(int n, double *psi_ri, const og_gate *gates, int64_t ng, int nt
 #else
     (void)nthreads;
 #endif
-    cplx *psi = (cplx *)psi_ri;
     for (int64_t i = 0; i < ng; ++i)
-        if (apply_gate(n, psi, &gates[i]) != 0) return (int)(-(1 + i));
+        if (apply_gate(n, psi_ri, 0, &gates[i]) != 0) return (int)(-(1 + i));
+    return 0;
+}
+
+/* Reading A19: psi (2*2^n floats, complex64 storage) <- e_{x0}, then every gate computed in
+ * complex128 from the stored amplitudes and rounded to complex64 when stored. */
+int oracle_run_c64store(int n, uint64_t x0, float *psi_ri, const og_gate *gates, int64_t ng, int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    const uint64_t N = 1ull << n;
+    if (x0 >= N) return -1000000;
+    memset(psi_ri, 0, sizeof(float) * 2 * N);
+    psi_ri[2 * x0] = 1.0f;
+    for (int64_t i = 0; i < ng; ++i)
+        if (apply_gate(n, psi_ri, 1, &gates[i]) != 0) return (int)(-(1 + i));
     return 0;
 }
 

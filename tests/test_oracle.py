@@ -354,3 +354,31 @@ def test_qft_basis_amplitudes_vs_run(n):
     psi = oracle.run(circ)
     got = oracle.qft_basis_amplitudes(n, circ.x0, np.arange(1 << n))
     assert close(got, psi, 1e-12)
+
+
+# --------------------------------------------------------------------------
+# complex64-storage mode (reading A19: the full-state c4 oracle, 128 GiB)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [3, 10])
+def test_c64store_closed_forms(n):
+    """H^n|0> is uniform and the QFT of a basis state is 2^{-n/2} e^{2 pi i x y / 2^n} (A7),
+    to complex64 rounding (each gate rounded once when stored)."""
+    h = oracle.run_c64store(C.Circuit("hn", n, [("h", (q,), ()) for q in range(n)]))
+    assert h.dtype == np.complex64
+    assert close(h, np.full(1 << n, 2 ** (-n / 2)), 1e-7)
+    circ = C.qft_circuit(n, tail=0, seed=3)
+    y = np.arange(1 << n)
+    ref = 2 ** (-n / 2) * np.exp(2j * np.pi * ((circ.x0 * y) % (1 << n)) / (1 << n))
+    assert close(oracle.run_c64store(circ), ref, 1e-6)
+
+
+@pytest.mark.parametrize("n,seed", [(9, 1), (12, 2)])
+def test_c64store_vs_run_and_grid(n, seed):
+    """Random circuits of every gate kind and the c4-shaped grid circuit at small size: the
+    complex64-storage run stays within complex64 rounding of the complex128 oracle
+    (per-gate rounding ~2^-24 relative, random-walk accumulated) and keeps the norm."""
+    for circ in (C.random_circuit(n, 300, seed), C.grid_circuit("g", 3, 4, 0, 14, "fsim", seed)):
+        a = oracle.run_c64store(circ)
+        b = oracle.run(circ)
+        assert np.max(np.abs(a.astype(np.complex128) - b)) < 2e-6
+        assert abs(np.vdot(a, a).real - 1) < 1e-5

@@ -1,0 +1,55 @@
+"""One-off full-state c4 parity (n=34, 128 GiB complex64 on one B200): the GPU state against
+the oracle run gate by gate with complex64 storage and complex128 arithmetic per gate
+(oracle.run_c64store, reading A19: the complex128 oracle state, 256 GiB, exceeds the
+box's host memory).  The GPU state is compared on 2^28 uniformly sampled amplitudes (the full
+GPU state does not fit host memory next to the oracle's).  ~30-40 min on 16 host cores: too
+slow for the round-end test budget, so its result is committed in profiles/.
+    python tools/c4_full_oracle.py [out.json]"""
+import gc
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2008_00216_b200 as stv  # noqa: E402
+from inputs import circuits as C  # noqa: E402
+
+circ = C.config(4)
+rng = np.random.default_rng(34)
+y = np.unique(rng.integers(0, 1 << circ.n, size=1 << 28, dtype=np.uint64))
+st = stv.State(circ.n, "c64")
+st.set_basis(circ.x0)
+st.apply(circ.gates)
+stats = st.stats()
+a = st.amplitudes(y)                       # logical order
+norm = st.norm()
+st.close()
+del st
+import torch  # noqa: E402
+gc.collect()
+torch.cuda.empty_cache()
+t0 = time.perf_counter()
+ref = oracle.run_c64store(circ)            # complex64 storage, 128 GiB
+t_or = time.perf_counter() - t0
+b = ref[y.astype(np.int64)].astype(np.complex128)
+onorm = float(np.vdot(ref[: 1 << 30], ref[: 1 << 30]).real)
+for k in range(1, 16):
+    blk = ref[k << 30:(k + 1) << 30]
+    onorm += float(np.vdot(blk, blk).real)
+del ref
+gc.collect()
+a = a.astype(np.complex128)
+d = float(np.max(np.abs(a - b)))
+fid = abs(np.vdot(b, a)) ** 2 / (np.vdot(a, a).real * np.vdot(b, b).real)
+line = {"test": "c4_c64_full_oracle_c64store", "n": circ.n, "gates": len(circ.gates), "sampled": int(y.size),
+        "max_abs": d, "fidelity_sampled": float(fid), "norm_gpu": norm, "norm_oracle": onorm, "oracle_s": t_or,
+        "cores": len(os.sched_getaffinity(0)), "passes": stats["n_pass"], "run_ms": stats["run_ms"],
+        "bars": {"max_abs": 2e-6, "fidelity": 1 - 1e-5},
+        "pass": bool(d <= 2e-6 and fid >= 1 - 1e-5)}
+print("PARITY", json.dumps(line), flush=True)
+if len(sys.argv) > 1:
+    json.dump(line, open(sys.argv[1], "w"), indent=1)

@@ -111,58 +111,54 @@ int oracle_gate_matrix(int kind, int adjoint, double theta, double phi,
     return d;
 }
 
-/* Amplitude storage: complex128 (the oracle proper), or complex64 storage with every gate
- * computed in complex128 and rounded once when stored (reading A19: the only way
- * the 2^34-amplitude c4 state fits the GPU box's host memory, 128 GiB instead of 256 GiB). */
+/* Apply one gate in place: PAPER.md L236-241 ("set id" iteration).  AMP is the amplitude
+ * storage type: complex128 (the oracle proper), or complex64 with every gate computed in
+ * complex128 from the stored amplitudes and rounded once when stored (reading A19:
+ * the only way the 2^34-amplitude c4 state fits the GPU box's host memory).  One definition,
+ * instantiated per storage type so each loop is compiled for its own loads and stores. */
 typedef float complex cplx32;
-static inline cplx ld_amp(const void *psi, int c64, uint64_t j) {
-    return c64 ? (cplx)((const cplx32 *)psi)[j] : ((const cplx *)psi)[j];
+#define DEFINE_APPLY_GATE(NAME, AMP)                                                            \
+static int NAME(int n, AMP *psi, const og_gate *g) {                                            \
+    int q = oracle_nqubits_of(g->kind);                                                         \
+    int tq[2] = {g->q0, g->q1};                                                                 \
+    double Ud[32];                                                                              \
+    if (oracle_gate_matrix(g->kind, g->adjoint, g->theta, g->phi, g->m, Ud) < 0) return -1;     \
+    for (int i = 0; i < q; ++i)                                                                 \
+        if (tq[i] < 0 || tq[i] >= n) return -2;                                                 \
+    if (q == 2 && tq[0] == tq[1]) return -3;                                                    \
+    int d = 1 << q;                                                                             \
+    cplx U[16];                                                                                 \
+    for (int i = 0; i < d * d; ++i) U[i] = Ud[2 * i] + Ud[2 * i + 1] * I;                       \
+    /* sorted target positions for zero-bit insertion */                                        \
+    int sorted[2] = {tq[0], tq[1]};                                                             \
+    if (q == 2 && sorted[0] > sorted[1]) { int t = sorted[0]; sorted[0] = sorted[1]; sorted[1] = t; } \
+    const int64_t nsets = (int64_t)1 << (n - q);                                                \
+    _Pragma("omp parallel for schedule(static)")                                                \
+    for (int64_t s = 0; s < nsets; ++s) {                                                       \
+        uint64_t base = (uint64_t)s;                                                            \
+        for (int i = 0; i < q; ++i) {       /* insert a 0 bit at sorted[i] */                   \
+            uint64_t lo = base & ((1ull << sorted[i]) - 1);                                     \
+            base = ((base >> sorted[i]) << (sorted[i] + 1)) | lo;                               \
+        }                                                                                       \
+        uint64_t idx[4];                                                                        \
+        cplx v[4];                                                                              \
+        for (int l = 0; l < d; ++l) {                                                           \
+            uint64_t j = base;                                                                  \
+            for (int i = 0; i < q; ++i)      /* first-listed qubit = MSB of l */                \
+                j |= (uint64_t)((l >> (q - 1 - i)) & 1) << tq[i];                               \
+            idx[l] = j;                                                                         \
+            v[l] = (cplx)psi[j];                                                                \
+        }                                                                                       \
+        for (int r = 0; r < d; ++r) {                                                           \
+            cplx acc = 0;                                                                       \
+            for (int c = 0; c < d; ++c) acc += U[r * d + c] * v[c];                             \
+            psi[idx[r]] = (AMP)acc;                                                             \
+        }                                                                                       \
+    }                                                                                           \
+    return 0;                                                                                   \
 }
-static inline void st_amp(void *psi, int c64, uint64_t j, cplx z) {
-    if (c64) ((cplx32 *)psi)[j] = (cplx32)z;
-    else ((cplx *)psi)[j] = z;
-}
-
-/* Apply one gate in place: PAPER.md L236-241 ("set id" iteration). */
-static int apply_gate(int n, void *psi, int c64, const og_gate *g) {
-    int q = oracle_nqubits_of(g->kind);
-    int tq[2] = {g->q0, g->q1};
-    double Ud[32];
-    if (oracle_gate_matrix(g->kind, g->adjoint, g->theta, g->phi, g->m, Ud) < 0) return -1;
-    for (int i = 0; i < q; ++i)
-        if (tq[i] < 0 || tq[i] >= n) return -2;
-    if (q == 2 && tq[0] == tq[1]) return -3;
-    int d = 1 << q;
-    cplx U[16];
-    for (int i = 0; i < d * d; ++i) U[i] = Ud[2 * i] + Ud[2 * i + 1] * I;
-    /* sorted target positions for zero-bit insertion */
-    int sorted[2] = {tq[0], tq[1]};
-    if (q == 2 && sorted[0] > sorted[1]) { int t = sorted[0]; sorted[0] = sorted[1]; sorted[1] = t; }
-    const int64_t nsets = (int64_t)1 << (n - q);
-#pragma omp parallel for schedule(static)
-    for (int64_t s = 0; s < nsets; ++s) {
-        uint64_t base = (uint64_t)s;
-        for (int i = 0; i < q; ++i) {       /* insert a 0 bit at sorted[i] */
-            uint64_t lo = base & ((1ull << sorted[i]) - 1);
-            base = ((base >> sorted[i]) << (sorted[i] + 1)) | lo;
-        }
-        uint64_t idx[4];
-        cplx v[4];
-        for (int l = 0; l < d; ++l) {
-            uint64_t j = base;
-            for (int i = 0; i < q; ++i)      /* first-listed qubit = MSB of l */
-                j |= (uint64_t)((l >> (q - 1 - i)) & 1) << tq[i];
-            idx[l] = j;
-            v[l] = ld_amp(psi, c64, j);
-        }
-        for (int r = 0; r < d; ++r) {
-            cplx acc = 0;
-            for (int c = 0; c < d; ++c) acc += U[r * d + c] * v[c];
-            st_amp(psi, c64, idx[r], acc);
-        }
-    }
-    return 0;
-}
+DEFINE_APPLY_GATE(apply_gate, cplx)
+DEFINE_APPLY_GATE(apply_gate_c64store, cplx32)
 
 /* psi <- U_G...U_1 psi.  Returns 0, or -(1+i) on a bad gate i. */
 int oracle_apply(int n, double *psi_ri, const og_gate *gates, int64_t ng, int nthreads) {
@@ -172,7 +168,7 @@ int oracle_apply(int n, double *psi_ri, const og_gate *gates, int64_t ng, int nt
     (void)nthreads;
 #endif
     for (int64_t i = 0; i < ng; ++i)
-        if (apply_gate(n, psi_ri, 0, &gates[i]) != 0) return (int)(-(1 + i));
+        if (apply_gate(n, (cplx *)psi_ri, &gates[i]) != 0) return (int)(-(1 + i));
     return 0;
 }
 
@@ -189,7 +185,7 @@ int oracle_run_c64store(int n, uint64_t x0, float *psi_ri, const og_gate *gates,
     memset(psi_ri, 0, sizeof(float) * 2 * N);
     psi_ri[2 * x0] = 1.0f;
     for (int64_t i = 0; i < ng; ++i)
-        if (apply_gate(n, psi_ri, 1, &gates[i]) != 0) return (int)(-(1 + i));
+        if (apply_gate_c64store(n, (cplx32 *)psi_ri, &gates[i]) != 0) return (int)(-(1 + i));
     return 0;
 }
 

@@ -421,6 +421,13 @@ def main():
                          f"{cpu_cores()} OpenMP threads, {t:.2f} s{note}; value = its state-update GB/s "
                          f"(each gate reads + writes the 16-B complex128 state)",
                "sec_per_circuit_extrapolated": t / ng * G * 2.0 ** (n - on)}
+        # the whole c1 circuit (n=16, 380 gates) on ONE host core, for scale
+        import oracle
+        from inputs import circuits as Cc
+        c1 = Cc.config(1)
+        t1 = time.perf_counter()
+        oracle.run(c1, nthreads=1)
+        cpu["c1_single_core_s"] = time.perf_counter() - t1
     remap = None
     if world > 1 or remap_bytes > 0:
         remap = {"bytes_per_rank_per_step": remap_bytes / max(1, args.steps), "ms_per_step": remap_ms / max(1, args.steps),

@@ -41,10 +41,10 @@ t0 = time.perf_counter()
 ref = oracle.run_c64store(circ)            # complex64 storage, 128 GiB
 t_or = time.perf_counter() - t0
 b = ref[y.astype(np.int64)].astype(np.complex128)
-onorm = float(np.vdot(ref[: 1 << 30], ref[: 1 << 30]).real)
-for k in range(1, 16):
-    blk = ref[k << 30:(k + 1) << 30]
-    onorm += float(np.vdot(blk, blk).real)
+onorm = 0.0   # float64 per 2^26-amplitude chunk (np.vdot of complex64 accumulates in single precision)
+for k in range(0, ref.size, 1 << 26):
+    blk = ref[k:k + (1 << 26)].view(np.float32).astype(np.float64)
+    onorm += float(np.dot(blk, blk))
 del ref
 gc.collect()
 a = a.astype(np.complex128)

@@ -1914,7 +1914,9 @@ static cudaError_t tc_launch(void *state, const uint8_t *dblob, uint32_t pass_of
     }
     uint64_t grid = (uint64_t)num_sms() * 2;
     if (grid > ntiles) grid = ntiles;
-    static const int dbg = getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0;
+    // STV_NO_HALFSYNC=1: a CTA barrier at every group boundary (A/B switch of the per-half barriers)
+    static const int dbg = (getenv("STV_TILE_DEBUG") ? atoi(getenv("STV_TILE_DEBUG")) : 0) |
+                           (getenv("STV_NO_HALFSYNC") ? 256 : 0);
     k_tc_group_pass<NS, FULL><<<(unsigned)grid, 256, smem, st>>>((float2 *)state, dblob, pass_off, ntiles, dbg, tm, tma,
                                                                  rp);
     return cudaGetLastError();

@@ -2073,6 +2073,7 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                 for (int j = 0; j < 4; ++j) g.tpos[j] = pos[j];
                 g.nvb = hd.S - STV_GROUP_BITS;
                 g.pair16 = (!c128 && pos[0] == 0) ? 1 : 0;
+                bool v7free = false;
                 std::vector<int> vp = vector_bit_order(pos, hd.S, c128);
                 if (!c128 && g.nvb >= 8 && hd.S == 12) {
                     // tensor-core block variant (tc_pass.cuh): the in-tile bit outside the group
@@ -2092,7 +2093,12 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         if (kv.second > bc) { best = kv.first; bc = kv.second; }
                     if (best >= 0) vp = vector_bit_order(pos, hd.S, c128, best);
                     auto it = std::find(vp.begin(), vp.end(), best);
-                    if (best >= 0 && it != vp.end() && it - vp.begin() >= 4) std::swap(*it, vp[7]);
+                    // (lane bits of a shared-memory phase: vector bits 0..2 for 16-B accesses, 0..3
+                    // for 8-B accesses; STV_V7_STRICT=1: 0..3 for both, the earlier rule)
+                    static const bool strict = getenv("STV_V7_STRICT") != nullptr;
+                    const int nlane = (g.pair16 && !strict) ? 3 : 4;
+                    if (best >= 0 && it != vp.end() && it - vp.begin() >= nlane) std::swap(*it, vp[7]);
+                    v7free = best < 0;   // no block variant: vector bit 7 is chosen after the loop
                 }
                 for (int v = 0; v < g.nvb; ++v) {
                     g.vbit[v][0] = 1u << vp[v];
@@ -2115,6 +2121,7 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                         put(tail, &w, 4);
                     }
                 }
+                g.pad = v7free ? 1 : 0;   // read by the vector-bit-7 pass below, then cleared
                 g.nflip_g = (int)gflips.size();
                 g.nflip_s = (int)sflips.size();
                 for (size_t q = 0; q < gflips.size(); ++q) g.flip[q] = gflips[q];
@@ -2163,6 +2170,57 @@ Encoded encode(const Plan &p, int n_local, bool c128, uint64_t rank_bits) {
                     for (int q = 0; q < G2.nflip_g; ++q) G1.flip[STV_MAX_FLIPS + G1.nflip_s++] = G2.flip[q];
                     for (int q = 0; q < G2.nflip_s; ++q) G1.flip[STV_MAX_FLIPS + G1.nflip_s++] = G2.flip[STV_MAX_FLIPS + q];
                     grecs.erase(grecs.begin() + (long)i);
+                }
+                // Vector bit 7 of the groups without a block variant: the tile position that the
+                // previous group maps to vector bit 7 if it is a V-bit here, else one the next group
+                // will share, with the lane bits re-chosen around it (vector_bit_order's `avoid`).  Thread t's half t >> 7 then holds
+                // the same amplitudes in both groups, and the tensor-core pass separates them with
+                // a per-half barrier instead of a CTA barrier (tc_pass.cuh hsync)
+                static const bool v7chain = !getenv("STV_NO_V7CHAIN");
+                for (size_t i = 0; i < grecs.size(); ++i) {
+                    StvGroup &G = grecs[i];
+                    const bool freeb = G.pad != 0;
+                    G.pad = 0;
+                    if (!freeb || !v7chain || c128 || hd.S != 12 || G.nvb != 8) continue;
+                    const std::vector<int> pos(G.tpos, G.tpos + 4);
+                    auto in = [](const StvGroup &X, int q) {
+                        for (int j = 0; j < 4; ++j)
+                            if (X.tpos[j] == q) return true;
+                        return false;
+                    };
+                    int want = -1;
+                    if (i) {
+                        const int q = __builtin_ctz(grecs[i - 1].vbit[7][0]);
+                        if (!in(G, q)) want = q;
+                    }
+                    if (want < 0 && i + 1 < grecs.size()) {
+                        const StvGroup &N = grecs[i + 1];
+                        if (!N.pad) {   // fixed: its vector bit 7
+                            const int q = __builtin_ctz(N.vbit[7][0]);
+                            if (!in(G, q)) want = q;
+                        } else {        // free as well: the highest position outside both groups
+                            for (int q = hd.S - 1; q >= 0 && want < 0; --q)
+                                if (!in(G, q) && !in(N, q)) want = q;
+                        }
+                    }
+                    if (want < 0) continue;
+                    std::vector<int> vp = vector_bit_order(pos, hd.S, c128, want);
+                    auto it = std::find(vp.begin(), vp.end(), want);
+                    // vector bits 0..2 (16-B accesses, pair16) or 0..3 (8-B accesses) are the
+                    // conflict-free lane bits of a shared-memory phase
+                    if (it == vp.end() || it - vp.begin() < (G.pair16 ? 3 : 4)) continue;
+                    std::swap(*it, vp[7]);
+                    for (int v = 0; v < 8; ++v) {
+                        G.vbit[v][0] = 1u << vp[v];
+                        G.vbit[v][1] = swz_amp(1u << vp[v], c128);
+                    }
+                    for (uint32_t t = 0; t < 256; ++t) {   // its per-thread vector bases
+                        uint32_t raw = 0, sw = 0;
+                        for (int v = 0; v < 8; ++v)
+                            if ((t >> v) & 1) { raw |= G.vbit[v][0]; sw ^= G.vbit[v][1]; }
+                        const uint32_t w = (sw & 0xffffu) | (raw << 16);
+                        std::memcpy(&tail[G.vtab_off + 4 * t], &w, 4);
+                    }
                 }
                 hd.nops = (int)grecs.size();
                 std::memcpy(&b[ops_at], grecs.data(), grecs.size() * sizeof(StvGroup));

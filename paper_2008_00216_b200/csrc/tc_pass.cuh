@@ -177,7 +177,7 @@ struct alignas(16) TcShared {
     uint64_t bar[2];
     uint64_t tbar[2];   // TMA tile loads, one per ring slot
     uint32_t tmem;
-    uint32_t pad;
+    uint32_t hsync;     // bit o: groups o and o + 1 split the tile into the same two halves
     uint64_t key[STV_TC_MAX_OPS];
     uint64_t cm[48];    // base xor-mask when the permuted ordinal's trailing-ones count is j
     uint32_t tm[48];    // ordinal xor-mask for the same carry
@@ -474,6 +474,23 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     }
     if (tid < STV_TC_MAX_OPS) sh->key[tid] = ~0ull;
     for (int e = tid; e < nops * 16; e += NT) sh->gso[e >> 4][e & 15] = groups[e >> 4].sw_off[e & 15] << 3;
+    if (tid == 64) {
+        // Group boundaries that need only a per-half barrier: thread t owns vector t, and its
+        // half t >> 7 is vector bit 7.  When groups o and o + 1 map vector bit 7 to the same
+        // tile position and no folded X flip moves amplitudes across it, each half of the CTA
+        // gathers in group o + 1 exactly the amplitudes it scattered in group o.
+        uint32_t m = 0;
+        if (FULL && !(dbg_flags & 256))
+            for (int o = 0; o + 1 < nops; ++o) {
+                const StvGroup &a = groups[o], &b = groups[o + 1];
+                const uint32_t s7 = a.vbit[7][1];
+                bool ok = a.nvb == 8 && b.nvb == 8 && a.vbit[7][0] == b.vbit[7][0];
+                for (int q = 0; q < a.nflip_s && ok; ++q) ok = (a.flip[STV_MAX_FLIPS + q] & 0xffffu) != s7;
+                for (int q = 0; q < b.nflip_g && ok; ++q) ok = (b.flip[q] & 0xffffu) != s7;
+                if (ok) m |= 1u << o;
+            }
+        sh->hsync = m;
+    }
     if (tid < 48) {   // carry masks of the permuted ordinal: bits 0..tid flip together
         uint64_t cm = 0;
         uint32_t tm = 0;
@@ -494,6 +511,7 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
     __syncthreads();
     tc_fence_after();
     uint32_t phase = 0;
+    const uint32_t hsync = sh->hsync;
     // this thread's TMEM row (lane 32 (warp % 4) + lane, block warp / 4); the CTA's base (warp-uniform)
     const uint32_t tmu = __shfl_sync(~0u, sh->tmem, 0);
     const uint32_t trow = tmu + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 96);
@@ -580,7 +598,10 @@ k_tc_group_pass(float2 *__restrict__ state, const uint8_t *__restrict__ blob, ui
                 if (o + 1 < nops) vw = __ldg((const uint32_t *)(grec + groups[o + 1].vtab_off) + tid);
                 tc_group<FULL>(slot * tile_elems * (uint32_t)esz, groups[o], P, steps, s0, mat, tables, full_base, tord, grec, scal, opsm, sh,
                                sh->gso[o], w, trow, phase, tid, dbg_flags);
-                __syncthreads();
+                if (FULL && ((hsync >> o) & 1u))   // (never set for the last group: the write-back needs all)
+                    asm volatile("bar.sync %0, 128;" ::"r"(1 + (tid >> 7)) : "memory");
+                else
+                    __syncthreads();
             }
         }
         if (!(dbg_flags & 2)) {

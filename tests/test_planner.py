@@ -421,17 +421,62 @@ def test_tc_step_plan_structure(case):
 @pytest.mark.parametrize("case", ["qft20", "rand20"])
 def test_auto_low_run_full_tile_blob_semantics(case):
     """Full 12-bit tiles at n = 20: the tensor-core step encoding, tile-base terms sunk to the
-    end of groups, and plan_auto's choice of the tile's low run (these circuits pick L = 5
-    over L = 4; an explicit low_bits is kept).  The exact device blob, emulated on CPU,
-    reproduces the oracle (complex64 bar 2e-6)."""
+    end of groups, and plan_auto's choice of the tile's low run L in {4, 5}: the automatic plan
+    is the explicit plan of the L it chose, and both that plan and the explicit plan of the
+    other L -- exact device blobs, emulated on CPU -- reproduce the oracle (complex64 bar 2e-6)."""
     circ = C.qft_circuit(20, tail=100, seed=3) if case == "qft20" else C.random_circuit(20, 300, 3)
     blob, offs = stv.plan_blob(circ.n, circ.gates)
-    Ls = [BE._at(blob, BE.Pass, po).L for po in offs]
-    assert 5 in Ls and 4 not in Ls[:1]
+    L0 = BE._at(blob, BE.Pass, offs[0]).L
+    assert L0 in (4, 5)
     assert any(BE._at(blob, BE.Pass, po).ntc for po in offs)
-    blob4, offs4 = stv.plan_blob(circ.n, circ.gates, low_bits=4)   # explicit: no automatic choice
-    assert bytes(blob4) != bytes(blob)
-    plan = stv.plan_json(circ.n, circ.gates)
-    psi = PI.logical(plan, BE.run(circ.n, blob, offs, x0=circ.x0, c128=False))
+    same, _ = stv.plan_blob(circ.n, circ.gates, low_bits=L0)
+    assert bytes(same) == bytes(blob)
+    other, offs_o = stv.plan_blob(circ.n, circ.gates, low_bits=9 - L0)   # explicit: no automatic choice
+    assert bytes(other) != bytes(blob)
     ref = oracle.run(circ)
-    assert np.max(np.abs(psi - ref)) < 2e-6
+    for bl, of, lb in ((blob, offs, None), (other, offs_o, 9 - L0)):
+        plan = stv.plan_json(circ.n, circ.gates, **({} if lb is None else dict(low_bits=lb)))
+        psi = PI.logical(plan, BE.run(circ.n, bl, of, x0=circ.x0, c128=False))
+        assert np.max(np.abs(psi - ref)) < 2e-6
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_vector_tables_and_half_local_boundaries(cfg):
+    """Full-tile complex64 plans of c2-c4: every group's per-thread vector table equals the
+    bases its vector bits define (the encoder re-chooses vector bit 7 after the groups are
+    built), and at every boundary the tensor-core pass separates with a per-half barrier
+    (same tile position at vector bit 7, no folded X flip across it; the kernel's hsync rule)
+    thread t's half t >> 7 scatters in group o exactly the amplitudes it gathers in group o+1."""
+    import struct
+    c = C.config(cfg)
+    blob, offs = stv.plan_blob(c.n, c.gates)
+    nhalf = 0
+    for po in offs:
+        P = BE._at(blob, BE.Pass, po)
+        if P.kind != 1 or not P.grouped or P.S != 12:
+            continue
+        gs = [BE._at(blob, BE.Group, po + P.ops_off + 256 * i) for i in range(P.nops)]
+        halves = []
+        for g in gs:
+            sets = [set(), set()]
+            for t in range(256):
+                raw = sw = 0
+                for v in range(8):
+                    if (t >> v) & 1:
+                        raw |= g.vbit[v][0]
+                        sw ^= g.vbit[v][1]
+                w = struct.unpack_from("<I", blob, po + g.vtab_off + 4 * t)[0]
+                assert w == (sw & 0xFFFF) | (raw << 16)
+                for l in range(16):
+                    sets[t >> 7].add(raw | sum(1 << g.tpos[k] for k in range(4) if (l >> k) & 1))
+            halves.append(sets)
+        for o in range(len(gs) - 1):
+            a, b = gs[o], gs[o + 1]
+            s7 = a.vbit[7][1]
+            ok = a.vbit[7][0] == b.vbit[7][0]
+            ok = ok and all((a.flip[8 + q] & 0xFFFF) != s7 for q in range(a.nflip_s))
+            ok = ok and all((b.flip[q] & 0xFFFF) != s7 for q in range(b.nflip_g))
+            if ok:
+                nhalf += 1
+                assert halves[o][0] == halves[o + 1][0] and halves[o][1] == halves[o + 1][1]
+    assert nhalf >= 3

@@ -395,8 +395,10 @@ def main():
         ee0.record(stream)
         for _ in range(args.e2e_steps):
             st.set_basis(0)
+            # no plan cache here: every e2e step plans its host gate list and copies the encoded
+            # plan to the device, as a first call on a new circuit does
             st.apply(circ.gates, kmax=args.kmax, tile_bits=args.tile_bits, low_bits=args.low_bits,
-                     budget=args.budget, flags=args.flags)
+                     budget=args.budget, flags=args.flags | stv.OPT_NO_PLAN_CACHE)
             if world == 1:
                 st.read_state(0, 1 << n, out=hv.ctypes.data)
         ee1.record(stream)
@@ -407,7 +409,8 @@ def main():
                "h2d_bytes_per_step": h2d if h2d is not None else 0,
                "d2h_bytes_per_step": (esz << n) if world == 1 else 0,
                "ms_per_step": ems,
-               "what": "host gate list -> sv_apply_circuit -> sv_read_state of all 2^n amplitudes into pinned host memory"}
+               "what": "host gate list -> sv_apply_circuit (planned from scratch, encoded plan copied H2D every step) "
+                       "-> sv_read_state of all 2^n amplitudes into pinned host memory"}
         del host
 
     if rank != 0:

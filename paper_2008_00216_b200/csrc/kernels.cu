@@ -1909,7 +1909,7 @@ static cudaError_t tc_launch(void *state, const uint8_t *dblob, uint32_t pass_of
                              const CUtensorMap &tm, const TcTma &tma, const RecParam &rp, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_tc_group_pass<NS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+        cudaFuncSetAttribute(k_tc_group_pass<NS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, STV_TC_SMEM_CAP);
         attr = true;
     }
     uint64_t grid = (uint64_t)num_sms() * 2;
@@ -1929,7 +1929,7 @@ cudaError_t launch_tc_group_pass(void *state, const uint8_t *dblob, const uint8_
     const size_t fixed = kTcShBytes + (size_t)ntcop * kTcOpBytes + 512 + (((size_t)tab_entries * 8 + 127u) & ~(size_t)127);
     const size_t tile = (size_t)8 << S;
     const uint64_t ntiles = 1ull << (n_local - S);
-    const size_t cap = 113 * 1024;   // 2 CTAs per SM
+    const size_t cap = STV_TC_SMEM_CAP;   // 2 CTAs per SM (the encoder checks the same bound)
     if (fixed + tile > cap || (ntiles >> 32) || rec_bytes > STV_REC_PARAM_BYTES) return cudaErrorInvalidValue;
     static thread_local RecParam rp;
     std::memcpy(rp.b, hrec, rec_bytes);

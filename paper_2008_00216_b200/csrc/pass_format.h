@@ -99,6 +99,11 @@ struct alignas(16) StvPass {
 #define STV_TC_MAX_OPS 12
 #define STV_TC_MAX_STEPS 64
 #define STV_TC_MAX_GROUPS 16
+// shared memory of the tensor-core pass (tc_pass.cuh): TcShared region | tile ring (1 or 2
+// tiles) | operator slots | 512 B of scalars | phase tables; 113 KB per CTA keeps 2 CTAs per SM
+#define STV_TC_SH_BYTES 2048
+#define STV_TC_OP_BYTES 8192
+#define STV_TC_SMEM_CAP (113 * 1024)
 struct alignas(16) StvTcStep {
     int16_t kind, last, first, n;
     int32_t op, group;

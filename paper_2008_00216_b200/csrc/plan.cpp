@@ -1758,6 +1758,16 @@ static void encode_tc_steps(std::vector<uint8_t> &b, size_t at, StvPass &hd, con
     // block variants cost operator slots (2 per step); measured on c2/c4 they pay even where
     // the extra slots push a pass to the single-buffered tile ring
     build(true);
+    // the operator slots share the CTA's shared memory with one tile and the phase tables
+    // (launch_tc_group_pass): a pass whose block variants do not fit drops them, and runs on
+    // the FMA group pass if its operators still do not fit
+    auto fits = [&](int slots) {
+        return (size_t)STV_TC_SH_BYTES + (size_t)slots * STV_TC_OP_BYTES + 512 +
+                   (((size_t)hd.tab_entries * 8 + 127u) & ~(size_t)127) + ((size_t)8 << hd.S) <=
+               (size_t)STV_TC_SMEM_CAP;
+    };
+    if (nop > 0 && nop <= STV_TC_MAX_OPS && !fits(nop)) build(false);
+    if (nop > 0 && !fits(nop)) return;   // FMA group pass
     const int nord = __builtin_popcountll(hd.out_mask);
     const size_t need = st.size() * sizeof(StvTcStep) + 16;
     if (nop == 0 || nop > STV_TC_MAX_OPS || st.size() > STV_TC_MAX_STEPS || nord > 48 ||

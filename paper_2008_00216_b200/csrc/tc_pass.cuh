@@ -99,7 +99,7 @@ constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) <
 __device__ __forceinline__ uint32_t tc_bt_off(int n, int k) {
     return (uint32_t)((n & 7) * 16 + (k & 3) * 4 + (k >> 2) * 128 + (n >> 3) * 1024);
 }
-constexpr uint32_t kTcOpBytes = 8192;   // hi (4 KB) + lo (4 KB)
+constexpr uint32_t kTcOpBytes = STV_TC_OP_BYTES;   // hi (4 KB) + lo (4 KB)
 constexpr uint32_t kTcCols = 256;       // TMEM columns per CTA: 2 blocks x (A_hi 32, A_lo 32, D 32), rounded up
 
 // Build the operator of M step st into its slot: lane j < 16 runs the step's sub-ops on e_j.
@@ -183,7 +183,7 @@ struct alignas(16) TcShared {
     uint32_t tm[48];    // ordinal xor-mask for the same carry
     alignas(16) uint32_t gso[STV_TC_MAX_GROUPS][16];   // per group: swizzled register offsets in bytes
 };
-constexpr uint32_t kTcShBytes = 2048;   // TcShared region at the start of shared memory (1024-multiple)
+constexpr uint32_t kTcShBytes = STV_TC_SH_BYTES;   // TcShared region at the start of shared memory (1024-multiple)
 static_assert(sizeof(TcShared) <= kTcShBytes, "TcShared exceeds its region");
 
 // the dynamic shared memory of k_tc_group_pass (same storage as its `smem`)

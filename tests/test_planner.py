@@ -480,3 +480,36 @@ def test_vector_tables_and_half_local_boundaries(cfg):
                 nhalf += 1
                 assert halves[o][0] == halves[o + 1][0] and halves[o][1] == halves[o + 1][1]
     assert nhalf >= 3
+
+
+def _tc_pass_launch_needs(n, gates, **kw):
+    """(shared-memory bytes, record bytes, operator slots) of every tensor-core pass of a plan,
+    as `launch_tc_group_pass` (kernels.cu) sizes them from the pass header."""
+    blob, offs = stv.plan_blob(n, gates, **kw)
+    out = []
+    for po in offs:
+        P = BE._at(blob, BE.Pass, po)
+        if P.kind != 1 or not P.grouped or P.ntc == 0:
+            continue
+        smem = 2048 + P.ntcop * 8192 + 512 + ((P.tab_entries * 8 + 127) & ~127) + (8 << P.S)
+        out.append((smem, P.rec_bytes, P.ntcop))
+    return out
+
+
+@pytest.mark.parametrize("case", [("rand", 20, 43, dict(kmax=1)), ("rand", 20, 43, dict(kmax=2)),
+                                  ("rand", 20, 43, dict(kmax=3)), ("rand", 20, 43, dict()),
+                                  ("rand", 21, 12, dict(kmax=2)), ("rand", 22, 10, dict(kmax=3)),
+                                  ("rand", 20, 7, dict(low_bits=5)), ("rand", 22, 5, dict(budget=400)),
+                                  ("cfg", 2, 0, dict()), ("cfg", 2, 0, dict(kmax=2)), ("cfg", 2, 0, dict(kmax=3)),
+                                  ("cfg", 3, 0, dict()), ("cfg", 4, 0, dict()), ("cfg", 4, 0, dict(kmax=3))])
+def test_tc_passes_fit_the_launch_limits(case):
+    """Every pass the encoder marks for the tensor-core kernel fits what its launch checks:
+    113 KB of shared memory (one tile + operator slots + tables; 2 CTAs per SM), the 24 KB
+    kernel-parameter record and 12 operator slots.  (kmax = 2, 3 at n = 20 once encoded 10
+    and 11 slots, 118 and 126 KB, and the launch failed with `invalid argument`.)"""
+    kind, a, seed, kw = case
+    c = C.random_circuit(a, 300, seed) if kind == "rand" else C.config(a)
+    needs = _tc_pass_launch_needs(c.n, c.gates, **kw)
+    assert needs, "no tensor-core pass in a full-tile complex64 plan"
+    for smem, rec, slots in needs:
+        assert smem <= 113 * 1024 and rec <= 24576 and 1 <= slots <= 12, (smem, rec, slots)

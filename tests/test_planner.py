@@ -483,7 +483,7 @@ def test_vector_tables_and_half_local_boundaries(cfg):
 
 
 def _tc_pass_launch_needs(n, gates, **kw):
-    """(shared-memory bytes, record bytes, operator slots) of every tensor-core pass of a plan,
+    """(shared-memory bytes, kernel-parameter bytes, operator slots) of every tensor-core pass of a plan,
     as `launch_tc_group_pass` (kernels.cu) sizes them from the pass header."""
     blob, offs = stv.plan_blob(n, gates, **kw)
     out = []
@@ -492,7 +492,7 @@ def _tc_pass_launch_needs(n, gates, **kw):
         if P.kind != 1 or not P.grouped or P.ntc == 0:
             continue
         smem = 2048 + P.ntcop * 8192 + 512 + ((P.tab_entries * 8 + 127) & ~127) + (8 << P.S)
-        out.append((smem, P.rec_bytes, P.ntcop))
+        out.append((smem, P.param_bytes, P.ntcop))
     return out
 
 
@@ -505,7 +505,7 @@ def _tc_pass_launch_needs(n, gates, **kw):
 def test_tc_passes_fit_the_launch_limits(case):
     """Every pass the encoder marks for the tensor-core kernel fits what its launch checks:
     113 KB of shared memory (one tile + operator slots + tables; 2 CTAs per SM), the 24 KB
-    kernel-parameter record and 12 operator slots.  (kmax = 2, 3 at n = 20 once encoded 10
+    kernel-parameter part of the record and 12 operator slots.  (kmax = 2, 3 at n = 20 once encoded 10
     and 11 slots, 118 and 126 KB, and the launch failed with `invalid argument`.)"""
     kind, a, seed, kw = case
     c = C.random_circuit(a, 300, seed) if kind == "rand" else C.config(a)

@@ -1,7 +1,7 @@
 """GPU fuzz (not part of the test suite): seeded circuits at n = 20..24 -- full 12-bit tiles, so
 complex64 runs on the tensor-core pass -- with planner options, dtype and virtual shards drawn
 per case, each compared element-wise with the CPU oracle (bars of tests/test_gpu_parity.py).
-    python tools/gpu_fuzz.py [seconds=480] [out.jsonl]
+    python tools/gpu_fuzz.py [seconds=480] [out.jsonl] [nmin=20] [nmax=24]
 Prints one JSON line per case and a summary; exit code 1 if any case fails."""
 import json
 import os
@@ -16,19 +16,21 @@ from inputs.circuits import SplitMix64  # noqa: E402
 
 budget_s = float(sys.argv[1]) if len(sys.argv) > 1 else 480.0
 out = open(sys.argv[2], "w") if len(sys.argv) > 2 else None
+nmin = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+nmax = int(sys.argv[4]) if len(sys.argv) > 4 else 24
 OPTS = [dict(), dict(), dict(kmax=1), dict(kmax=2), dict(kmax=3), dict(low_bits=5), dict(low_bits=6),
         dict(low_bits=7), dict(budget=400), dict(budget=3000), dict(flags=2), dict(flags=4), dict(flags=16),
         dict(flags=128), dict(flags=0x400), dict(flags=0x800), dict(tile_bits=11), dict(tile_bits=13),
         dict(kmax=2, low_bits=5), dict(kmax=3, budget=400), dict(kmax=2, flags=0x800)]
 KINDS = [None, None, ["h", "cz", "t", "x", "cnot"], ["u1", "fsim"], ["u2", "cphase", "h"], ["cnot", "x", "cz", "t", "h"]]
 TOL = {"c64": 2e-6, "c128": 1e-12}
-rng = SplitMix64(20260101)
+rng = SplitMix64(20260101 + 1000 * nmin + nmax)
 t0 = time.time()
 ncase = nfail = 0
 while time.time() - t0 < budget_s:
-    n = 20 + rng.u(5)
+    n = nmin + rng.u(nmax - nmin + 1)
     shape = rng.u(4)
-    seed = 1000 + ncase
+    seed = 1000 * (nmin - 19) + ncase
     if shape == 0:
         circ = C.qft_circuit(n, 60 + rng.u(100), seed, "fz")
     elif shape == 1:

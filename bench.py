@@ -463,6 +463,12 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    # a plan may mix the two group-pass kernels (c3: one of its 7 passes has no operator step)
+    tile_per_circuit = sum(v for k, v in kinds["n_pass"].items() if k.startswith("tile"))
+    n_fma = tile_per_circuit - kinds.get("n_tc_pass", 0)   # both are counted once per pass, not per shard
+    if line["roofline"] and used_tc and n_fma > 0:
+        line["roofline"]["kernel"] += " + %d of %d passes per circuit on k_group_pass (CUDA-core FMA)" % (
+            n_fma, tile_per_circuit)
     print(json.dumps(line), flush=True)
     st.close()
 

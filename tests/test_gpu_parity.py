@@ -331,3 +331,34 @@ def test_tma_staged_tc_pass_parity(stv, cfg):
     a, st = run_gpu(stv, circ, "c64", flags=stv.OPT_TMA)
     assert st["n_tc_pass"] > 0
     assert_parity(a, ref, "c64")
+
+
+_FUZZ_OPTS = [dict(), dict(kmax=1), dict(kmax=2), dict(kmax=3), dict(low_bits=5), dict(low_bits=6), dict(budget=400),
+              dict(flags=2), dict(flags=16), dict(flags=128), dict(flags=0x400), dict(flags=0x800), dict(tile_bits=11),
+              dict(tile_bits=13), dict(kmax=2, low_bits=5), dict(kmax=3, budget=400), dict(kmax=2, flags=0x800)]
+_FUZZ_KINDS = [None, ["h", "cz", "t", "x", "cnot"], ["u1", "fsim"], ["u2", "cphase", "h"], ["cnot", "x", "cz", "t", "h"]]
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_seeded_fuzz_full_tiles(stv, case):
+    """Seeded draws of (circuit shape, planner options, dtype, virtual shards) at n = 20..22, where
+    complex64 plans have full 12-bit tiles (tensor-core pass): the combinations the fixed option
+    lists above do not enumerate (`tools/gpu_fuzz.py` is the long-running form of this test)."""
+    rng = C.SplitMix64(77000 + case)
+    n = 20 + rng.u(3)
+    shape = rng.u(3)
+    if shape == 0:
+        circ = C.qft_circuit(n, 40 + rng.u(80), 500 + case, "fz")
+    elif shape == 1 and n % 4 == 0:
+        circ = C.grid_circuit("fz", 4, n // 4, 0, 6 + rng.u(6), "fsim" if rng.u(2) else "cz", 500 + case)
+    else:
+        circ = C.random_circuit(n, 150 + rng.u(250), 500 + case, _FUZZ_KINDS[rng.u(len(_FUZZ_KINDS))])
+    kw = _FUZZ_OPTS[rng.u(len(_FUZZ_OPTS))]
+    dtype = "c128" if rng.u(4) == 0 else "c64"
+    g = (0, 0, 1, 2, 3)[rng.u(5)]
+    st = stv.State(circ.n, dtype, virtual_g=g) if g else stv.State(circ.n, dtype)
+    st.set_basis(circ.x0)
+    st.apply(circ.gates, **kw)
+    psi = st.amplitudes()
+    st.close()
+    assert_parity(psi, oracle.run(circ), dtype)
